@@ -1,0 +1,138 @@
+/* usp_attn.h — C ABI of the B200-native USP attention forward engine.
+ *
+ * Drop-in for the hot path of the reference `uspsim`
+ * (/root/reference/proj): the SP attention forward
+ *   usp::usp_attention<T>(RankCtx&, const ProcessMesh&, q, k, v,
+ *                         positions, causal)      src/usp/usp_attention.hpp:41-47
+ * with its ulysses_degree x ring_degree process grid (src/simcomm/mesh.hpp:14-34),
+ * zigzag/contiguous sequence layout (src/usp/partition.hpp:19-53) and
+ * Q/K/V/O/LSE tensor conventions (src/numerics/tensor.hpp:19-75,
+ * src/numerics/attention.hpp:90-92). Conventions mirror the reference's
+ * own C ABI (include/uspsim.h): same status numbering, opaque handles,
+ * explicit destroy, thread-local last error, no exceptions across the ABI.
+ *
+ * Tensor conventions (all row-major, device memory, caller-owned):
+ *   q   bf16 (batch, T, heads,    head_size)  sequence-sharded, T = L/(U*R),
+ *   k,v bf16 (batch, T, kv_heads, head_size)  rows in usp_positions_for() order
+ *   o   bf16 (batch, T, heads,    head_size)  same rows / order as q
+ *   lse fp32 (batch, L/R, heads/U)            natural log, HEAD-sharded, rows in
+ *                                             usp_head_positions() order
+ *   GQA: query head h reads kv head h / (heads / kv_heads).
+ */
+#ifndef USP_ATTN_H
+#define USP_ATTN_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define USP_API __attribute__((visibility("default")))
+#else
+#define USP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Same numbering as uspsim_status (include/uspsim.h:26-31). */
+typedef enum usp_status {
+  USP_OK = 0,
+  USP_TOLERANCE_EXCEEDED = 1,
+  USP_INVALID_INPUT = 2,
+  USP_INTERNAL_ERROR = 3,
+} usp_status;
+
+/* The forward's static configuration. Replaces the (ProcessMesh, shapes,
+ * causal) arguments of usp_attention (usp_attention.hpp:41-47) and the
+ * simulate parameters (src/api/commands.cpp:189-215). */
+typedef struct usp_config {
+  int32_t ulysses_degree; /* U: ProcessMesh(ulysses, ring), mesh.hpp:16      */
+  int32_t ring_degree;    /* R                                                */
+  int32_t rank;           /* global rank, = ring_coord*U + ulysses_coord      */
+  int32_t device;         /* CUDA device ordinal of this rank                 */
+  int64_t batch;
+  int64_t seq_len;        /* global L                                         */
+  int32_t heads;          /* hc                                               */
+  int32_t kv_heads;       /* kv_hc (GQA)                                      */
+  int32_t head_size;      /* hs (<= 128; 64/128 run natively, others padded)  */
+  int32_t causal;         /* zigzag layout iff causal (commands.cpp:88)       */
+} usp_config;
+
+typedef struct usp_comm usp_comm;     /* transport between the mesh's ranks */
+typedef struct usp_engine usp_engine; /* one rank's forward engine          */
+
+/* ---- layout & validation (host only, no device work) ------------------- */
+
+/* ShardSpec + check_usp_inputs rules (partition.cpp:78-92,
+ * usp_attention.cpp:15-38) with the reference's messages. */
+USP_API usp_status usp_config_validate(const usp_config* cfg);
+/* zigzag_partition (partition.cpp:12-33): out[R * (L/R)]. */
+USP_API usp_status usp_zigzag_partition(int64_t seq_len, int32_t ring, int64_t* out);
+/* ShardSpec::positions_for (partition.cpp:95-105): out[T]. */
+USP_API usp_status usp_positions_for(const usp_config* cfg, int32_t rank, int64_t* out);
+/* gather_positions result over the Ulysses group (all_to_all_4d.cpp:128-132),
+ * i.e. the rows of the head-sharded O/LSE: out[L/R]. */
+USP_API usp_status usp_head_positions(const usp_config* cfg, int32_t rank, int64_t* out);
+/* causal_pair_counts (partition.cpp:52-72) of the ring assignment. */
+USP_API usp_status usp_causal_pair_counts(const int64_t* assignment, int32_t ring, int64_t seq_len,
+                                  int64_t* counts);
+
+/* Per-ring-step schedule of one rank: the ring source block and the tile
+ * plan the kernel will run (host logic behind usp_attn_fwd). */
+typedef struct usp_step_info {
+  int32_t step, src_ring_coord, send_to_rank, recv_from_rank;
+  int64_t full_tiles, partial_tiles, work_units, visible_pairs;
+  int64_t ring_bytes_sent; /* K+V bytes shifted after this step (0 on the last) */
+} usp_step_info;
+USP_API usp_status usp_schedule(const usp_config* cfg, int32_t step, usp_step_info* out);
+/* The step's tile plan itself (CSR over 128-row query tiles): sizes[0] =
+ * query tiles, sizes[1] = list entries; tile_off[sizes[0]+1] and
+ * tile_list[sizes[1]] (k tile | partial << 31) are filled when non-NULL. */
+USP_API usp_status usp_step_plan(const usp_config* cfg, int32_t step, int64_t sizes[2],
+                                 int32_t* tile_off, int32_t* tile_list);
+/* Algorithmic FLOPs of this rank's forward: 4 * batch * (heads/U) *
+ * head_size * visible (q,k) pairs. */
+USP_API usp_status usp_rank_flops(const usp_config* cfg, double* flops);
+
+/* ---- transports ---------------------------------------------------------- */
+
+/* NCCL over NVLink/NVSwitch, one process per GPU. All ranks pass the same
+ * 128-byte ncclUniqueId produced by usp_nccl_unique_id on one rank. */
+USP_API usp_status usp_nccl_unique_id(uint8_t out[128]);
+USP_API usp_status usp_comm_create_nccl(const uint8_t unique_id[128], int32_t world_size,
+                                int32_t rank, int32_t device, usp_comm** out);
+/* In-process transport: one host thread per rank, CUDA peer copies between
+ * the ranks' buffers (the analogue of simcomm::World::run, world.hpp:217-236).
+ * One handle is shared by all ranks of the world; ranks may share a device. */
+USP_API usp_status usp_comm_create_local(int32_t world_size, usp_comm** out);
+USP_API void usp_comm_destroy(usp_comm* comm);
+
+/* ---- engine -------------------------------------------------------------- */
+
+/* comm may be NULL when U*R == 1. Allocates all workspace up front. */
+USP_API usp_status usp_engine_create(const usp_config* cfg, usp_comm* comm, usp_engine** out);
+/* Collective over the mesh: every rank calls it with matching shapes, in
+ * the same order. Asynchronous on `stream` (a cudaStream_t; NULL = legacy
+ * default stream). */
+USP_API usp_status usp_attn_fwd(usp_engine* engine, const void* q, const void* k, const void* v,
+                        void* o, float* lse, void* stream);
+/* Launches of the engine's own kernels in the last usp_attn_fwd. */
+USP_API int32_t usp_engine_last_launches(const usp_engine* engine);
+USP_API void usp_engine_destroy(usp_engine* engine);
+
+/* Runs usp_attn_fwd on every rank of a local world, one host thread per
+ * rank (engines[i] must belong to rank i); blocks until all are issued. */
+USP_API usp_status usp_local_world_fwd(usp_engine* const* engines, int32_t world_size,
+                               const void* const* q, const void* const* k,
+                               const void* const* v, void* const* o, float* const* lse,
+                               void* const* streams);
+
+/* ---- diagnostics --------------------------------------------------------- */
+USP_API const char* usp_last_error(void);
+USP_API const char* usp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* USP_ATTN_H */

@@ -1,0 +1,125 @@
+"""ctypes binding of libusp_b200.so (the C ABI in include/usp_attn.h).
+
+There is no fallback: if the native library is missing and cannot be built
+(no nvcc), importing the engine raises. The library is built in-tree by
+build.py so it travels with the repository snapshot.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libusp_b200.so")
+
+USP_OK, USP_TOLERANCE_EXCEEDED, USP_INVALID_INPUT, USP_INTERNAL_ERROR = 0, 1, 2, 3
+
+
+class UspError(RuntimeError):
+    """A non-OK usp_status; ``status`` mirrors uspsim_status numbering."""
+
+    def __init__(self, status: int, message: str):
+        super().__init__(message)
+        self.status = status
+
+
+class UspInvalidInput(UspError, ValueError):
+    pass
+
+
+class UspConfig(ctypes.Structure):
+    _fields_ = [
+        ("ulysses_degree", ctypes.c_int32),
+        ("ring_degree", ctypes.c_int32),
+        ("rank", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+        ("batch", ctypes.c_int64),
+        ("seq_len", ctypes.c_int64),
+        ("heads", ctypes.c_int32),
+        ("kv_heads", ctypes.c_int32),
+        ("head_size", ctypes.c_int32),
+        ("causal", ctypes.c_int32),
+    ]
+
+
+class UspStepInfo(ctypes.Structure):
+    _fields_ = [
+        ("step", ctypes.c_int32),
+        ("src_ring_coord", ctypes.c_int32),
+        ("send_to_rank", ctypes.c_int32),
+        ("recv_from_rank", ctypes.c_int32),
+        ("full_tiles", ctypes.c_int64),
+        ("partial_tiles", ctypes.c_int64),
+        ("work_units", ctypes.c_int64),
+        ("visible_pairs", ctypes.c_int64),
+        ("ring_bytes_sent", ctypes.c_int64),
+    ]
+
+
+# Every symbol include/usp_attn.h declares (tests check the .so exports them).
+EXPORTS = [
+    "usp_config_validate", "usp_zigzag_partition", "usp_positions_for", "usp_head_positions",
+    "usp_causal_pair_counts", "usp_schedule", "usp_step_plan", "usp_rank_flops", "usp_nccl_unique_id",
+    "usp_comm_create_nccl", "usp_comm_create_local", "usp_comm_destroy", "usp_engine_create",
+    "usp_attn_fwd", "usp_engine_last_launches", "usp_engine_destroy", "usp_local_world_fwd",
+    "usp_last_error", "usp_version",
+]
+
+_lib = None
+_lock = threading.Lock()
+
+
+def _declare(lib):
+    P = ctypes.POINTER
+    vp = ctypes.c_void_p
+    st = ctypes.c_int
+    i64p = P(ctypes.c_int64)
+    sig = {
+        "usp_config_validate": (st, [P(UspConfig)]),
+        "usp_zigzag_partition": (st, [ctypes.c_int64, ctypes.c_int32, i64p]),
+        "usp_positions_for": (st, [P(UspConfig), ctypes.c_int32, i64p]),
+        "usp_head_positions": (st, [P(UspConfig), ctypes.c_int32, i64p]),
+        "usp_causal_pair_counts": (st, [i64p, ctypes.c_int32, ctypes.c_int64, i64p]),
+        "usp_schedule": (st, [P(UspConfig), ctypes.c_int32, P(UspStepInfo)]),
+        "usp_step_plan": (st, [P(UspConfig), ctypes.c_int32, i64p, P(ctypes.c_int32), P(ctypes.c_int32)]),
+        "usp_rank_flops": (st, [P(UspConfig), P(ctypes.c_double)]),
+        "usp_nccl_unique_id": (st, [ctypes.c_char_p]),
+        "usp_comm_create_nccl": (st, [ctypes.c_char_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P(vp)]),
+        "usp_comm_create_local": (st, [ctypes.c_int32, P(vp)]),
+        "usp_comm_destroy": (None, [vp]),
+        "usp_engine_create": (st, [P(UspConfig), vp, P(vp)]),
+        "usp_attn_fwd": (st, [vp, vp, vp, vp, vp, vp, vp]),
+        "usp_engine_last_launches": (ctypes.c_int32, [vp]),
+        "usp_engine_destroy": (None, [vp]),
+        "usp_local_world_fwd": (st, [P(vp), ctypes.c_int32, P(vp), P(vp), P(vp), P(vp), P(vp), P(vp)]),
+        "usp_last_error": (ctypes.c_char_p, []),
+        "usp_version": (ctypes.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+
+
+def lib():
+    """Loads (building first if needed) libusp_b200.so."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                from . import build as _build  # nvcc is required: no CPU fallback
+
+                _build.build()
+            _lib = ctypes.CDLL(LIB_PATH)
+            _declare(_lib)
+    return _lib
+
+
+def check(status: int) -> None:
+    if status == USP_OK:
+        return
+    msg = lib().usp_last_error().decode()
+    if status == USP_INVALID_INPUT:
+        raise UspInvalidInput(status, msg)
+    raise UspError(status, msg)

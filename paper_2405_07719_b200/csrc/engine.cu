@@ -1,0 +1,703 @@
+// engine.cu — one rank's USP attention forward and the C ABI (include/usp_attn.h).
+//
+// usp_attn_fwd is the B200 restatement of usp::usp_attention<T>
+// (reference src/usp/usp_attention.cpp:43-65), i.e. the paper's Algorithm 1:
+//   1. Ulysses all-to-all of Q, K, V, sequence-sharded -> head-sharded
+//      (all_to_all_4d(.,2,1), usp_attention.cpp:54-56): pack transposes
+//      (reshard.cu) + ONE grouped exchange for all three tensors;
+//   2. ring attention over the ring group (ring_attention.cpp:45-76): R
+//      launches of the tcgen05 attention kernel, step t on the K/V block of
+//      ring source (r - t) mod R, while K/V for step t+1 are shifted on a
+//      side stream into the other half of a double buffer; the online-softmax
+//      merge across steps is fused into the kernel epilogue;
+//   3. the inverse all-to-all for O (all_to_all_4d(.,1,2), :63).
+// The per-rank position all_gathers of the reference (usp_attention.cpp:53,
+// ring_attention.cpp:56) are not needed: the layout is static, so every
+// rank computes all positions on the host (plan.cpp).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/usp_attn.h"
+#include "fa_fwd.hpp"
+#include "plan.hpp"
+#include "reshard.hpp"
+#include "transport.hpp"
+
+namespace uspb200 {
+
+cudaError_t launch_fa_fwd(const FwdParams& p, int nq, int hs, int grid, cudaStream_t stream);
+
+#define USPB_CHECK(x)                                                                      \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      throw Error(ErrorCode::kInternal, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// ------------------------------------------------------------ tensor maps
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  if (!fn) throw Error(ErrorCode::kInternal, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  return fn;
+}
+
+// (hs, heads, seq, batch) bf16 tensor; box = one 128-row x 64-column block
+// of one head, 128-byte swizzled to match the UMMA SW128 descriptors.
+static CUtensorMap make_tmap(const void* base, int64_t hs, int64_t heads, int64_t seq,
+                             int64_t batch) {
+  CUtensorMap m;
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(hs), static_cast<cuuint64_t>(heads),
+                              static_cast<cuuint64_t>(seq), static_cast<cuuint64_t>(batch)};
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(hs * 2),
+                                 static_cast<cuuint64_t>(heads * hs * 2),
+                                 static_cast<cuuint64_t>(seq * heads * hs * 2)};
+  const cuuint32_t box[4] = {64, 1, static_cast<cuuint32_t>(kTileM), 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base),
+                                 dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    std::ostringstream os;
+    os << "cuTensorMapEncodeTiled failed (" << int(r) << "); base " << base
+       << " must be 16-byte aligned";
+    throw Error(ErrorCode::kInvalidArgument, os.str());
+  }
+  return m;
+}
+
+// ------------------------------------------------------------ device memory
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t n) : bytes(n) {
+    if (n) USPB_CHECK(cudaMalloc(&p, n));
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    std::swap(p, o.p);
+    std::swap(bytes, o.bytes);
+    return *this;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+template <class T>
+static DevBuf upload(const std::vector<T>& v) {
+  DevBuf b(std::max<size_t>(v.size() * sizeof(T), 16));
+  if (!v.empty()) USPB_CHECK(cudaMemcpy(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return b;
+}
+
+struct DevStep {
+  StepPlan host;
+  DevBuf q_pos, k_pos, tile_off, tile_list, units;
+  EpiMode mode = EpiMode::kSingle;
+};
+
+// ------------------------------------------------------------------ Engine
+class Engine {
+ public:
+  Engine(const usp_config& c, Transport* tr) : cfg_(c), tr_(tr) {
+    shape_ = to_shape(c);
+    shape_.validate();
+    const int world = shape_.mesh.world();
+    if (c.rank < 0 || c.rank >= world) throw_invalid("rank outside the mesh");
+    if (world > 1 && !tr_) throw_invalid("a transport (usp_comm) is required when U*R > 1");
+    if (tr_ && tr_->world_size() != world) throw_invalid("transport world size does not match U*R");
+    U_ = shape_.mesh.ulysses;
+    R_ = shape_.mesh.ring;
+    u_ = shape_.mesh.ulysses_coord(c.rank);
+    r_ = shape_.mesh.ring_coord(c.rank);
+    B_ = shape_.batch;
+    T_ = shape_.tokens_per_rank();
+    Tr_ = shape_.tokens_per_ring_rank();
+    H_ = shape_.heads;
+    KV_ = shape_.kv_heads;
+    hl_ = shape_.local_heads();
+    kvl_ = shape_.local_kv_heads();
+    hs_ = shape_.head_size;
+    hsk_ = shape_.kernel_head_size();
+    const int group = hl_ / kvl_;
+    nq_ = (group % 2 == 0) ? 2 : 1;
+
+    USPB_CHECK(cudaSetDevice(c.device));
+    USPB_CHECK(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, c.device));
+    if (tr_) groups_ = tr_->make_groups(c.rank, shape_.mesh.ulysses_group(c.rank),
+                                        shape_.mesh.ring_group(c.rank));
+
+    const size_t e = 2;  // bf16
+    const bool reshape = U_ > 1 || hs_ != hsk_;
+    q_part_ = size_t(B_) * T_ * hl_ * hsk_ * e;
+    kv_part_ = size_t(B_) * T_ * kvl_ * hsk_ * e;
+    const size_t q_heads = size_t(B_) * Tr_ * hl_ * hsk_ * e;
+    const size_t kv_heads = size_t(B_) * Tr_ * kvl_ * hsk_ * e;
+    kv_bytes_ = kv_heads;
+    if (reshape) {
+      q_h_ = DevBuf(q_heads);
+      kv0_ = DevBuf(2 * kv_heads);
+      o_h_ = DevBuf(q_heads);
+    }
+    if (U_ > 1) {
+      send_ = DevBuf(U_ * (q_part_ + 2 * kv_part_));
+      if (B_ > 1) recv_ = DevBuf(U_ * (q_part_ + 2 * kv_part_));
+      o_recv_ = DevBuf(U_ * q_part_);
+      if (B_ > 1) o_send_ = DevBuf(U_ * q_part_);
+    }
+    if (R_ > 1) {
+      kv_ring_[0] = DevBuf(2 * kv_heads);
+      if (R_ > 2) kv_ring_[1] = DevBuf(2 * kv_heads);
+      o_acc_ = DevBuf(size_t(B_) * Tr_ * hl_ * hsk_ * sizeof(float));
+      lse_acc_ = DevBuf(size_t(B_) * Tr_ * hl_ * sizeof(float));
+      USPB_CHECK(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking));
+      for (int t = 0; t < R_; ++t) {
+        cudaEvent_t a, b;
+        USPB_CHECK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+        USPB_CHECK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+        ev_pre_.push_back(a);
+        ev_recv_.push_back(b);
+      }
+    }
+
+    // Static layout -> per-step tile plans (the reference all_gathers these
+    // positions at run time; here they are known at create).
+    const auto my_pos = head_positions(shape_, c.rank);
+    for (int t = 0; t < R_; ++t) {
+      const int src = ring_source(r_, t, R_);
+      const auto k_pos = head_positions(shape_, shape_.mesh.rank_of(u_, src));
+      DevStep st;
+      st.mode = R_ == 1 ? EpiMode::kSingle
+                        : (t == 0 ? EpiMode::kFirst : (t == R_ - 1 ? EpiMode::kLast : EpiMode::kMiddle));
+      const bool include_empty = st.mode != EpiMode::kMiddle;
+      st.host = plan_step(my_pos, k_pos, shape_.causal, B_, hl_ / nq_, include_empty);
+      st.q_pos = upload(st.host.q_pos);
+      st.k_pos = upload(st.host.k_pos);
+      st.tile_off = upload(st.host.tile_off);
+      st.tile_list = upload(st.host.tile_list);
+      st.units = upload(st.host.units);
+      steps_.push_back(std::move(st));
+    }
+  }
+
+  ~Engine() {
+    for (auto e : ev_pre_) cudaEventDestroy(e);
+    for (auto e : ev_recv_) cudaEventDestroy(e);
+    if (comm_stream_) cudaStreamDestroy(comm_stream_);
+  }
+
+  static UspShape to_shape(const usp_config& c) {
+    UspShape s;
+    s.mesh.ulysses = c.ulysses_degree;
+    s.mesh.ring = c.ring_degree;
+    s.batch = c.batch;
+    s.seq_len = c.seq_len;
+    s.heads = c.heads;
+    s.kv_heads = c.kv_heads;
+    s.head_size = c.head_size;
+    s.causal = c.causal != 0;
+    return s;
+  }
+
+  int last_launches() const { return launches_; }
+
+  void fwd(const void* q, const void* k, const void* v, void* o, float* lse, cudaStream_t st) {
+    USPB_CHECK(cudaSetDevice(cfg_.device));
+    for (const void* ptr : {q, k, v, static_cast<const void*>(o), static_cast<const void*>(lse)})
+      if (!ptr || reinterpret_cast<uintptr_t>(ptr) % 16 != 0)
+        throw_invalid("q, k, v, o, lse must be non-null 16-byte aligned device pointers");
+    launches_ = 0;
+    const size_t e = 2;
+    const bool reshape = U_ > 1 || hs_ != hsk_;
+    const void* qh = q;
+    const void* kh = k;
+    const void* vh = v;
+    uint8_t* kv0 = kv0_.as<uint8_t>();
+    if (U_ > 1) {
+      // -- 1. Ulysses in: pack (b,T,H,hs) -> [peer][b][T][H/U][hsk], one exchange
+      uint8_t* sq = send_.as<uint8_t>();
+      uint8_t* sk = sq + U_ * q_part_;
+      uint8_t* sv = sk + U_ * kv_part_;
+      pack_heads(q, sq, H_, hl_, st);
+      pack_heads(k, sk, KV_, kvl_, st);
+      pack_heads(v, sv, KV_, kvl_, st);
+      uint8_t* rq = B_ > 1 ? recv_.as<uint8_t>() : nullptr;
+      uint8_t* rk = rq ? rq + U_ * q_part_ : nullptr;
+      uint8_t* rv = rk ? rk + U_ * kv_part_ : nullptr;
+      std::vector<std::vector<A2APart>> parts(3, std::vector<A2APart>(U_));
+      for (int p = 0; p < U_; ++p) {
+        // bs == 1: part p is exactly rows [p*T, (p+1)*T) of the head-sharded
+        // tensor, so it is received in place (no unpack kernel).
+        parts[0][p] = {sq + p * q_part_, rq ? rq + p * q_part_ : q_h_.as<uint8_t>() + p * q_part_};
+        parts[1][p] = {sk + p * kv_part_, rk ? rk + p * kv_part_ : kv0 + p * kv_part_};
+        parts[2][p] = {sv + p * kv_part_, rv ? rv + p * kv_part_ : kv0 + kv_bytes_ + p * kv_part_};
+      }
+      tr_->all_to_all(*groups_, parts, {q_part_, kv_part_, kv_part_}, st);
+      if (B_ > 1) {
+        gather_seq(rq, q_h_.p, hl_, st);
+        gather_seq(rk, kv0, kvl_, st);
+        gather_seq(rv, kv0 + kv_bytes_, kvl_, st);
+      }
+      qh = q_h_.p;
+      kh = kv0;
+      vh = kv0 + kv_bytes_;
+    } else if (reshape) {
+      pad_rows(q, q_h_.p, B_ * T_ * H_, st);
+      pad_rows(k, kv0, B_ * T_ * KV_, st);
+      pad_rows(v, kv0 + kv_bytes_, B_ * T_ * KV_, st);
+      qh = q_h_.p;
+      kh = kv0;
+      vh = kv0 + kv_bytes_;
+    }
+
+    // -- 2. ring: R kernel launches, K/V shifted one step ahead on comm_stream_
+    void* o_heads = reshape ? o_h_.p : o;
+    const CUtensorMap tm_q = make_tmap(qh, hsk_, hl_, Tr_, B_);
+    auto kbuf = [&](int t) -> const void* {
+      if (t == 0) return kh;
+      return kv_ring_[(t - 1) & 1].p;
+    };
+    auto vbuf = [&](int t) -> const void* {
+      if (t == 0) return vh;
+      return kv_ring_[(t - 1) & 1].as<uint8_t>() + kv_bytes_;
+    };
+    for (int t = 0; t < R_; ++t) {
+      if (t + 1 < R_) {
+        USPB_CHECK(cudaEventRecord(ev_pre_[t], st));  // buf(t) ready, buf(t+1) free
+        USPB_CHECK(cudaStreamWaitEvent(comm_stream_, ev_pre_[t], 0));
+        tr_->ring_shift(*groups_, {kbuf(t), vbuf(t)},
+                        {const_cast<void*>(kbuf(t + 1)), const_cast<void*>(vbuf(t + 1))},
+                        {kv_bytes_, kv_bytes_}, comm_stream_);
+        USPB_CHECK(cudaEventRecord(ev_recv_[t], comm_stream_));
+      }
+      if (t > 0) USPB_CHECK(cudaStreamWaitEvent(st, ev_recv_[t - 1], 0));
+      launch_step(t, tm_q, kbuf(t), vbuf(t), o_heads, lse, st);
+    }
+
+    // -- 3. Ulysses out: [peer][b][T][H/U] -> (b, T, H, hs)
+    if (U_ > 1) {
+      uint8_t* osend = o_h_.as<uint8_t>();
+      if (B_ > 1) {
+        split_seq(o_h_.p, o_send_.p, st);
+        osend = o_send_.as<uint8_t>();
+      }
+      std::vector<std::vector<A2APart>> parts(1, std::vector<A2APart>(U_));
+      for (int p = 0; p < U_; ++p)
+        parts[0][p] = {osend + p * q_part_, o_recv_.as<uint8_t>() + p * q_part_};
+      tr_->all_to_all(*groups_, parts, {q_part_}, st);
+      unpack_heads(o_recv_.p, o, st);
+    } else if (reshape) {
+      RowPermute rp;
+      rp.src = o_h_.p;
+      rp.dst = o;
+      rp.dims[3] = B_ * T_ * H_;
+      rp.src_stride[3] = rp.dst_stride[3] = 1;
+      rp.hs_src = hsk_;
+      rp.hs_dst = hs_;
+      permute(rp, st);
+    }
+    (void)e;
+  }
+
+  double rank_flops() const {
+    double pairs = 0;
+    for (const auto& s : steps_) pairs += double(s.host.visible_pairs);
+    return 4.0 * double(B_) * hl_ * hs_ * pairs;
+  }
+
+ private:
+  void permute(const RowPermute& rp, cudaStream_t st) {
+    USPB_CHECK(launch_row_permute(rp, num_sms_, st));
+    ++launches_;
+  }
+  // (b, T, heads, hs) -> [peer][b][T][heads/U][hsk]
+  void pack_heads(const void* src, void* dst, int heads, int local, cudaStream_t st) {
+    RowPermute rp;
+    rp.src = src;
+    rp.dst = dst;
+    rp.dims[0] = U_;
+    rp.dims[1] = B_;
+    rp.dims[2] = T_;
+    rp.dims[3] = local;
+    rp.src_stride[0] = local;
+    rp.src_stride[1] = T_ * heads;
+    rp.src_stride[2] = heads;
+    rp.src_stride[3] = 1;
+    rp.dst_stride[0] = B_ * T_ * local;
+    rp.dst_stride[1] = T_ * local;
+    rp.dst_stride[2] = local;
+    rp.dst_stride[3] = 1;
+    rp.hs_src = hs_;
+    rp.hs_dst = hsk_;
+    permute(rp, st);
+  }
+  // [src][b][T][local] -> (b, U*T, local)   (bs > 1 receive placement)
+  void gather_seq(const void* src, void* dst, int local, cudaStream_t st) {
+    RowPermute rp;
+    rp.src = src;
+    rp.dst = dst;
+    rp.dims[0] = U_;
+    rp.dims[1] = B_;
+    rp.dims[2] = T_;
+    rp.dims[3] = local;
+    rp.src_stride[0] = B_ * T_ * local;
+    rp.src_stride[1] = T_ * local;
+    rp.src_stride[2] = local;
+    rp.src_stride[3] = 1;
+    rp.dst_stride[0] = T_ * local;
+    rp.dst_stride[1] = Tr_ * local;
+    rp.dst_stride[2] = local;
+    rp.dst_stride[3] = 1;
+    rp.hs_src = rp.hs_dst = hsk_;
+    permute(rp, st);
+  }
+  // (b, U*T, hl) -> [dst][b][T][hl]   (bs > 1 send staging for O)
+  void split_seq(const void* src, void* dst, cudaStream_t st) {
+    RowPermute rp;
+    rp.src = src;
+    rp.dst = dst;
+    rp.dims[0] = U_;
+    rp.dims[1] = B_;
+    rp.dims[2] = T_;
+    rp.dims[3] = hl_;
+    rp.src_stride[0] = T_ * hl_;
+    rp.src_stride[1] = Tr_ * hl_;
+    rp.src_stride[2] = hl_;
+    rp.src_stride[3] = 1;
+    rp.dst_stride[0] = B_ * T_ * hl_;
+    rp.dst_stride[1] = T_ * hl_;
+    rp.dst_stride[2] = hl_;
+    rp.dst_stride[3] = 1;
+    rp.hs_src = rp.hs_dst = hsk_;
+    permute(rp, st);
+  }
+  // [src][b][T][hl][hsk] -> (b, T, H, hs), heads [src*hl, (src+1)*hl)
+  void unpack_heads(const void* src, void* dst, cudaStream_t st) {
+    RowPermute rp;
+    rp.src = src;
+    rp.dst = dst;
+    rp.dims[0] = U_;
+    rp.dims[1] = B_;
+    rp.dims[2] = T_;
+    rp.dims[3] = hl_;
+    rp.src_stride[0] = B_ * T_ * hl_;
+    rp.src_stride[1] = T_ * hl_;
+    rp.src_stride[2] = hl_;
+    rp.src_stride[3] = 1;
+    rp.dst_stride[0] = hl_;
+    rp.dst_stride[1] = T_ * H_;
+    rp.dst_stride[2] = H_;
+    rp.dst_stride[3] = 1;
+    rp.hs_src = hsk_;
+    rp.hs_dst = hs_;
+    permute(rp, st);
+  }
+  void pad_rows(const void* src, void* dst, int64_t rows, cudaStream_t st) {
+    RowPermute rp;
+    rp.src = src;
+    rp.dst = dst;
+    rp.dims[3] = rows;
+    rp.src_stride[3] = rp.dst_stride[3] = 1;
+    rp.hs_src = hs_;
+    rp.hs_dst = hsk_;
+    permute(rp, st);
+  }
+
+  void launch_step(int t, const CUtensorMap& tm_q, const void* kb, const void* vb, void* o_heads,
+                   float* lse, cudaStream_t st) {
+    const DevStep& s = steps_[t];
+    if (s.host.units.empty()) return;
+    FwdParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.tm_q = tm_q;
+    p.tm_k = make_tmap(kb, hsk_, kvl_, Tr_, B_);
+    p.tm_v = make_tmap(vb, hsk_, kvl_, Tr_, B_);
+    p.o = o_heads;
+    p.lse = lse;
+    p.o_acc = o_acc_.as<float>();
+    p.lse_acc = lse_acc_.as<float>();
+    p.units = s.units.as<uint32_t>();
+    p.tile_off = s.tile_off.as<int32_t>();
+    p.tile_list = s.tile_list.as<int32_t>();
+    p.q_pos = s.q_pos.as<int32_t>();
+    p.k_pos = s.k_pos.as<int32_t>();
+    p.num_units = static_cast<int>(s.host.units.size());
+    p.batch = static_cast<int>(B_);
+    p.q_len = static_cast<int>(Tr_);
+    p.k_len = static_cast<int>(Tr_);
+    p.heads = hl_;
+    p.kv_heads = kvl_;
+    p.mode = static_cast<int>(s.mode);
+    p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(double(hs_)));
+    const int reserve = (R_ > 1 && tr_) ? tr_->reserved_sms() : 0;
+    const int slots = std::max(1, num_sms_ - reserve);
+    const int grid = std::min(p.num_units, slots);
+    USPB_CHECK(launch_fa_fwd(p, nq_, hsk_, grid, st));
+    ++launches_;
+  }
+
+  usp_config cfg_;
+  Transport* tr_;
+  std::shared_ptr<Groups> groups_;
+  UspShape shape_;
+  int U_ = 1, R_ = 1, u_ = 0, r_ = 0, H_ = 0, KV_ = 0, hl_ = 0, kvl_ = 0, hs_ = 0, hsk_ = 0, nq_ = 1;
+  int64_t B_ = 1, T_ = 0, Tr_ = 0;
+  int num_sms_ = 148;
+  size_t q_part_ = 0, kv_part_ = 0, kv_bytes_ = 0;
+  DevBuf q_h_, kv0_, o_h_, send_, recv_, o_send_, o_recv_, o_acc_, lse_acc_;
+  DevBuf kv_ring_[2];
+  std::vector<DevStep> steps_;
+  cudaStream_t comm_stream_ = nullptr;
+  std::vector<cudaEvent_t> ev_pre_, ev_recv_;
+  int launches_ = 0;
+};
+
+}  // namespace uspb200
+
+// =================================================================== C ABI
+using namespace uspb200;
+
+struct usp_comm {
+  std::unique_ptr<Transport> impl;
+};
+struct usp_engine {
+  std::unique_ptr<Engine> impl;
+};
+
+namespace {
+thread_local std::string g_last_error;
+
+template <class F>
+usp_status guarded(F&& f) {
+  try {
+    f();
+    return USP_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return (e.code() == ErrorCode::kInvalidArgument || e.code() == ErrorCode::kConstraint)
+               ? USP_INVALID_INPUT
+               : USP_INTERNAL_ERROR;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "out of memory";
+    return USP_INTERNAL_ERROR;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return USP_INTERNAL_ERROR;
+  }
+}
+
+UspShape shape_of(const usp_config* cfg) {
+  if (!cfg) throw_invalid("config is null");
+  return Engine::to_shape(*cfg);
+}
+}  // namespace
+
+extern "C" {
+
+usp_status usp_config_validate(const usp_config* cfg) {
+  return guarded([&] { shape_of(cfg).validate(); });
+}
+
+usp_status usp_zigzag_partition(int64_t seq_len, int32_t ring, int64_t* out) {
+  return guarded([&] {
+    const auto v = zigzag_partition(seq_len, ring);
+    std::memcpy(out, v.data(), v.size() * sizeof(int64_t));
+  });
+}
+
+usp_status usp_positions_for(const usp_config* cfg, int32_t rank, int64_t* out) {
+  return guarded([&] {
+    const UspShape s = shape_of(cfg);
+    s.validate();
+    const auto v = positions_for(s, rank);
+    std::memcpy(out, v.data(), v.size() * sizeof(int64_t));
+  });
+}
+
+usp_status usp_head_positions(const usp_config* cfg, int32_t rank, int64_t* out) {
+  return guarded([&] {
+    const UspShape s = shape_of(cfg);
+    s.validate();
+    const auto v = head_positions(s, rank);
+    std::memcpy(out, v.data(), v.size() * sizeof(int64_t));
+  });
+}
+
+usp_status usp_causal_pair_counts(const int64_t* assignment, int32_t ring, int64_t seq_len,
+                                  int64_t* counts) {
+  return guarded([&] {
+    if (ring < 1 || seq_len % ring != 0) throw_invalid("assignment must cover 0..L-1 exactly once");
+    std::vector<int64_t> flat(assignment, assignment + seq_len);
+    const auto c = causal_pair_counts(flat, ring, seq_len);
+    std::memcpy(counts, c.data(), c.size() * sizeof(int64_t));
+  });
+}
+
+usp_status usp_schedule(const usp_config* cfg, int32_t step, usp_step_info* out) {
+  return guarded([&] {
+    const UspShape s = shape_of(cfg);
+    s.validate();
+    if (step < 0 || step >= s.mesh.ring) throw_invalid("step outside [0, ring_degree)");
+    const int u = s.mesh.ulysses_coord(cfg->rank), r = s.mesh.ring_coord(cfg->rank);
+    const int R = s.mesh.ring;
+    const int src = ring_source(r, step, R);
+    const int hl = s.local_heads(), kvl = s.local_kv_heads();
+    const int nq = ((hl / kvl) % 2 == 0) ? 2 : 1;
+    const auto st = plan_step(head_positions(s, cfg->rank),
+                              head_positions(s, s.mesh.rank_of(u, src)), s.causal, s.batch,
+                              hl / nq, R == 1 || step == 0 || step == R - 1);
+    out->step = step;
+    out->src_ring_coord = src;
+    out->send_to_rank = s.mesh.rank_of(u, (r + 1) % R);
+    out->recv_from_rank = s.mesh.rank_of(u, (r - 1 + R) % R);
+    out->full_tiles = st.full_tiles;
+    out->partial_tiles = st.partial_tiles;
+    out->work_units = static_cast<int64_t>(st.units.size());
+    out->visible_pairs = st.visible_pairs;
+    out->ring_bytes_sent =
+        step + 1 < R ? 2 * s.batch * s.tokens_per_ring_rank() * kvl * int64_t(s.head_size) * 2 : 0;
+  });
+}
+
+usp_status usp_step_plan(const usp_config* cfg, int32_t step, int64_t sizes[2], int32_t* tile_off,
+                         int32_t* tile_list) {
+  return guarded([&] {
+    const UspShape s = shape_of(cfg);
+    s.validate();
+    if (step < 0 || step >= s.mesh.ring) throw_invalid("step outside [0, ring_degree)");
+    const int u = s.mesh.ulysses_coord(cfg->rank), r = s.mesh.ring_coord(cfg->rank);
+    const int src = ring_source(r, step, s.mesh.ring);
+    const auto st = plan_step(head_positions(s, cfg->rank), head_positions(s, s.mesh.rank_of(u, src)),
+                              s.causal, s.batch, 1, true);
+    sizes[0] = st.n_q_tiles;
+    sizes[1] = static_cast<int64_t>(st.tile_list.size());
+    if (tile_off) std::memcpy(tile_off, st.tile_off.data(), st.tile_off.size() * sizeof(int32_t));
+    if (tile_list) std::memcpy(tile_list, st.tile_list.data(), st.tile_list.size() * sizeof(int32_t));
+  });
+}
+
+usp_status usp_rank_flops(const usp_config* cfg, double* flops) {
+  return guarded([&] {
+    const UspShape s = shape_of(cfg);
+    s.validate();
+    const int u = s.mesh.ulysses_coord(cfg->rank), r = s.mesh.ring_coord(cfg->rank);
+    const auto mine = head_positions(s, cfg->rank);
+    double pairs = 0;
+    for (int t = 0; t < s.mesh.ring; ++t)
+      pairs += double(visible_pairs(
+          mine, head_positions(s, s.mesh.rank_of(u, ring_source(r, t, s.mesh.ring))), s.causal));
+    *flops = 4.0 * double(s.batch) * s.local_heads() * s.head_size * pairs;
+  });
+}
+
+usp_status usp_nccl_unique_id(uint8_t out[128]) {
+  return guarded([&] { nccl_unique_id(out); });
+}
+
+usp_status usp_comm_create_nccl(const uint8_t unique_id[128], int32_t world_size, int32_t rank,
+                                int32_t device, usp_comm** out) {
+  if (!out) return USP_INVALID_INPUT;
+  *out = nullptr;
+  return guarded([&] {
+    auto c = std::make_unique<usp_comm>();
+    c->impl = make_nccl_transport(unique_id, world_size, rank, device);
+    *out = c.release();
+  });
+}
+
+usp_status usp_comm_create_local(int32_t world_size, usp_comm** out) {
+  if (!out) return USP_INVALID_INPUT;
+  *out = nullptr;
+  return guarded([&] {
+    auto c = std::make_unique<usp_comm>();
+    c->impl = make_local_transport(world_size);
+    *out = c.release();
+  });
+}
+
+void usp_comm_destroy(usp_comm* comm) { delete comm; }
+
+usp_status usp_engine_create(const usp_config* cfg, usp_comm* comm, usp_engine** out) {
+  if (!out) return USP_INVALID_INPUT;
+  *out = nullptr;
+  return guarded([&] {
+    if (!cfg) throw_invalid("config is null");
+    auto e = std::make_unique<usp_engine>();
+    e->impl = std::make_unique<Engine>(*cfg, comm ? comm->impl.get() : nullptr);
+    *out = e.release();
+  });
+}
+
+usp_status usp_attn_fwd(usp_engine* engine, const void* q, const void* k, const void* v, void* o,
+                        float* lse, void* stream) {
+  return guarded([&] {
+    if (!engine) throw_invalid("engine is null");
+    engine->impl->fwd(q, k, v, o, lse, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int32_t usp_engine_last_launches(const usp_engine* engine) {
+  return engine ? engine->impl->last_launches() : 0;
+}
+
+void usp_engine_destroy(usp_engine* engine) { delete engine; }
+
+usp_status usp_local_world_fwd(usp_engine* const* engines, int32_t world_size,
+                               const void* const* q, const void* const* k, const void* const* v,
+                               void* const* o, float* const* lse, void* const* streams) {
+  std::vector<usp_status> rc(world_size, USP_OK);
+  std::vector<std::string> err(world_size);
+  std::vector<std::thread> th;
+  for (int i = 0; i < world_size; ++i) {
+    th.emplace_back([&, i] {
+      rc[i] = usp_attn_fwd(engines[i], q[i], k[i], v[i], o[i], lse[i],
+                           streams ? streams[i] : nullptr);
+      if (rc[i] != USP_OK) err[i] = g_last_error;
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int i = 0; i < world_size; ++i)
+    if (rc[i] != USP_OK) {
+      g_last_error = "rank " + std::to_string(i) + ": " + err[i];
+      return rc[i];
+    }
+  return USP_OK;
+}
+
+const char* usp_last_error(void) { return g_last_error.c_str(); }
+
+const char* usp_version(void) { return "0.1.0-b200"; }
+
+}  // extern "C"

@@ -1,0 +1,51 @@
+// fa_fwd.hpp — host/device contract of the per-block attention kernel.
+//
+// One launch folds one K/V block (one ring step) into the attention state
+// of every (batch, q-head, 128-row query tile) of this rank:
+//   SoftmaxState::update  (reference src/numerics/attention.cpp:181-230)
+//   finalize + logsumexp  (attention.cpp:232-264)
+//   ring-step LSE merge   (the online-softmax fold across the R steps of
+//                          src/usp/ring_attention.cpp:62-75)
+// The causal mask is the reference BlockMask::causal (attention.hpp:32-34):
+// key j is hidden from query i iff k_pos[j] > q_pos[i]. Tile classification
+// (full / partial / skipped) is done on the host by plan.cpp.
+#pragma once
+
+#include <cuda.h>
+#include <cstdint>
+
+namespace uspb200 {
+
+constexpr int kTileM = 128;  // query rows per tile (TMEM lanes)
+constexpr int kTileN = 128;  // keys per K/V tile
+
+enum class EpiMode : int {
+  kSingle = 0,  // only step: write bf16 O + natural-log LSE
+  kFirst = 1,   // first of several steps: write fp32 (O, lse2) running state
+  kMiddle = 2,  // merge into the running state
+  kLast = 3,    // merge, then write bf16 O + natural-log LSE
+};
+
+struct FwdParams {
+  CUtensorMap tm_q;  // (hs, heads, q_len, batch) bf16, box (64, 1, 128, 1), SW128
+  CUtensorMap tm_k;  // (hs, kv_heads, k_len, batch)
+  CUtensorMap tm_v;
+
+  void* o;            // bf16 (batch, q_len, heads, hs)  [kSingle, kLast]
+  float* lse;         // fp32 (batch, q_len, heads), natural log [kSingle, kLast]
+  float* o_acc;       // fp32 running O (batch, q_len, heads, hs) [kFirst..kLast]
+  float* lse_acc;     // fp32 running LSE, log2 domain           [kFirst..kLast]
+
+  const uint32_t* units;     // packed work units: q_tile | hp << 16 | b << 24
+  const int32_t* tile_off;   // CSR row offsets per q tile (n_q_tiles + 1)
+  const int32_t* tile_list;  // k tile index | partial << 31
+  const int32_t* q_pos;      // effective query positions, padded to 128
+  const int32_t* k_pos;      // effective key positions, padded to 128 (INT_MAX)
+
+  int num_units;
+  int batch, q_len, k_len, heads, kv_heads;
+  int mode;          // EpiMode
+  float scale_log2;  // log2(e) / sqrt(head_size)
+};
+
+}  // namespace uspb200

@@ -1,0 +1,423 @@
+// fa_fwd_sm100.cu — per-block flash-attention forward for sm_100a.
+//
+// The B200 restatement of SoftmaxState::update / finalize / logsumexp
+// (reference src/numerics/attention.cpp:181-264), one launch per ring step
+// (src/usp/ring_attention.cpp:62-75). Design:
+//
+//   * persistent CTAs, one per SM, walking a host-built LPT-ordered list of
+//     work units (batch, q-head pair, 128-row query tile);
+//   * warp-specialised: 1 TMA producer warp, 1 MMA-issuer warp (one elected
+//     thread issues every tcgen05.mma), 4*NQ softmax warps (one TMEM lane =
+//     one query row per thread);
+//   * NQ = 2 query tiles per CTA = two q heads of the same GQA group over the
+//     same rows, so every K/V tile staged in shared memory feeds both, and
+//     the tensor core alternates between the tiles while the other's
+//     softmax runs (S_A/P_A, S_B/P_B, O_A, O_B fill the 512 TMEM columns);
+//   * S = Q K^T: tcgen05.mma SS (Q, K from 128B-swizzled smem via TMA) into
+//     TMEM; P = exp2(S*scale*log2e - m) is written back over S as bf16 and
+//     O += P V runs as a TS MMA (P from TMEM, V MN-major from smem);
+//   * O is rescaled lazily: the running max only moves when it grows by more
+//     than 2^8, so the TMEM read-modify-write of O is rare;
+//   * the epilogue normalises, merges into the fp32 ring-step running state
+//     (log-sum-exp merge) and/or writes bf16 O + natural-log LSE.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "fa_fwd.hpp"
+#include "ptx_sm100.cuh"
+
+namespace uspb200 {
+
+using namespace ptx;
+
+template <int NQ, int HS>
+struct FwdCfg {
+  static constexpr int kSoftmaxWarps = 4 * NQ;
+  static constexpr int kTmaWarp = kSoftmaxWarps;
+  static constexpr int kMmaWarp = kSoftmaxWarps + 1;
+  static constexpr int kThreads = 32 * (kSoftmaxWarps + 2);
+  static constexpr int kSub = HS / 64;           // 128-byte (64 x bf16) column blocks
+  static constexpr int kSubBytes = 128 * 128;    // one block: 128 rows x 128 B
+  static constexpr int kQBytes = kTileM * HS * 2;
+  static constexpr int kKVBytes = kTileN * HS * 2;
+  static constexpr int kBudget = 227 * 1024 - 2048;
+  static constexpr int kStagesFit = (kBudget - NQ * kQBytes) / kKVBytes;
+  static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
+  static constexpr int kNumBars = 3 * NQ + 1 + NQ + 2 * kStages;
+  static constexpr int kSmemBytes = 1024 /*align slack*/ + NQ * kQBytes + kStages * kKVBytes +
+                                    kNumBars * 8 + 16;
+  static constexpr uint32_t kColsUsed = NQ * 128 + NQ * HS;
+  static constexpr uint32_t kTmemCols = kColsUsed <= 128 ? 128 : (kColsUsed <= 256 ? 256 : 512);
+  static constexpr uint32_t kSCol = 0;          // S_t / P_t at t*128
+  static constexpr uint32_t kOCol = NQ * 128;   // O_t at kOCol + t*HS
+  static_assert(HS == 64 || HS == 128, "head_size must be 64 or 128 on the tcgen05 path");
+  static_assert(kStages >= 2, "not enough shared memory for a K/V pipeline");
+};
+
+template <int NQ, int HS>
+__global__ void __launch_bounds__(FwdCfg<NQ, HS>::kThreads, 1)
+    fa_fwd_sm100_kernel(const __grid_constant__ FwdParams p) {
+  using C = FwdCfg<NQ, HS>;
+  constexpr int NS = C::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sKV = smem + NQ * C::kQBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + NS * C::kKVBytes);
+  uint64_t* q_full = bars;              // [NQ]  TMA -> MMA
+  uint64_t* q_empty = q_full + NQ;      // [1]   MMA -> TMA
+  uint64_t* kv_full = q_empty + 1;      // [NS]  TMA -> MMA
+  uint64_t* kv_empty = kv_full + NS;    // [NS]  MMA -> TMA
+  uint64_t* s_full = kv_empty + NS;     // [NQ]  MMA -> softmax
+  uint64_t* p_ready = s_full + NQ;      // [NQ]  softmax -> MMA (128 arrivals)
+  uint64_t* o_full = p_ready + NQ;      // [NQ]  MMA -> epilogue
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + NQ);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int t = 0; t < NQ; ++t) {
+      mbar_init(&q_full[t], 1);
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_ready[t], 128);
+      mbar_init(&o_full[t], 1);
+    }
+    mbar_init(q_empty, 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == C::kMmaWarp) tmem_alloc(tmem_slot, C::kTmemCols);
+  if (warp == C::kTmaWarp && lane == 0) {
+    tma_prefetch_desc(&p.tm_q);
+    tma_prefetch_desc(&p.tm_k);
+    tma_prefetch_desc(&p.tm_v);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int group = p.heads / p.kv_heads;  // q heads per kv head (GQA)
+
+  if (warp < C::kSoftmaxWarps) {
+    // ------------------------------------------------------------ softmax
+    const int t = warp >> 2;
+    const int quarter = warp & 3;
+    const int row_in_tile = quarter * 32 + lane;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+    const uint32_t s_addr = lane_base + C::kSCol + t * 128;
+    const uint32_t o_addr = lane_base + C::kOCol + t * HS;
+    const float sl2 = p.scale_log2;
+    uint32_t s_phase = 0, o_phase = 0;
+    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+      const uint32_t unit = p.units[u];
+      const int qt = unit & 0xFFFF, hp = (unit >> 16) & 0xFF, b = unit >> 24;
+      const int h = hp * NQ + t;
+      const int beg = p.tile_off[qt];
+      const int n = p.tile_off[qt + 1] - beg;
+      const int q_row = qt * kTileM + row_in_tile;
+      const int qpos = p.q_pos[q_row];
+      float m_run = -INFINITY, l_run = 0.f, m_use = 0.f;
+      for (int j = 0; j < n; ++j) {
+        const int entry = p.tile_list[beg + j];
+        mbar_wait(&s_full[t], s_phase & 1);
+        ++s_phase;
+        tc_fence_after();
+        uint32_t s[128];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld32(s_addr + c * 32, s + c * 32);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld_wait(s + c * 32);
+        if (entry < 0) {  // partial tile: apply the position mask per element
+          const int kt = entry & 0x7FFFFFFF;
+          const int4* kp4 = reinterpret_cast<const int4*>(p.k_pos + kt * kTileN);
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const int4 kp = __ldg(kp4 + c);
+            if (kp.x > qpos) s[4 * c + 0] = __float_as_uint(-INFINITY);
+            if (kp.y > qpos) s[4 * c + 1] = __float_as_uint(-INFINITY);
+            if (kp.z > qpos) s[4 * c + 2] = __float_as_uint(-INFINITY);
+            if (kp.w > qpos) s[4 * c + 3] = __float_as_uint(-INFINITY);
+          }
+        }
+        float mx0 = __uint_as_float(s[0]), mx1 = __uint_as_float(s[1]);
+        float mx2 = __uint_as_float(s[2]), mx3 = __uint_as_float(s[3]);
+#pragma unroll
+        for (int i = 4; i < 128; i += 4) {
+          mx0 = fmaxf(mx0, __uint_as_float(s[i + 0]));
+          mx1 = fmaxf(mx1, __uint_as_float(s[i + 1]));
+          mx2 = fmaxf(mx2, __uint_as_float(s[i + 2]));
+          mx3 = fmaxf(mx3, __uint_as_float(s[i + 3]));
+        }
+        const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+        const float m_new = fmaxf(m_run, mx * sl2);
+        float alpha = 1.f;
+        if (m_run == -INFINITY) {
+          m_run = m_new;  // first visible keys: O holds only zeros so far
+        } else if (m_new > m_run + 8.f) {
+          alpha = ex2(m_run - m_new);
+          m_run = m_new;
+        }
+        m_use = (m_run == -INFINITY) ? 0.f : m_run;
+        const float neg = -m_use;
+        float sum0 = 0.f, sum1 = 0.f;
+        // P = exp2(S*scale*log2e - m), packed to bf16 pairs in place: word i
+        // of s[] is rewritten only after s[2i], s[2i+1] were consumed.
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          const float a = ex2(fmaf(__uint_as_float(s[2 * i]), sl2, neg));
+          const float c = ex2(fmaf(__uint_as_float(s[2 * i + 1]), sl2, neg));
+          sum0 += a;
+          sum1 += c;
+          s[i] = pack_bf16x2(a, c);
+        }
+        l_run = l_run * alpha + (sum0 + sum1);
+        tmem_st32(s_addr, s);
+        tmem_st32(s_addr + 32, s + 32);
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+          for (int c = 0; c < HS / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld32(o_addr + c * 32, o);
+            tmem_ld_wait(o);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st32(o_addr + c * 32, o);
+          }
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&p_ready[t]);
+      }
+
+      // ------------------------------------------------------------ epilogue
+      if (n > 0) {
+        mbar_wait(&o_full[t], o_phase & 1);
+        ++o_phase;
+        tc_fence_after();
+      }
+      const bool valid = q_row < p.q_len;
+      const size_t row = (static_cast<size_t>(b) * p.q_len + q_row) * p.heads + h;
+      const float lse_t = l_run > 0.f ? m_use + log2f(l_run) : -INFINITY;  // log2 domain
+      const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
+      float w_run = 0.f, w_new = inv_l, lse_out = lse_t;
+      const int mode = p.mode;
+      if (mode == static_cast<int>(EpiMode::kMiddle) || mode == static_cast<int>(EpiMode::kLast)) {
+        const float a = valid ? p.lse_acc[row] : -INFINITY;
+        const float mx = fmaxf(a, lse_t);
+        if (mx == -INFINITY) {
+          lse_out = -INFINITY;
+          w_run = 0.f;
+          w_new = 0.f;
+        } else {
+          lse_out = mx + log2f(exp2f(a - mx) + exp2f(lse_t - mx));
+          w_run = exp2f(a - lse_out);
+          w_new = exp2f(lse_t - lse_out) * inv_l;
+        }
+      }
+      const bool write_bf16 =
+          mode == static_cast<int>(EpiMode::kSingle) || mode == static_cast<int>(EpiMode::kLast);
+      const bool read_acc = mode >= static_cast<int>(EpiMode::kMiddle);
+#pragma unroll 1
+      for (int c = 0; c < HS / 32; ++c) {
+        float o[32];
+        if (n > 0) {
+          uint32_t r[32];
+          tmem_ld32(o_addr + c * 32, r);
+          tmem_ld_wait(r);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(r[i]) * w_new;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = 0.f;
+        }
+        if (!valid) continue;
+        if (read_acc) {
+          const float4* acc4 = reinterpret_cast<const float4*>(p.o_acc + row * HS + c * 32);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 a = acc4[i];
+            o[4 * i + 0] = fmaf(a.x, w_run, o[4 * i + 0]);
+            o[4 * i + 1] = fmaf(a.y, w_run, o[4 * i + 1]);
+            o[4 * i + 2] = fmaf(a.z, w_run, o[4 * i + 2]);
+            o[4 * i + 3] = fmaf(a.w, w_run, o[4 * i + 3]);
+          }
+        }
+        if (write_bf16) {
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<uint8_t*>(p.o) + (row * HS + c * 32) * 2);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            dst[i] = make_uint4(pack_bf16x2(o[8 * i + 0], o[8 * i + 1]),
+                                pack_bf16x2(o[8 * i + 2], o[8 * i + 3]),
+                                pack_bf16x2(o[8 * i + 4], o[8 * i + 5]),
+                                pack_bf16x2(o[8 * i + 6], o[8 * i + 7]));
+          }
+        } else {
+          float4* dst = reinterpret_cast<float4*>(p.o_acc + row * HS + c * 32);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            dst[i] = make_float4(o[4 * i + 0], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+        }
+      }
+      if (valid) {
+        if (write_bf16)
+          p.lse[row] = lse_out * 0.69314718055994530942f;  // natural log (attention.cpp:260)
+        else
+          p.lse_acc[row] = lse_out;
+      }
+    }
+  } else if (warp == C::kTmaWarp) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      uint32_t kv_it = 0, q_it = 0;
+      const uint64_t keep = l2_policy_evict_last();
+      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+        const uint32_t unit = p.units[u];
+        const int qt = unit & 0xFFFF, hp = (unit >> 16) & 0xFF, b = unit >> 24;
+        const int beg = p.tile_off[qt];
+        const int n = p.tile_off[qt + 1] - beg;
+        if (n == 0) continue;
+        mbar_wait(q_empty, (q_it & 1) ^ 1);
+        ++q_it;
+        for (int t = 0; t < NQ; ++t) {
+          mbar_arrive_expect_tx(&q_full[t], C::kQBytes);
+#pragma unroll
+          for (int sb = 0; sb < C::kSub; ++sb)
+            tma_load_4d(sQ + t * C::kQBytes + sb * C::kSubBytes, &p.tm_q, &q_full[t], sb * 64,
+                        hp * NQ + t, qt * kTileM, b);
+        }
+        const int kvh = (hp * NQ) / group;
+        for (int j = 0; j < n; ++j) {
+          const int kt = p.tile_list[beg + j] & 0x7FFFFFFF;
+#pragma unroll
+          for (int which = 0; which < 2; ++which) {
+            const uint32_t slot = kv_it % NS;
+            mbar_wait(&kv_empty[slot], ((kv_it / NS) & 1) ^ 1);
+            ++kv_it;
+            mbar_arrive_expect_tx(&kv_full[slot], C::kKVBytes);
+            const CUtensorMap* tm = which == 0 ? &p.tm_k : &p.tm_v;
+#pragma unroll
+            for (int sb = 0; sb < C::kSub; ++sb)
+              tma_load_4d_hint(sKV + slot * C::kKVBytes + sb * C::kSubBytes, tm, &kv_full[slot],
+                               sb * 64, kvh, kt * kTileN, b, keep);
+          }
+        }
+      }
+    }
+  } else if (warp == C::kMmaWarp) {
+    // ------------------------------------------------------------ MMA issue
+    if (lane == 0) {
+      constexpr uint32_t kIdescQK = idesc_bf16_f32(128, 128, 0, 0);
+      constexpr uint32_t kIdescPV = idesc_bf16_f32(128, HS, 0, 1);
+      const uint32_t sq = smem_u32(sQ), skv = smem_u32(sKV);
+      uint32_t kv_it = 0, q_phase = 0;
+      uint32_t p_phase[NQ];
+#pragma unroll
+      for (int t = 0; t < NQ; ++t) p_phase[t] = 0;
+
+      auto wait_full = [&](uint32_t idx) {
+        mbar_wait(&kv_full[idx % NS], (idx / NS) & 1);
+        tc_fence_after();
+      };
+      auto issue_qk = [&](int t, uint32_t slot) {
+#pragma unroll
+        for (int kk = 0; kk < HS / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * C::kSubBytes + (kk & 3) * 32;
+          const uint64_t ad = smem_desc_sw128(sq + t * C::kQBytes + off, 16, 1024);
+          const uint64_t bd = smem_desc_sw128(skv + slot * C::kKVBytes + off, 16, 1024);
+          mma_ss(tmem + C::kSCol + t * 128, ad, bd, kIdescQK, kk > 0 ? 1u : 0u);
+        }
+      };
+      auto issue_pv = [&](int t, uint32_t slot, bool acc) {
+#pragma unroll
+        for (int kk = 0; kk < kTileN / 16; ++kk) {
+          const uint64_t bd =
+              smem_desc_sw128(skv + slot * C::kKVBytes + kk * 2048, C::kSubBytes, 1024);
+          mma_ts(tmem + C::kOCol + t * HS, tmem + C::kSCol + t * 128 + kk * 8, bd, kIdescPV,
+                 (acc || kk > 0) ? 1u : 0u);
+        }
+      };
+
+      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+        const int qt = p.units[u] & 0xFFFF;
+        const int n = p.tile_off[qt + 1] - p.tile_off[qt];
+        if (n == 0) continue;
+#pragma unroll
+        for (int t = 0; t < NQ; ++t) mbar_wait(&q_full[t], q_phase & 1);
+        ++q_phase;
+        tc_fence_after();
+        const uint32_t k0 = kv_it;
+        wait_full(k0);
+#pragma unroll
+        for (int t = 0; t < NQ; ++t) {
+          issue_qk(t, k0 % NS);
+          mma_commit(&s_full[t]);
+        }
+        mma_commit(&kv_empty[k0 % NS]);
+        if (n == 1) mma_commit(q_empty);
+        for (int j = 0; j < n; ++j) {
+          const uint32_t vi = kv_it + 2 * j + 1;
+          const uint32_t kn = kv_it + 2 * j + 2;
+          wait_full(vi);
+#pragma unroll
+          for (int t = 0; t < NQ; ++t) {
+            mbar_wait(&p_ready[t], p_phase[t] & 1);
+            ++p_phase[t];
+            tc_fence_after();
+            issue_pv(t, vi % NS, j > 0);
+            if (j + 1 < n) {
+              if (t == 0) wait_full(kn);
+              issue_qk(t, kn % NS);
+              mma_commit(&s_full[t]);
+            }
+          }
+          mma_commit(&kv_empty[vi % NS]);
+          if (j + 1 < n) {
+            mma_commit(&kv_empty[kn % NS]);
+            if (j + 2 == n) mma_commit(q_empty);
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < NQ; ++t) mma_commit(&o_full[t]);
+        kv_it += 2 * n;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == C::kMmaWarp) tmem_dealloc(tmem, C::kTmemCols);
+}
+
+// --------------------------------------------------------------- launchers
+template <int NQ, int HS>
+static cudaError_t launch_impl(const FwdParams& p, int grid, cudaStream_t stream) {
+  using C = FwdCfg<NQ, HS>;
+  auto kern = fa_fwd_sm100_kernel<NQ, HS>;
+  static bool attr_set = false;  // per instantiation; set before first launch
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  kern<<<grid, C::kThreads, C::kSmemBytes, stream>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fa_fwd(const FwdParams& p, int nq, int hs, int grid, cudaStream_t stream) {
+  if (nq == 2 && hs == 128) return launch_impl<2, 128>(p, grid, stream);
+  if (nq == 1 && hs == 128) return launch_impl<1, 128>(p, grid, stream);
+  if (nq == 2 && hs == 64) return launch_impl<2, 64>(p, grid, stream);
+  if (nq == 1 && hs == 64) return launch_impl<1, 64>(p, grid, stream);
+  return cudaErrorInvalidValue;
+}
+
+int fa_fwd_threads(int nq) { return 32 * (4 * nq + 2); }
+
+}  // namespace uspb200

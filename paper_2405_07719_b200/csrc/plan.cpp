@@ -1,0 +1,248 @@
+// plan.cpp — see plan.hpp. Pure host logic; unit-tested on CPU through the
+// C-ABI (tests/test_plan.py) and exercised multi-process by the gloo tests.
+#include "plan.hpp"
+
+#include <algorithm>
+#include <climits>
+#include <numeric>
+#include <sstream>
+
+#include "fa_fwd.hpp"
+
+namespace uspb200 {
+
+void throw_invalid(const std::string& what) { throw Error(ErrorCode::kInvalidArgument, what); }
+void throw_constraint(const std::string& what) { throw Error(ErrorCode::kConstraint, what); }
+
+static void check_rank(const MeshShape& m, int rank) {
+  if (rank < 0 || rank >= m.world()) {
+    std::ostringstream os;
+    os << "rank " << rank << " outside mesh of size " << m.world();  // mesh.cpp:15-21
+    throw_invalid(os.str());
+  }
+}
+
+int MeshShape::ulysses_coord(int rank) const {
+  check_rank(*this, rank);
+  return rank % ulysses;
+}
+int MeshShape::ring_coord(int rank) const {
+  check_rank(*this, rank);
+  return rank / ulysses;
+}
+int MeshShape::rank_of(int u, int r) const {
+  if (u < 0 || u >= ulysses || r < 0 || r >= ring) throw_invalid("mesh coordinates out of range");
+  return r * ulysses + u;
+}
+std::vector<int> MeshShape::ulysses_group(int rank) const {
+  const int r = ring_coord(rank);
+  std::vector<int> g(ulysses);
+  for (int u = 0; u < ulysses; ++u) g[u] = rank_of(u, r);
+  return g;
+}
+std::vector<int> MeshShape::ring_group(int rank) const {
+  const int u = ulysses_coord(rank);
+  std::vector<int> g(ring);
+  for (int r = 0; r < ring; ++r) g[r] = rank_of(u, r);
+  return g;
+}
+
+void UspShape::validate() const {
+  if (batch < 1 || seq_len < 1 || heads < 1 || kv_heads < 1 || head_size < 1)
+    throw_invalid("Tensor4 extents must all be >= 1");  // tensor.hpp:27-29
+  if (mesh.ulysses < 1 || mesh.ring < 1) throw_invalid("mesh degrees must be >= 1");
+  const int ring = mesh.ring, ulysses = mesh.ulysses;
+  // ShardSpec (partition.cpp:78-92); zigzag iff causal (commands.cpp:88)
+  if (causal && seq_len % (2 * ring) != 0) {
+    std::ostringstream os;
+    os << "sequence length " << seq_len << " is not divisible by 2*ring = " << 2 * ring
+       << " as the zigzag partition requires";
+    throw_constraint(os.str());
+  }
+  if (seq_len % ring != 0) throw_constraint("sequence length is not divisible by the ring degree");
+  if ((seq_len / ring) % ulysses != 0) {
+    std::ostringstream os;
+    os << "per-ring-rank token count " << seq_len / ring
+       << " is not divisible by the ulysses degree " << ulysses;
+    throw_constraint(os.str());
+  }
+  // check_usp_inputs (usp_attention.cpp:22-34)
+  if (kv_heads % ulysses != 0 || ulysses > kv_heads) {
+    std::ostringstream os;
+    os << "ulysses degree " << ulysses << " exceeds or does not divide the kv head count "
+       << kv_heads << "; the ulysses degree cannot exceed the number of attention heads";
+    throw_constraint(os.str());
+  }
+  if (heads % ulysses != 0) {
+    std::ostringstream os;
+    os << "query head count " << heads << " is not divisible by the ulysses degree " << ulysses;
+    throw_constraint(os.str());
+  }
+  // check_attention_shapes (attention.cpp:27-32)
+  if (heads % kv_heads != 0) {
+    std::ostringstream os;
+    os << "query head count " << heads << " is not divisible by kv head count " << kv_heads;
+    throw_invalid(os.str());
+  }
+  // B200 engine limits (not reference rules).
+  if (head_size > 128) {
+    std::ostringstream os;
+    os << "head_size " << head_size << " exceeds 128, the largest the tcgen05 kernel supports";
+    throw_invalid(os.str());
+  }
+  if (batch > 255) throw_invalid("batch above 255 is not supported by the work-unit encoding");
+  if (tokens_per_ring_rank() > INT32_MAX / 2 || seq_len > INT32_MAX / 2)
+    throw_invalid("sequence length exceeds the int32 position range");
+  if ((tokens_per_ring_rank() + kTileM - 1) / kTileM > 65535)
+    throw_invalid("too many query tiles for the work-unit encoding");
+}
+
+std::vector<int64_t> zigzag_partition(int64_t seq_len, int ring) {
+  if (ring < 1) throw_invalid("ring degree must be >= 1");
+  if (seq_len % (2 * ring) != 0) {
+    std::ostringstream os;
+    os << "sequence length " << seq_len << " is not divisible by 2*ring = " << 2 * ring
+       << " as the zigzag partition requires";
+    throw_constraint(os.str());
+  }
+  const int64_t chunk = seq_len / (2 * ring);
+  std::vector<int64_t> out;
+  out.reserve(seq_len);
+  for (int p = 0; p < ring; ++p) {  // rank p owns chunks p and 2R-1-p (partition.cpp:24-32)
+    for (int64_t i = 0; i < chunk; ++i) out.push_back(chunk * p + i);
+    for (int64_t i = 0; i < chunk; ++i) out.push_back(chunk * (2 * ring - 1 - p) + i);
+  }
+  return out;
+}
+
+std::vector<int64_t> even_partition(int64_t seq_len, int ring) {
+  if (ring < 1) throw_invalid("ring degree must be >= 1");
+  if (seq_len % ring != 0) throw_constraint("sequence length is not divisible by the ring degree");
+  std::vector<int64_t> out(seq_len);
+  std::iota(out.begin(), out.end(), 0);
+  return out;
+}
+
+std::vector<int64_t> causal_pair_counts(const std::vector<int64_t>& flat, int ring,
+                                        int64_t seq_len) {
+  std::vector<char> seen(seq_len, 0);
+  std::vector<int64_t> counts;
+  const int64_t per = static_cast<int64_t>(flat.size()) / ring;
+  for (int p = 0; p < ring; ++p) {
+    int64_t pairs = 0;
+    for (int64_t i = 0; i < per; ++i) {
+      const int64_t q = flat[p * per + i];
+      if (q < 0 || q >= seq_len || seen[q]) throw_invalid("assignment must cover 0..L-1 exactly once");
+      seen[q] = 1;
+      pairs += q + 1;
+    }
+    counts.push_back(pairs);
+  }
+  for (char s : seen)
+    if (!s) throw_invalid("assignment must cover 0..L-1 exactly once");
+  return counts;
+}
+
+std::vector<int64_t> head_positions(const UspShape& s, int rank) {
+  const int r = s.mesh.ring_coord(rank);
+  const auto lists = s.causal ? zigzag_partition(s.seq_len, s.mesh.ring)
+                              : even_partition(s.seq_len, s.mesh.ring);
+  const int64_t per_ring = s.tokens_per_ring_rank();
+  return std::vector<int64_t>(lists.begin() + r * per_ring, lists.begin() + (r + 1) * per_ring);
+}
+
+std::vector<int64_t> positions_for(const UspShape& s, int rank) {
+  const int u = s.mesh.ulysses_coord(rank);
+  const auto ring_list = head_positions(s, rank);
+  const int64_t per_rank = s.tokens_per_rank();
+  return std::vector<int64_t>(ring_list.begin() + u * per_rank,
+                              ring_list.begin() + (u + 1) * per_rank);
+}
+
+int64_t visible_pairs(const std::vector<int64_t>& q_pos, const std::vector<int64_t>& k_pos,
+                      bool causal) {
+  if (!causal) return static_cast<int64_t>(q_pos.size()) * static_cast<int64_t>(k_pos.size());
+  std::vector<int64_t> ks(k_pos);
+  std::sort(ks.begin(), ks.end());
+  int64_t pairs = 0;
+  for (int64_t q : q_pos)
+    pairs += std::upper_bound(ks.begin(), ks.end(), q) - ks.begin();  // k_pos <= q_pos
+  return pairs;
+}
+
+StepPlan plan_step(const std::vector<int64_t>& q_pos, const std::vector<int64_t>& k_pos,
+                   bool causal, int64_t batch, int head_pairs, bool include_empty) {
+  StepPlan p;
+  p.q_len = static_cast<int>(q_pos.size());
+  p.k_len = static_cast<int>(k_pos.size());
+  p.n_q_tiles = (p.q_len + kTileM - 1) / kTileM;
+  p.n_k_tiles = (p.k_len + kTileN - 1) / kTileN;
+  // Effective positions: masked(i, j) <=> k_eff[j] > q_eff[i]. Non-causal
+  // sees every real key; padding keys are never visible.
+  const int32_t kPadK = INT32_MAX, kAllQ = INT32_MAX - 1;
+  p.q_pos.assign(static_cast<size_t>(p.n_q_tiles) * kTileM, kAllQ);
+  p.k_pos.assign(static_cast<size_t>(p.n_k_tiles) * kTileN, kPadK);
+  for (int i = 0; i < p.q_len; ++i) p.q_pos[i] = causal ? static_cast<int32_t>(q_pos[i]) : kAllQ;
+  for (int j = 0; j < p.k_len; ++j) p.k_pos[j] = causal ? static_cast<int32_t>(k_pos[j]) : 0;
+
+  std::vector<int32_t> kmin(p.n_k_tiles, INT32_MAX), kmax(p.n_k_tiles, INT32_MIN);
+  std::vector<char> ragged(p.n_k_tiles, 0);
+  for (int kt = 0; kt < p.n_k_tiles; ++kt) {
+    for (int c = 0; c < kTileN; ++c) {
+      const int j = kt * kTileN + c;
+      if (j >= p.k_len) {
+        ragged[kt] = 1;
+        continue;
+      }
+      kmin[kt] = std::min(kmin[kt], p.k_pos[j]);
+      kmax[kt] = std::max(kmax[kt], p.k_pos[j]);
+    }
+  }
+  p.tile_off.assign(p.n_q_tiles + 1, 0);
+  std::vector<int> cost(p.n_q_tiles, 0);
+  for (int qt = 0; qt < p.n_q_tiles; ++qt) {
+    int32_t qmin = INT32_MAX, qmax = INT32_MIN;
+    for (int r = 0; r < kTileM; ++r) {
+      const int i = qt * kTileM + r;
+      if (i >= p.q_len) break;
+      qmin = std::min(qmin, p.q_pos[i]);
+      qmax = std::max(qmax, p.q_pos[i]);
+    }
+    for (int kt = 0; kt < p.n_k_tiles; ++kt) {
+      if (kmin[kt] > qmax) continue;  // every key hidden from every row: skip
+      const bool full = kmax[kt] <= qmin && !ragged[kt];
+      p.tile_list.push_back(full ? kt : static_cast<int32_t>(static_cast<uint32_t>(kt) | 0x80000000u));
+      if (full)
+        ++p.full_tiles;
+      else
+        ++p.partial_tiles;
+      ++cost[qt];
+    }
+    p.tile_off[qt + 1] = static_cast<int32_t>(p.tile_list.size());
+  }
+  // Work units in longest-processing-time-first order; ties broken by
+  // (q tile, batch, head pair) so CTAs that start together share K/V tiles.
+  struct U {
+    int cost, qt, b, hp;
+  };
+  std::vector<U> us;
+  for (int qt = 0; qt < p.n_q_tiles; ++qt) {
+    if (cost[qt] == 0 && !include_empty) continue;
+    for (int64_t b = 0; b < batch; ++b)
+      for (int hp = 0; hp < head_pairs; ++hp) us.push_back({cost[qt], qt, static_cast<int>(b), hp});
+  }
+  std::stable_sort(us.begin(), us.end(), [](const U& a, const U& b) {
+    if (a.cost != b.cost) return a.cost > b.cost;
+    if (a.qt != b.qt) return a.qt < b.qt;
+    if (a.b != b.b) return a.b < b.b;
+    return a.hp < b.hp;
+  });
+  p.units.reserve(us.size());
+  for (const U& x : us)
+    p.units.push_back(static_cast<uint32_t>(x.qt) | (static_cast<uint32_t>(x.hp) << 16) |
+                      (static_cast<uint32_t>(x.b) << 24));
+  p.visible_pairs = visible_pairs(q_pos, k_pos, causal);
+  return p;
+}
+
+}  // namespace uspb200

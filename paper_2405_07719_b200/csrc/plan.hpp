@@ -1,0 +1,97 @@
+// plan.hpp — host-side layout and schedule logic of the USP forward.
+//
+// Pure C++ (no CUDA): the process mesh, the zigzag / even sequence layout,
+// the Ulysses and Ring group structure, and the per-ring-step tile plan the
+// attention kernel consumes. Every rule restates the reference:
+//   ProcessMesh          src/simcomm/mesh.cpp:8-57
+//   zigzag/even layout   src/usp/partition.cpp:12-50
+//   ShardSpec checks     src/usp/partition.cpp:74-105
+//   usp input checks     src/usp/usp_attention.cpp:15-38
+//   ring step order      src/usp/ring_attention.cpp:62-75
+//   causal mask          src/numerics/attention.hpp:32-34
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace uspb200 {
+
+// Mirrors uspsim::ErrorCode (src/common/error.hpp:11-17).
+enum class ErrorCode { kInvalidArgument, kConstraint, kCommMismatch, kNumeric, kInternal };
+
+class Error : public std::runtime_error {
+ public:
+  Error(ErrorCode code, const std::string& what) : std::runtime_error(what), code_(code) {}
+  ErrorCode code() const { return code_; }
+
+ private:
+  ErrorCode code_;
+};
+
+[[noreturn]] void throw_invalid(const std::string& what);
+[[noreturn]] void throw_constraint(const std::string& what);
+
+struct MeshShape {
+  int ulysses = 1, ring = 1;
+  int world() const { return ulysses * ring; }
+  int ulysses_coord(int rank) const;              // rank % U       (mesh.cpp:23-26)
+  int ring_coord(int rank) const;                 // rank / U       (mesh.cpp:28-31)
+  int rank_of(int u, int r) const;                // r * U + u      (mesh.cpp:33-39)
+  std::vector<int> ulysses_group(int rank) const; // mesh row       (mesh.cpp:41-48)
+  std::vector<int> ring_group(int rank) const;    // mesh column    (mesh.cpp:50-57)
+};
+
+struct UspShape {
+  MeshShape mesh;
+  int64_t batch = 1, seq_len = 0;
+  int heads = 0, kv_heads = 0, head_size = 0;
+  bool causal = false;
+
+  // Reference validation, same rules and message substrings.
+  void validate() const;
+  int64_t tokens_per_rank() const { return seq_len / mesh.world(); }       // T
+  int64_t tokens_per_ring_rank() const { return seq_len / mesh.ring; }     // U*T
+  int local_heads() const { return heads / mesh.ulysses; }
+  int local_kv_heads() const { return kv_heads / mesh.ulysses; }
+  // The head size the tcgen05 kernel runs at (zero padding is exact).
+  int kernel_head_size() const { return head_size <= 64 ? 64 : 128; }
+};
+
+std::vector<int64_t> zigzag_partition(int64_t seq_len, int ring);  // flattened R x L/R
+std::vector<int64_t> even_partition(int64_t seq_len, int ring);
+std::vector<int64_t> causal_pair_counts(const std::vector<int64_t>& flat, int ring,
+                                        int64_t seq_len);
+// ShardSpec::positions_for (zigzag iff causal, as commands.cpp:88 does).
+std::vector<int64_t> positions_for(const UspShape& s, int rank);
+// gather_positions over the Ulysses group == the ring list of ring coord r.
+std::vector<int64_t> head_positions(const UspShape& s, int rank);
+
+// The ring source block at step t for ring coordinate r (ring_attention.cpp:63).
+inline int ring_source(int r, int step, int ring) { return (r - step + ring) % ring; }
+
+// Per-ring-step tile plan for the attention kernel.
+struct StepPlan {
+  int q_len = 0, k_len = 0, n_q_tiles = 0, n_k_tiles = 0;
+  std::vector<int32_t> q_pos;      // effective positions, padded to 128
+  std::vector<int32_t> k_pos;      // effective positions, padded to 128 (INT32_MAX)
+  std::vector<int32_t> tile_off;   // CSR offsets, n_q_tiles + 1
+  std::vector<int32_t> tile_list;  // k tile | partial << 31
+  std::vector<uint32_t> units;     // q_tile | head_pair << 16 | batch << 24, LPT order
+  int64_t full_tiles = 0, partial_tiles = 0, visible_pairs = 0;
+};
+
+// q_pos/k_pos are ORIGINAL token positions; causal == false makes every key
+// visible (BlockMask::none). include_empty keeps query tiles with no visible
+// key tile in the unit list (needed by first/last ring steps so every row is
+// written). head_pairs = local q heads / NQ.
+StepPlan plan_step(const std::vector<int64_t>& q_pos, const std::vector<int64_t>& k_pos,
+                   bool causal, int64_t batch, int head_pairs, bool include_empty);
+
+// Exact unmasked (q, k) pair count of one block, summed over the block
+// (causal_pair_counts semantics, partition.cpp:52-72) — for FLOP accounting.
+int64_t visible_pairs(const std::vector<int64_t>& q_pos, const std::vector<int64_t>& k_pos,
+                      bool causal);
+
+}  // namespace uspb200

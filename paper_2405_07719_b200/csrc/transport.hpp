@@ -1,0 +1,59 @@
+// transport.hpp — the two exchanges of the USP forward.
+//
+// Semantics follow the reference's simulated collectives:
+//   all_to_all  RankCtx::all_to_all  (src/simcomm/world.hpp:134-166): part p
+//               of every member goes to member p, received parts land in
+//               member order;
+//   ring_shift  RankCtx::ring_shift  (world.hpp:169-190): send to member
+//               (i+1) % n, receive from (i-1+n) % n.
+// Both are stream-ordered and collective over the group: every member must
+// call them in the same order (world.cpp:135-165).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <memory>
+#include <vector>
+
+namespace uspb200 {
+
+struct A2APart {
+  const void* send;  // my part for member p
+  void* recv;        // where member p's part for me lands
+};
+
+// The two sub-groups of one rank (ProcessMesh::ulysses_group / ring_group).
+struct Groups {
+  int rank = 0;
+  std::vector<int> ulysses, ring;
+  void* ulysses_comm = nullptr;  // transport-private (ncclComm_t for NCCL)
+  void* ring_comm = nullptr;
+};
+
+class Transport {
+ public:
+  virtual ~Transport() = default;
+  virtual int world_size() const = 0;
+  // Collective over the world: builds this rank's sub-groups.
+  virtual std::shared_ptr<Groups> make_groups(int rank, const std::vector<int>& ulysses_group,
+                                              const std::vector<int>& ring_group) = 0;
+  // Several tensors exchanged in one collective over the Ulysses group:
+  // parts[t][p] for tensor t and member index p, bytes[t] per part.
+  virtual void all_to_all(const Groups& g, const std::vector<std::vector<A2APart>>& parts,
+                          const std::vector<size_t>& bytes, cudaStream_t stream) = 0;
+  // Ring shift of several buffers at once (K and V) over the ring group.
+  virtual void ring_shift(const Groups& g, const std::vector<const void*>& send,
+                          const std::vector<void*>& recv, const std::vector<size_t>& bytes,
+                          cudaStream_t stream) = 0;
+  // NCCL kernels occupy SMs (the attention grid leaves room for them);
+  // the local transport uses copy engines.
+  virtual int reserved_sms() const = 0;
+};
+
+std::unique_ptr<Transport> make_local_transport(int world_size);
+std::unique_ptr<Transport> make_nccl_transport(const unsigned char unique_id[128],
+                                               int world_size, int rank, int device);
+void nccl_unique_id(unsigned char out[128]);
+
+}  // namespace uspb200

@@ -1,0 +1,106 @@
+"""GPU parity: the B200 engine (through the C ABI) vs the CPU oracle.
+
+Inputs: the reference generator (UniformSource, Q,K,V order) rounded to
+bf16; the oracle runs in fp64 on the SAME bf16 values widened (as
+commands.cpp:142-153 widens fp32), isolating kernel error from input
+quantisation. The oracle itself is pinned bitwise to the reference
+(tests/test_oracle.py).
+
+Tolerance (bf16 in / fp32 accumulate vs fp64, stated per SURVEY §8(c)):
+  O   max-abs <= 1e-2 and relative L2 <= 1e-2
+  LSE max-abs <= 2e-3 (natural log)
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle.oracle import Oracle
+from tests.usp_harness import UspCase, errors, make_globals, run_usp_gpu, to_bf16, widen
+
+O_TOL = 1e-2
+O_REL_L2 = 1e-2
+LSE_TOL = 2e-3
+
+pytestmark = pytest.mark.gpu
+
+
+def _check_case(c: UspCase, device):
+    q, k, v = make_globals(c)
+    tq, tk, tv = (to_bf16(x, device) for x in (q, k, v))
+    out, lses, engines, _ = run_usp_gpu(c, tq, tk, tv, device)
+    qd, kd, vd = widen(tq), widen(tk), widen(tv)
+    ref_out, ref_lse = Oracle.usp_forward(qd, kd, vd, c.ulysses, c.ring, c.causal)
+    eo = errors(widen(out), ref_out)
+    got_lse = np.stack([widen(l_) for l_ in lses])
+    el = errors(got_lse, ref_lse)
+    msg = f"{c}: O {eo} LSE {el}"
+    assert np.isfinite(widen(out)).all(), msg
+    assert eo["max_abs"] <= O_TOL and eo["rel_l2"] <= O_REL_L2, msg
+    assert el["max_abs"] <= LSE_TOL, msg
+    assert all(e.last_launches() >= 1 for e in engines), "native kernels did not launch"
+    return eo, el
+
+
+@pytest.mark.parametrize("causal", [True, False])
+@pytest.mark.parametrize("shape", [(512, 8, 2, 128), (640, 4, 4, 64), (1000, 4, 1, 128), (384, 6, 3, 128)])
+def test_single_rank_matches_oracle(cuda, shape, causal):
+    L, hc, kv, hs = shape
+    _check_case(UspCase(seq=L, hc=hc, kv_hc=kv, hs=hs, causal=causal, seed=7 + L), cuda)
+
+
+def test_single_rank_batch2_and_padded_head_size(cuda):
+    _check_case(UspCase(bs=2, seq=256, hc=4, kv_hc=2, hs=4, causal=True, seed=99), cuda)
+    _check_case(UspCase(bs=1, seq=300, hc=2, kv_hc=1, hs=96, causal=False, seed=98), cuda)
+
+
+@pytest.mark.parametrize("causal", [True, False])
+@pytest.mark.parametrize("u,r", [(1, 8), (2, 4), (4, 2), (8, 1)])
+def test_all_factorizations_of_8(cuda, u, r, causal):
+    # test_usp.cpp:315-341 (L32 hc8 kv8 hs4 seed 4242) at a GPU-sized L.
+    _check_case(UspCase(seq=2048, hc=8, kv_hc=8, hs=128, ulysses=u, ring=r, causal=causal, seed=4242), cuda)
+
+
+@pytest.mark.parametrize("u,r", [(1, 8), (2, 4), (4, 2), (8, 1)])
+def test_reference_tiny_factorizations(cuda, u, r):
+    # The exact reference case: L32 hc8 kv8 hs4 seed 4242 (test_usp.cpp:315-341).
+    for causal in (True, False):
+        _check_case(UspCase(seq=32, hc=8, kv_hc=8, hs=4, ulysses=u, ring=r, causal=causal, seed=4242), cuda)
+
+
+def test_gqa_hybrid_batch2(cuda):
+    # test_usp.cpp:343-362: GQA hc8 kv2, U2 R2, bs2, seed 999.
+    _check_case(UspCase(bs=2, seq=512, hc=8, kv_hc=2, hs=128, ulysses=2, ring=2, causal=True, seed=999), cuda)
+
+
+def test_llama_shape_hybrid(cuda):
+    _check_case(UspCase(seq=4096, hc=32, kv_hc=8, hs=128, ulysses=4, ring=2, causal=True, seed=0), cuda)
+
+
+def test_c1_shape(cuda):
+    # config c1: L4096 hc8 kv8 hs64 U2R2 causal.
+    _check_case(UspCase(seq=4096, hc=8, kv_hc=8, hs=64, ulysses=2, ring=2, causal=True, seed=0), cuda)
+
+
+def test_long_sequence_sampled_rows(cuda):
+    """L = 32K, Llama heads, U=R=1: sampled-row oracle."""
+    L, hc, kv, hs = 32768, 32, 8, 128
+    c = UspCase(seq=L, hc=hc, kv_hc=kv, hs=hs, causal=True, seed=0)
+    q, k, v = make_globals(c)
+    tq, tk, tv = (to_bf16(x, cuda) for x in (q, k, v))
+    out, lses, _, _ = run_usp_gpu(c, tq, tk, tv, cuda)
+    rows = np.unique(np.concatenate([np.arange(0, 8), np.linspace(0, L - 1, 120).astype(np.int64),
+                                     np.arange(L - 8, L)]))
+    qd = widen(tq[:, rows])
+    kd, vd = widen(tk), widen(tv)
+    ref_o, ref_l = Oracle.softmax_rows(qd, kd, vd, True, rows, np.arange(L))
+    eo = errors(widen(out[:, rows]), ref_o)
+    el = errors(widen(lses[0][:, rows]), ref_l)
+    assert eo["max_abs"] <= O_TOL and el["max_abs"] <= LSE_TOL, (eo, el)
+
+
+def test_invalid_ulysses_degree_message(cuda):
+    from paper_2405_07719_b200 import ProcessMesh, UspAttention, UspInvalidInput
+
+    with pytest.raises(UspInvalidInput, match="cannot exceed"):
+        UspAttention(ProcessMesh(16, 1), rank=0, seq_len=256, heads=32, kv_heads=8, head_size=128,
+                     causal=True)

@@ -1,0 +1,90 @@
+"""Shared test harness — the analogue of the reference's tests/usp_harness.hpp.
+
+make_globals draws Q, K, V from ONE UniformSource stream in that order
+(usp_harness.hpp:30-41, commands.cpp:90-102) via the oracle's restated
+mt19937_64 generator; run_usp_gpu shards them with ShardSpec (zigzag iff
+causal), runs the B200 engine on a U x R in-process world on one GPU
+(usp_local_world_fwd: one host thread per rank, like World::run) and
+reassembles O in original order (place_rows, partition.hpp:75-87).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from oracle.oracle import Oracle
+
+
+@dataclass
+class UspCase:
+    bs: int = 1
+    seq: int = 8
+    hc: int = 2
+    kv_hc: int = 2
+    hs: int = 4
+    ulysses: int = 1
+    ring: int = 1
+    causal: bool = False
+    seed: int = 1234
+
+
+def make_globals(c: UspCase):
+    nq = c.bs * c.seq * c.hc * c.hs
+    nk = c.bs * c.seq * c.kv_hc * c.hs
+    g = Oracle.uniform(c.seed, nq + 2 * nk)
+    q = g[:nq].reshape(c.bs, c.seq, c.hc, c.hs)
+    k = g[nq:nq + nk].reshape(c.bs, c.seq, c.kv_hc, c.hs)
+    v = g[nq + nk:].reshape(c.bs, c.seq, c.kv_hc, c.hs)
+    return q, k, v
+
+
+def to_bf16(x, device):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(x)).to(torch.bfloat16).to(device)
+
+
+def widen(t) -> np.ndarray:
+    return t.detach().double().cpu().numpy()
+
+
+def run_usp_gpu(c: UspCase, q, k, v, device):
+    """Runs the engine on every rank of a local world on ``device``.
+    q, k, v: global bf16 torch tensors. Returns (out_global, lse_blocks,
+    engines) with lse_blocks[rank] head-sharded (bs, L/R, hc/U)."""
+    import torch
+
+    from paper_2405_07719_b200 import Comm, ProcessMesh, UspAttention, local_world_forward
+
+    mesh = ProcessMesh(c.ulysses, c.ring)
+    n = mesh.world_size()
+    comm = Comm.local(n) if n > 1 else None
+    engines = [UspAttention(mesh, rank=r, seq_len=c.seq, heads=c.hc, kv_heads=c.kv_hc, head_size=c.hs,
+                            causal=c.causal, batch=c.bs, device=device.index or 0, comm=comm)
+               for r in range(n)]
+    pos = [torch.tensor(e.positions(), dtype=torch.long, device=device) for e in engines]
+    qs = [q[:, p].contiguous() for p in pos]
+    ks = [k[:, p].contiguous() for p in pos]
+    vs = [v[:, p].contiguous() for p in pos]
+    outs, lses = zip(*[e.alloc_outputs() for e in engines])
+    streams = [torch.cuda.Stream(device) for _ in engines]
+    torch.cuda.synchronize(device)
+    local_world_forward(engines, qs, ks, vs, outs, lses, streams)
+    torch.cuda.synchronize(device)
+    out = torch.empty_like(q)
+    for p, o in zip(pos, outs):
+        out[:, p] = o
+    return out, [l_ for l_ in lses], engines, comm
+
+
+def errors(got: np.ndarray, want: np.ndarray):
+    """max-abs, and the reference's max-rel (commands.cpp:71-83) plus a
+    well-conditioned relative error max|d| / (1e-2 + |ref|)."""
+    d = np.abs(got - want)
+    return {
+        "max_abs": float(d.max()),
+        "max_rel_ref": float((d / np.maximum(np.abs(want), 1e-12)).max()),
+        "max_rel_cond": float((d / (1e-2 + np.abs(want))).max()),
+        "rel_l2": float(np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-300)),
+    }
