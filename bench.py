@@ -1,0 +1,381 @@
+#!/usr/bin/env python
+"""USP attention forward benchmark (the BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+
+One "step" = one USP attention forward (usp_attn_fwd through the C ABI) of
+the Llama-3-8B attention layer (hc=32, kv=8, hs=128, bs=1) at L=128K,
+causal with zigzag load balance, over a U x R mesh of N GPUs (default pure
+ring, U=1, R=N: config c3; N=1 is the single-GPU kernel). Inputs are
+synthetic bf16, resident in HBM; Q alone is 1 GiB, larger than the 126 MB
+L2, so no flush is needed between steps. Prints ONE JSON line on rank 0.
+
+--impl reference times the reference's own CPU implementation
+(oracle/_ref/libuspref.so: usp_attention<float> on U*R rank threads,
+compiled from /root/reference sources) on a bounded sample of the same
+workload, with as many host threads as its mesh allows.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "USP attn fwd TFLOP/s, L=128K Llama3-8B layer, 1/2/4/8 B200; % of BF16 peak"
+UNIT = "TFLOP/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--seq-len", type=int, default=131072)
+    ap.add_argument("--heads", type=int, default=32)
+    ap.add_argument("--kv-heads", type=int, default=8)
+    ap.add_argument("--head-size", type=int, default=128)
+    ap.add_argument("--ulysses", type=int, default=1, help="Ulysses degree U (R = N / U)")
+    ap.add_argument("--non-causal", action="store_true")
+    ap.add_argument("--cpu-sample-len", type=int, default=4096)
+    ap.add_argument("--skip-cpu-baseline", action="store_true")
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def causal_flops(L, hc, hs, causal=True, batch=1):
+    pairs = L * (L + 1) // 2 if causal else L * L
+    return 4.0 * batch * hc * hs * pairs
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["bf16_tflops"]), float(p.get("bf16_tflops_sustained", p["bf16_tflops"])), "measured"
+    except Exception:
+        return 1590.0, 1400.0, "fallback"
+
+
+def workload_config(a, n, U, R):
+    return {
+        "workload": f"usp_attn_fwd llama3-8b layer L={a.seq_len} {'causal zigzag' if not a.non_causal else 'full'}",
+        "seq_len": a.seq_len, "batch": 1, "heads": a.heads, "kv_heads": a.kv_heads, "head_size": a.head_size,
+        "causal": not a.non_causal, "ulysses": U, "ring": R, "parallelism": f"u{U}r{R}",
+        "l2": "inputs larger than L2 (Q alone %d MiB > 126 MB); no flush" % (a.seq_len * a.heads * a.head_size * 2 // n >> 20),
+    }
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+                power.append(float(parts[3]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm), "power_w_max": max(power) if power else None}
+
+
+# ------------------------------------------------------------- reference
+def reference_mesh(kv_heads, seq_len, threads):
+    """Largest U*R <= threads the reference accepts (U | kv, L % 2R == 0)."""
+    best = (1, 1)
+    for U in range(1, kv_heads + 1):
+        if kv_heads % U:
+            continue
+        for R in range(1, threads // U + 1):
+            if seq_len % (2 * R) or (seq_len // R) % U:
+                continue
+            if U * R > best[0] * best[1] or (U * R == best[0] * best[1] and U > best[0]):
+                best = (U, R)
+    return best
+
+
+def cpu_reference_sample(a, repeats=1):
+    """Times the reference CPU forward on one bounded sample; returns a dict."""
+    import numpy as np
+
+    from oracle.oracle import Oracle, Reference
+
+    L, hc, kv, hs = a.cpu_sample_len, a.heads, a.kv_heads, a.head_size
+    causal = not a.non_causal
+    cores = os.cpu_count() or 1
+    g = Oracle.uniform(0, L * hc * hs + 2 * L * kv * hs)
+    q = g[:L * hc * hs].reshape(1, L, hc, hs)
+    k = g[L * hc * hs:L * hc * hs + L * kv * hs].reshape(1, L, kv, hs)
+    v = g[L * hc * hs + L * kv * hs:].reshape(1, L, kv, hs)
+    f = causal_flops(L, hc, hs, causal)
+    if Reference.available():
+        U, R = reference_mesh(kv, L, cores)
+        secs = [Reference.usp_forward(q, k, v, U, R, causal, precision="fp32", want_out=False)[2]
+                for _ in range(repeats)]
+        kind, threads = "reference", U * R
+        sample = (f"reference usp_attention<float> (oracle/_ref, built from /root/reference sources), "
+                  f"L={L} hc={hc} kv={kv} hs={hs} {'causal' if causal else 'full'}, mesh U{U}xR{R} = {U * R} "
+                  f"rank threads of {cores} host cores; x{repeats}")
+    else:
+        secs = []
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            Oracle.usp_forward(q, k, v, 1, 1, causal)
+            secs.append(time.perf_counter() - t0)
+        kind, threads = "port", cores
+        sample = (f"oracle C port (fp64, OpenMP) of the reference forward, L={L} hc={hc} kv={kv} hs={hs}; "
+                  f"x{repeats}")
+    mean = sum(secs) / len(secs)
+    return {"value": f / mean / 1e12, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample,
+            "seconds_per_sample": mean, "flops_per_sample": f,
+            "extrapolated_full_workload_s": causal_flops(a.seq_len, hc, hs, causal) / (f / mean)}
+
+
+def run_reference_arm(a):
+    rank = int(os.environ.get("RANK", "0"))
+    n = a.gpus
+    U = a.ulysses
+    R = max(1, n // U)
+    if rank != 0:
+        return
+    for _ in range(a.warmup):
+        cpu_reference_sample(a)
+    vals, secs = [], []
+    for _ in range(a.steps):
+        r = cpu_reference_sample(a)
+        vals.append(r["value"])
+        secs.append(r["seconds_per_sample"])
+    v = sum(vals) / len(vals)
+    cfg = workload_config(a, n, U, R)
+    cfg["sample"] = r["sample"]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": n, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": 1000 * sum(secs) / len(secs), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic", "config": cfg,
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": r["cores"], "kind": r["kind"], "sample": r["sample"]},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------- ours
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_07719_b200 import Comm, ProcessMesh, UspAttention
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n = a.gpus
+    if world != n:
+        raise SystemExit(f"--gpus {n} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    distributed = world > 1
+    if distributed:
+        dist.init_process_group("nccl", device_id=dev)
+    U = a.ulysses
+    if n % U:
+        raise SystemExit("ulysses degree must divide the GPU count")
+    R = n // U
+    mesh = ProcessMesh(U, R)
+    comm = Comm.from_torch_distributed(local) if distributed else None
+    causal = not a.non_causal
+    eng = UspAttention(mesh, rank=rank, seq_len=a.seq_len, heads=a.heads, kv_heads=a.kv_heads,
+                       head_size=a.head_size, causal=causal, device=local, comm=comm)
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    q = torch.randn(eng.q_shape(), device=dev, dtype=torch.bfloat16, generator=gen)
+    k = torch.randn(eng.kv_shape(), device=dev, dtype=torch.bfloat16, generator=gen)
+    v = torch.randn(eng.kv_shape(), device=dev, dtype=torch.bfloat16, generator=gen)
+    o, lse = eng.alloc_outputs()
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if distributed:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if not distributed:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(a.warmup):
+        eng.forward(q, k, v, o, lse, stream)
+    torch.cuda.synchronize(dev)
+
+    # ---- timed region (device time, CUDA events, max over ranks)
+    clocks = ClockSampler(local)
+    launches = 0
+    barrier()
+    torch.cuda.synchronize(dev)
+    clocks.start()
+    time.sleep(0.3)
+    eng.enable_timing(True)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(a.steps):
+        eng.forward(q, k, v, o, lse, stream)
+        launches += eng.last_launches()
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier()
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1) / a.steps
+    kts = eng.kernel_times()
+    eng.enable_timing(False)
+    ms = max_over_ranks(ms)
+
+    rank_flops = eng.flops()
+    total_flops = causal_flops(a.seq_len, a.heads, a.head_size, causal)
+    value = total_flops / (ms * 1e-3) / 1e12
+    peak, peak_sus, peak_kind = peaks()
+
+    # roofline of the dominant kernel: algorithmic FLOPs per launch / mean
+    # launch duration, both over the timed region
+    kernel_ms = sum(kts) / len(kts) if kts else None
+    flops_per_launch = rank_flops * a.steps / max(len(kts), 1)
+    achieved = flops_per_launch / (kernel_ms * 1e-3) / 1e12 if kernel_ms else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                tr = json.load(f)
+            key = f"L{a.seq_len}_u{U}r{R}_{'causal' if causal else 'full'}"
+            traffic = tr.get(key, {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": UNIT,
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "peak_kind": f"{peak_kind} burst bf16_tflops (cuBLAS)",
+                "frac_of_sustained": (achieved / peak_sus) if achieved else None,
+                "kernel_ms_mean": kernel_ms, "launches_timed": len(kts),
+                "flops_per_launch": flops_per_launch}
+
+    # ---- e2e through the public API: pinned host -> device, forward, device -> host
+    e2e = None
+    if not a.skip_e2e:
+        qh = torch.empty(q.shape, dtype=q.dtype, pin_memory=True).copy_(q)
+        kh = torch.empty(k.shape, dtype=k.dtype, pin_memory=True).copy_(k)
+        vh = torch.empty(v.shape, dtype=v.dtype, pin_memory=True).copy_(v)
+        oh = torch.empty(o.shape, dtype=o.dtype, pin_memory=True)
+        lh = torch.empty(lse.shape, dtype=lse.dtype, pin_memory=True)
+
+        def e2e_step():
+            q.copy_(qh, non_blocking=True)
+            k.copy_(kh, non_blocking=True)
+            v.copy_(vh, non_blocking=True)
+            eng.forward(q, k, v, o, lse, stream)
+            oh.copy_(o, non_blocking=True)
+            lh.copy_(lse, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize(dev)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(a.e2e_steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        ems = max_over_ranks(e0.elapsed_time(e1) / a.e2e_steps)
+        h2d = sum(t.numel() * t.element_size() for t in (q, k, v))
+        d2h = o.numel() * o.element_size() + lse.numel() * lse.element_size()
+        e2e = {"value": total_flops / (ems * 1e-3) / 1e12, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": ems, "steps": a.e2e_steps,
+               "path": "paper_2405_07719_b200.UspAttention.forward -> usp_attn_fwd (C ABI)"}
+
+    cpu = None
+    if rank == 0 and n == 1 and not a.skip_cpu_baseline:
+        try:
+            cpu = cpu_reference_sample(a, repeats=2)
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "unavailable", "sample": repr(e)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (torch.randn bf16, resident in HBM)",
+            "config": workload_config(a, n, U, R),
+            "pct_of_peak_per_gpu": value / n / peak * 100.0,
+            "tokens_per_s": a.seq_len / (ms * 1e-3),
+            "roofline": roofline, "cpu_baseline": cpu, "clocks": clk, "e2e": e2e,
+            "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if distributed:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference_arm(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

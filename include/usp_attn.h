@@ -119,6 +119,12 @@ USP_API usp_status usp_attn_fwd(usp_engine* engine, const void* q, const void* k
 /* Launches of the engine's own kernels in the last usp_attn_fwd. */
 USP_API int32_t usp_engine_last_launches(const usp_engine* engine);
 USP_API void usp_engine_destroy(usp_engine* engine);
+/* Optional per-launch timing of the attention kernel: CUDA events recorded
+ * around every launch on its stream while enabled. kernel_times
+ * synchronises, writes up to cap durations (ms) and returns how many launches
+ * were recorded since the last call (-1 on error). */
+USP_API usp_status usp_engine_enable_timing(usp_engine* engine, int32_t on);
+USP_API int32_t usp_engine_kernel_times(usp_engine* engine, float* ms, int32_t cap);
 
 /* Runs usp_attn_fwd on every rank of a local world, one host thread per
  * rank (engines[i] must belong to rank i); blocks until all are issued. */

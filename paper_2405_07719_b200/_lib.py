@@ -62,7 +62,8 @@ EXPORTS = [
     "usp_config_validate", "usp_zigzag_partition", "usp_positions_for", "usp_head_positions",
     "usp_causal_pair_counts", "usp_schedule", "usp_step_plan", "usp_rank_flops", "usp_nccl_unique_id",
     "usp_comm_create_nccl", "usp_comm_create_local", "usp_comm_destroy", "usp_engine_create",
-    "usp_attn_fwd", "usp_engine_last_launches", "usp_engine_destroy", "usp_local_world_fwd",
+    "usp_attn_fwd", "usp_engine_last_launches", "usp_engine_destroy", "usp_engine_enable_timing",
+    "usp_engine_kernel_times", "usp_local_world_fwd",
     "usp_last_error", "usp_version",
 ]
 
@@ -92,6 +93,8 @@ def _declare(lib):
         "usp_attn_fwd": (st, [vp, vp, vp, vp, vp, vp, vp]),
         "usp_engine_last_launches": (ctypes.c_int32, [vp]),
         "usp_engine_destroy": (None, [vp]),
+        "usp_engine_enable_timing": (st, [vp, ctypes.c_int32]),
+        "usp_engine_kernel_times": (ctypes.c_int32, [vp, P(ctypes.c_float), ctypes.c_int32]),
         "usp_local_world_fwd": (st, [P(vp), ctypes.c_int32, P(vp), P(vp), P(vp), P(vp), P(vp), P(vp)]),
         "usp_last_error": (ctypes.c_char_p, []),
         "usp_version": (ctypes.c_char_p, []),

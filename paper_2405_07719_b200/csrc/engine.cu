@@ -192,6 +192,9 @@ class Engine {
       }
     }
 
+    sched_ = DevBuf(64);
+    USPB_CHECK(cudaMemset(sched_.p, 0, 64));
+
     // Static layout -> per-step tile plans (the reference all_gathers these
     // positions at run time; here they are known at create).
     const auto my_pos = head_positions(shape_, c.rank);
@@ -202,7 +205,8 @@ class Engine {
       st.mode = R_ == 1 ? EpiMode::kSingle
                         : (t == 0 ? EpiMode::kFirst : (t == R_ - 1 ? EpiMode::kLast : EpiMode::kMiddle));
       const bool include_empty = st.mode != EpiMode::kMiddle;
-      st.host = plan_step(my_pos, k_pos, shape_.causal, B_, hl_ / nq_, include_empty);
+      st.host = plan_step(my_pos, k_pos, shape_.causal, B_, hl_ / nq_, include_empty,
+                          std::max(1, group / nq_));
       st.q_pos = upload(st.host.q_pos);
       st.k_pos = upload(st.host.k_pos);
       st.tile_off = upload(st.host.tile_off);
@@ -213,6 +217,7 @@ class Engine {
   }
 
   ~Engine() {
+    for (auto e : event_pool_) cudaEventDestroy(e);
     for (auto e : ev_pre_) cudaEventDestroy(e);
     for (auto e : ev_recv_) cudaEventDestroy(e);
     if (comm_stream_) cudaStreamDestroy(comm_stream_);
@@ -453,6 +458,7 @@ class Engine {
     p.tile_list = s.tile_list.as<int32_t>();
     p.q_pos = s.q_pos.as<int32_t>();
     p.k_pos = s.k_pos.as<int32_t>();
+    p.sched = sched_.as<int>();
     p.num_units = static_cast<int>(s.host.units.size());
     p.batch = static_cast<int>(B_);
     p.q_len = static_cast<int>(Tr_);
@@ -461,12 +467,67 @@ class Engine {
     p.kv_heads = kvl_;
     p.mode = static_cast<int>(s.mode);
     p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(double(hs_)));
+    static const int kv_hint = [] {
+      const char* e = std::getenv("USP_KV_HINT");
+      return e ? std::atoi(e) : 0;
+    }();
+    p.kv_hint = kv_hint;
+    static const bool trace = std::getenv("USP_FA_TRACE") != nullptr;
+    if (trace) {
+      if (!trace_buf_.p) trace_buf_ = DevBuf(sizeof(unsigned long long) * kTraceTiles * kTraceEvents);
+      USPB_CHECK(cudaMemsetAsync(trace_buf_.p, 0, trace_buf_.bytes, st));
+      p.trace = trace_buf_.as<unsigned long long>();
+    }
     const int reserve = (R_ > 1 && tr_) ? tr_->reserved_sms() : 0;
     const int slots = std::max(1, num_sms_ - reserve);
     const int grid = std::min(p.num_units, slots);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timing_) {
+      e0 = timing_event(2 * timed_.size());
+      e1 = timing_event(2 * timed_.size() + 1);
+      USPB_CHECK(cudaEventRecord(e0, st));
+    }
     USPB_CHECK(launch_fa_fwd(p, nq_, hsk_, grid, st));
     ++launches_;
+    if (timing_) {
+      USPB_CHECK(cudaEventRecord(e1, st));
+      timed_.push_back({e0, e1});
+    }
   }
+
+  // Per-launch CUDA-event timing of the attention kernel, recorded on the
+  // stream it is launched on (for roofline accounting).
+  cudaEvent_t timing_event(size_t i) {
+    while (event_pool_.size() <= i) {
+      cudaEvent_t e;
+      USPB_CHECK(cudaEventCreate(&e));
+      event_pool_.push_back(e);
+    }
+    return event_pool_[i];
+  }
+
+ public:
+  void enable_timing(bool on) {
+    timing_ = on;
+    timed_.clear();
+  }
+  int kernel_times(float* ms, int cap) {
+    int n = 0;
+    for (const auto& pr : timed_) {
+      USPB_CHECK(cudaEventSynchronize(pr.second));
+      float t = 0.f;
+      USPB_CHECK(cudaEventElapsedTime(&t, pr.first, pr.second));
+      if (n < cap) ms[n] = t;
+      ++n;
+    }
+    timed_.clear();
+    return n;
+  }
+
+ private:
+  bool timing_ = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed_;
+  std::vector<cudaEvent_t> event_pool_;
 
   usp_config cfg_;
   Transport* tr_;
@@ -478,6 +539,13 @@ class Engine {
   size_t q_part_ = 0, kv_part_ = 0, kv_bytes_ = 0;
   DevBuf q_h_, kv0_, o_h_, send_, recv_, o_send_, o_recv_, o_acc_, lse_acc_;
   DevBuf kv_ring_[2];
+  DevBuf sched_;  // unit tickets of the attention kernel (self-resetting)
+  DevBuf trace_buf_;  // USP_FA_TRACE development stamps
+
+ public:
+  const void* trace_ptr() const { return trace_buf_.p; }
+
+ private:
   std::vector<DevStep> steps_;
   cudaStream_t comm_stream_ = nullptr;
   std::vector<cudaEvent_t> ev_pre_, ev_recv_;
@@ -668,11 +736,34 @@ usp_status usp_attn_fwd(usp_engine* engine, const void* q, const void* k, const 
   });
 }
 
+// Development: copies the USP_FA_TRACE stamps (kTraceEvents x kTraceTiles)
+// to host memory; returns 0 when tracing is off.
+extern "C" USP_API int usp_engine_trace_copy(const usp_engine* engine, unsigned long long* host) {
+  if (!engine || !engine->impl->trace_ptr()) return 0;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, engine->impl->trace_ptr(), sizeof(unsigned long long) * kTraceTiles * kTraceEvents,
+             cudaMemcpyDeviceToHost);
+  return 1;
+}
+
 int32_t usp_engine_last_launches(const usp_engine* engine) {
   return engine ? engine->impl->last_launches() : 0;
 }
 
 void usp_engine_destroy(usp_engine* engine) { delete engine; }
+
+usp_status usp_engine_enable_timing(usp_engine* engine, int32_t on) {
+  return guarded([&] {
+    if (!engine) throw_invalid("engine is null");
+    engine->impl->enable_timing(on != 0);
+  });
+}
+
+int32_t usp_engine_kernel_times(usp_engine* engine, float* ms, int32_t cap) {
+  int32_t n = -1;
+  if (guarded([&] { n = engine->impl->kernel_times(ms, cap); }) != USP_OK) return -1;
+  return n;
+}
 
 usp_status usp_local_world_fwd(usp_engine* const* engines, int32_t world_size,
                                const void* const* q, const void* const* k, const void* const* v,

@@ -18,6 +18,8 @@ namespace uspb200 {
 
 constexpr int kTileM = 128;  // query rows per tile (TMEM lanes)
 constexpr int kTileN = 128;  // keys per K/V tile
+constexpr int kTraceTiles = 256;
+constexpr int kTraceEvents = 16;
 
 enum class EpiMode : int {
   kSingle = 0,  // only step: write bf16 O + natural-log LSE
@@ -42,10 +44,15 @@ struct FwdParams {
   const int32_t* q_pos;      // effective query positions, padded to 128
   const int32_t* k_pos;      // effective key positions, padded to 128 (INT_MAX)
 
+  int* sched;  // [0] next-unit ticket, [1] finished-CTA count; zero between launches
   int num_units;
   int batch, q_len, k_len, heads, kv_heads;
   int mode;          // EpiMode
   float scale_log2;  // log2(e) / sqrt(head_size)
+  int kv_hint;       // L2 policy for K/V tile loads: 0 normal, 1 evict_last
+  // Development tracing (nullptr in production): clock64 stamps of CTA 0's
+  // first kTraceTiles tiles, [event][tile]; see tools/trace_fa.py.
+  unsigned long long* trace;
 };
 
 }  // namespace uspb200

@@ -22,6 +22,9 @@
 //     (log-sum-exp merge) and/or writes bf16 O + natural-log LSE.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
+
+#include <type_traits>
 
 #include "fa_fwd.hpp"
 #include "ptx_sm100.cuh"
@@ -30,12 +33,22 @@ namespace uspb200 {
 
 using namespace ptx;
 
-template <int NQ, int HS>
+template <int NQ, int HS, int POLY>
 struct FwdCfg {
   static constexpr int kSoftmaxWarps = 4 * NQ;
   static constexpr int kTmaWarp = kSoftmaxWarps;
   static constexpr int kMmaWarp = kSoftmaxWarps + 1;
-  static constexpr int kThreads = 32 * (kSoftmaxWarps + 2);
+  // NQ == 2: a full third warpgroup (TMA, MMA, 2 idle warps) so registers
+  // can be moved to the softmax warpgroups with setmaxnreg.
+  static constexpr bool kRegSplit = NQ == 2;
+  static constexpr int kThreads = kRegSplit ? 32 * (kSoftmaxWarps + 4) : 32 * (kSoftmaxWarps + 2);
+  static constexpr int kSoftmaxRegs = 208;  // 8 x 208 + 4 x 88 = 384 x 168 (the launch allocation)
+  static constexpr int kProducerRegs = 88;
+  // setmaxnreg only redistributes the registers allocated at launch
+  // (384 threads x 168 under __launch_bounds__(384, 1)); asking for more
+  // would block the .inc forever.
+  static_assert(!kRegSplit || 8 * 32 * kSoftmaxRegs + 4 * 32 * kProducerRegs <= 384 * 168,
+                "register split exceeds the launch allocation");
   static constexpr int kSub = HS / 64;           // 128-byte (64 x bf16) column blocks
   static constexpr int kSubBytes = 128 * 128;    // one block: 128 rows x 128 B
   static constexpr int kQBytes = kTileM * HS * 2;
@@ -43,9 +56,10 @@ struct FwdCfg {
   static constexpr int kBudget = 227 * 1024 - 2048;
   static constexpr int kStagesFit = (kBudget - NQ * kQBytes) / kKVBytes;
   static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
-  static constexpr int kNumBars = 3 * NQ + 1 + NQ + 2 * kStages;
+  static constexpr int kSchedDepth = 4;  // unit-ticket ring between producer and consumers
+  static constexpr int kNumBars = 3 * NQ + 1 + NQ + 2 * kStages + 2 * kSchedDepth;
   static constexpr int kSmemBytes = 1024 /*align slack*/ + NQ * kQBytes + kStages * kKVBytes +
-                                    kNumBars * 8 + 16;
+                                    kNumBars * 8 + 16 + 4 * kSchedDepth;
   static constexpr uint32_t kColsUsed = NQ * 128 + NQ * HS;
   static constexpr uint32_t kTmemCols = kColsUsed <= 128 ? 128 : (kColsUsed <= 256 ? 256 : 512);
   static constexpr uint32_t kSCol = 0;          // S_t / P_t at t*128
@@ -54,10 +68,59 @@ struct FwdCfg {
   static_assert(kStages >= 2, "not enough shared memory for a K/V pipeline");
 };
 
-template <int NQ, int HS>
-__global__ void __launch_bounds__(FwdCfg<NQ, HS>::kThreads, 1)
+// Development trace: event ev of tile i, CTA 0 only.
+// `dep` orders the clock read after the value it depends on.
+__device__ __forceinline__ void trace_ev(const FwdParams& p, int ev, uint32_t i, float dep = 0.f) {
+  if (p.trace != nullptr && blockIdx.x == 0 && i < static_cast<uint32_t>(kTraceTiles)) {
+    unsigned long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c) : "f"(dep));
+    p.trace[ev * kTraceTiles + i] = c;
+  }
+}
+
+// tcgen05.commit from one elected lane of a converged warp.
+__device__ __forceinline__ void commit_one(uint64_t* bar) {
+  if (elect_one()) mma_commit(bar);
+  __syncwarp();
+}
+
+// Calls f(integral_constant<int, S>) with S == slot (slot < N): turns a
+// runtime pipeline-stage index into a compile-time smem offset.
+template <int N, class F>
+__device__ __forceinline__ void dispatch_slot(uint32_t slot, F&& f) {
+  if constexpr (N > 0) {
+    if (slot == N - 1)
+      f(std::integral_constant<int, N - 1>{});
+    else
+      dispatch_slot<N - 1>(slot, f);
+  }
+}
+
+// Consumer side of the unit-ticket ring: every consumer warp waits for slot
+// it % depth, reads the unit index, and one lane per warp releases the slot.
+// whole_warp: all 32 lanes run this (softmax warps); otherwise a single
+// lane (the MMA issuer) does.
+template <int kDepth>
+__device__ __forceinline__ int next_unit_impl(uint64_t* full, uint64_t* empty, const int* slot,
+                                              uint32_t it, bool whole_warp) {
+  const uint32_t d = it % kDepth;
+  mbar_wait(&full[d], (it / kDepth) & 1);
+  const int u = *reinterpret_cast<const volatile int*>(&slot[d]);
+  if (whole_warp) {
+    __syncwarp();
+    if (lane_id() == 0) mbar_arrive(&empty[d]);
+  } else {
+    mbar_arrive(&empty[d]);
+  }
+  return u;
+}
+#define next_unit(full, empty, slot, it, whole_warp) \
+  next_unit_impl<C::kSchedDepth>(full, empty, slot, it, whole_warp)
+
+template <int NQ, int HS, int POLY>
+__global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY>::kThreads, 1)
     fa_fwd_sm100_kernel(const __grid_constant__ FwdParams p) {
-  using C = FwdCfg<NQ, HS>;
+  using C = FwdCfg<NQ, HS, POLY>;
   constexpr int NS = C::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -72,7 +135,10 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS>::kThreads, 1)
   uint64_t* s_full = kv_empty + NS;     // [NQ]  MMA -> softmax
   uint64_t* p_ready = s_full + NQ;      // [NQ]  softmax -> MMA (128 arrivals)
   uint64_t* o_full = p_ready + NQ;      // [NQ]  MMA -> epilogue
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + NQ);
+  uint64_t* sched_full = o_full + NQ;           // [D] producer -> consumers
+  uint64_t* sched_empty = sched_full + C::kSchedDepth;  // [D] consumers -> producer
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sched_empty + C::kSchedDepth);
+  int* sched_slot = reinterpret_cast<int*>(tmem_slot + 4);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -85,6 +151,10 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS>::kThreads, 1)
       mbar_init(&o_full[t], 1);
     }
     mbar_init(q_empty, 1);
+    for (int d = 0; d < C::kSchedDepth; ++d) {
+      mbar_init(&sched_full[d], 1);
+      mbar_init(&sched_empty[d], 1 + C::kSoftmaxWarps);  // MMA thread + one lane per softmax warp
+    }
     for (int s = 0; s < NS; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
@@ -101,10 +171,15 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS>::kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // One CTA per SM (shared memory) owns all of TMEM, so the allocation
+  // starts at lane 0 / column 0; the MMA issue relies on that.
+  if (tmem != 0) __trap();
   const int group = p.heads / p.kv_heads;  // q heads per kv head (GQA)
 
   if (warp < C::kSoftmaxWarps) {
     // ------------------------------------------------------------ softmax
+    if constexpr (C::kRegSplit)
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::kSoftmaxRegs));
     const int t = warp >> 2;
     const int quarter = warp & 3;
     const int row_in_tile = quarter * 32 + lane;
@@ -113,7 +188,9 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS>::kThreads, 1)
     const uint32_t o_addr = lane_base + C::kOCol + t * HS;
     const float sl2 = p.scale_log2;
     uint32_t s_phase = 0, o_phase = 0;
-    for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+    for (uint32_t it = 0;; ++it) {
+      const int u = next_unit(sched_full, sched_empty, sched_slot, it, true);
+      if (u >= p.num_units) break;
       const uint32_t unit = p.units[u];
       const int qt = unit & 0xFFFF, hp = (unit >> 16) & 0xFF, b = unit >> 24;
       const int h = hp * NQ + t;
@@ -125,6 +202,8 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS>::kThreads, 1)
       for (int j = 0; j < n; ++j) {
         const int entry = p.tile_list[beg + j];
         mbar_wait(&s_full[t], s_phase & 1);
+        const bool tr = (warp & 3) == 0 && lane == 0;
+        if (tr) trace_ev(p, 0 + 5 * t, s_phase);
         ++s_phase;
         tc_fence_after();
         uint32_t s[128];
@@ -132,6 +211,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS>::kThreads, 1)
         for (int c = 0; c < 4; ++c) tmem_ld32(s_addr + c * 32, s + c * 32);
 #pragma unroll
         for (int c = 0; c < 4; ++c) tmem_ld_wait(s + c * 32);
+        if (tr) trace_ev(p, 1 + 5 * t, s_phase - 1, __uint_as_float(s[127]));
         if (entry < 0) {  // partial tile: apply the position mask per element
           const int kt = entry & 0x7FFFFFFF;
           const int4* kp4 = reinterpret_cast<const int4*>(p.k_pos + kt * kTileN);
@@ -154,6 +234,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS>::kThreads, 1)
           mx3 = fmaxf(mx3, __uint_as_float(s[i + 3]));
         }
         const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+        if (tr) trace_ev(p, 2 + 5 * t, s_phase - 1, mx);
         const float m_new = fmaxf(m_run, mx * sl2);
         float alpha = 1.f;
         if (m_run == -INFINITY) {
@@ -164,17 +245,42 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS>::kThreads, 1)
         }
         m_use = (m_run == -INFINITY) ? 0.f : m_run;
         const float neg = -m_use;
-        float sum0 = 0.f, sum1 = 0.f;
         // P = exp2(S*scale*log2e - m), packed to bf16 pairs in place: word i
-        // of s[] is rewritten only after s[2i], s[2i+1] were consumed.
+        // of s[] is rewritten only after s[2i], s[2i+1] were consumed. In
+        // full tiles POLY of every 8 pairs take the FMA-pipe polynomial
+        // exp2 instead of MUFU.EX2; partial tiles stay on MUFU (exact zeros
+        // for masked keys).
+        const float2 sc2 = make_float2(sl2, sl2), nb2 = make_float2(neg, neg);
+        float2 acc2 = make_float2(0.f, 0.f);
+        if (POLY > 0 && entry >= 0) {
 #pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          const float a = ex2(fmaf(__uint_as_float(s[2 * i]), sl2, neg));
-          const float c = ex2(fmaf(__uint_as_float(s[2 * i + 1]), sl2, neg));
-          sum0 += a;
-          sum1 += c;
-          s[i] = pack_bf16x2(a, c);
+          for (int i = 0; i < 64; ++i) {
+            const float2 x = ffma2(make_float2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])),
+                                   sc2, nb2);
+            float2 e;
+            if ((i & 7) >= 8 - POLY) {
+              e = exp2_poly2(x);
+            } else {
+              e.x = ex2(x.x);
+              e.y = ex2(x.y);
+            }
+            acc2 = fadd2(acc2, e);
+            s[i] = pack_bf16x2_pos(e.x, e.y);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 64; ++i) {
+            const float2 x = ffma2(make_float2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])),
+                                   sc2, nb2);
+            float2 e;
+            e.x = ex2(x.x);
+            e.y = ex2(x.y);
+            acc2 = fadd2(acc2, e);
+            s[i] = pack_bf16x2_pos(e.x, e.y);
+          }
         }
+        const float sum0 = acc2.x, sum1 = acc2.y;
+        if (tr) trace_ev(p, 3 + 5 * t, s_phase - 1, sum0 + sum1);
         l_run = l_run * alpha + (sum0 + sum1);
         tmem_st32(s_addr, s);
         tmem_st32(s_addr + 32, s + 32);
@@ -192,6 +298,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS>::kThreads, 1)
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&p_ready[t]);
+        if (tr) trace_ev(p, 4 + 5 * t, s_phase - 1);
       }
 
       // ------------------------------------------------------------ epilogue
@@ -270,12 +377,24 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS>::kThreads, 1)
           p.lse_acc[row] = lse_out;
       }
     }
-  } else if (warp == C::kTmaWarp) {
+  } else {
+    if constexpr (C::kRegSplit)
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(C::kProducerRegs));
+  if (warp == C::kTmaWarp) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       uint32_t kv_it = 0, q_it = 0;
       const uint64_t keep = l2_policy_evict_last();
-      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+      const bool hint = p.kv_hint == 1;
+      for (uint32_t it = 0;; ++it) {
+        // Claim the next unit (dynamic, longest-first) and hand it to the
+        // consumer roles through the ticket ring.
+        const int u = atomicAdd(&p.sched[0], 1);
+        const uint32_t d = it % C::kSchedDepth;
+        mbar_wait(&sched_empty[d], ((it / C::kSchedDepth) & 1) ^ 1);
+        sched_slot[d] = u;
+        mbar_arrive(&sched_full[d]);
+        if (u >= p.num_units) break;
         const uint32_t unit = p.units[u];
         const int qt = unit & 0xFFFF, hp = (unit >> 16) & 0xFF, b = unit >> 24;
         const int beg = p.tile_off[qt];
@@ -301,16 +420,23 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS>::kThreads, 1)
             mbar_arrive_expect_tx(&kv_full[slot], C::kKVBytes);
             const CUtensorMap* tm = which == 0 ? &p.tm_k : &p.tm_v;
 #pragma unroll
-            for (int sb = 0; sb < C::kSub; ++sb)
-              tma_load_4d_hint(sKV + slot * C::kKVBytes + sb * C::kSubBytes, tm, &kv_full[slot],
-                               sb * 64, kvh, kt * kTileN, b, keep);
+            for (int sb = 0; sb < C::kSub; ++sb) {
+              if (hint)
+                tma_load_4d_hint(sKV + slot * C::kKVBytes + sb * C::kSubBytes, tm, &kv_full[slot],
+                                 sb * 64, kvh, kt * kTileN, b, keep);
+              else
+                tma_load_4d(sKV + slot * C::kKVBytes + sb * C::kSubBytes, tm, &kv_full[slot],
+                            sb * 64, kvh, kt * kTileN, b);
+            }
           }
         }
       }
     }
   } else if (warp == C::kMmaWarp) {
     // ------------------------------------------------------------ MMA issue
-    if (lane == 0) {
+    // The whole warp runs this loop (converged, warp-uniform state); one
+    // elected lane issues each MMA chain / commit.
+    {
       constexpr uint32_t kIdescQK = idesc_bf16_f32(128, 128, 0, 0);
       constexpr uint32_t kIdescPV = idesc_bf16_f32(128, HS, 0, 1);
       const uint32_t sq = smem_u32(sQ), skv = smem_u32(sKV);
@@ -323,26 +449,46 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS>::kThreads, 1)
         mbar_wait(&kv_full[idx % NS], (idx / NS) & 1);
         tc_fence_after();
       };
+      // Descriptor bases (16-byte units in the low bits); the batched
+      // chains add the per-k-step offsets in PTX.
+      const uint64_t q_desc0 = smem_desc_sw128(sq, 16, 1024);
+      const uint64_t kv_desc0 = smem_desc_sw128(skv, 16, 1024);
+      const uint64_t v_desc0 = smem_desc_sw128(skv, C::kSubBytes, 1024);
+      // Every MMA operand below is a uniform base plus a compile-time offset
+      // (TMEM base is 0 — checked at kernel start — and the stage index is
+      // dispatched to a constant), so ptxas feeds UTCHMMA straight from
+      // uniform registers: no per-instruction R2UR / ELECT loop.
       auto issue_qk = [&](int t, uint32_t slot) {
-#pragma unroll
-        for (int kk = 0; kk < HS / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * C::kSubBytes + (kk & 3) * 32;
-          const uint64_t ad = smem_desc_sw128(sq + t * C::kQBytes + off, 16, 1024);
-          const uint64_t bd = smem_desc_sw128(skv + slot * C::kKVBytes + off, 16, 1024);
-          mma_ss(tmem + C::kSCol + t * 128, ad, bd, kIdescQK, kk > 0 ? 1u : 0u);
-        }
+        dispatch_slot<NS>(slot, [&](auto S) {
+          constexpr int sl = decltype(S)::value;
+          const uint64_t ad = q_desc0 + static_cast<uint64_t>((t * C::kQBytes) >> 4);
+          const uint64_t bd = kv_desc0 + static_cast<uint64_t>((sl * C::kKVBytes) >> 4);
+          if (elect_one()) {
+            if constexpr (HS == 128)
+              mma_qk_hs128(C::kSCol + t * 128, ad, bd, kIdescQK, 0u);
+            else
+              mma_qk_hs64(C::kSCol + t * 128, ad, bd, kIdescQK, 0u);
+          }
+          __syncwarp();
+        });
       };
       auto issue_pv = [&](int t, uint32_t slot, bool acc) {
-#pragma unroll
-        for (int kk = 0; kk < kTileN / 16; ++kk) {
-          const uint64_t bd =
-              smem_desc_sw128(skv + slot * C::kKVBytes + kk * 2048, C::kSubBytes, 1024);
-          mma_ts(tmem + C::kOCol + t * HS, tmem + C::kSCol + t * 128 + kk * 8, bd, kIdescPV,
-                 (acc || kk > 0) ? 1u : 0u);
-        }
+        dispatch_slot<NS>(slot, [&](auto S) {
+          constexpr int sl = decltype(S)::value;
+          const uint64_t bd = v_desc0 + static_cast<uint64_t>((sl * C::kKVBytes) >> 4);
+          if (elect_one()) {
+            if (acc)
+              mma_pv_chain(C::kOCol + t * HS, C::kSCol + t * 128, bd, kIdescPV, 1u);
+            else
+              mma_pv_chain(C::kOCol + t * HS, C::kSCol + t * 128, bd, kIdescPV, 0u);
+          }
+          __syncwarp();
+        });
       };
 
-      for (int u = blockIdx.x; u < p.num_units; u += gridDim.x) {
+      for (uint32_t it = 0;; ++it) {
+        const int u = next_unit(sched_full, sched_empty, sched_slot, it, true);
+        if (u >= p.num_units) break;
         const int qt = p.units[u] & 0xFFFF;
         const int n = p.tile_off[qt + 1] - p.tile_off[qt];
         if (n == 0) continue;
@@ -355,10 +501,10 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS>::kThreads, 1)
 #pragma unroll
         for (int t = 0; t < NQ; ++t) {
           issue_qk(t, k0 % NS);
-          mma_commit(&s_full[t]);
+          commit_one(&s_full[t]);
         }
-        mma_commit(&kv_empty[k0 % NS]);
-        if (n == 1) mma_commit(q_empty);
+        commit_one(&kv_empty[k0 % NS]);
+        if (n == 1) commit_one(q_empty);
         for (int j = 0; j < n; ++j) {
           const uint32_t vi = kv_it + 2 * j + 1;
           const uint32_t kn = kv_it + 2 * j + 2;
@@ -366,28 +512,39 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS>::kThreads, 1)
 #pragma unroll
           for (int t = 0; t < NQ; ++t) {
             mbar_wait(&p_ready[t], p_phase[t] & 1);
+            if (lane == 0) trace_ev(p, 10 + 2 * t, p_phase[t]);
             ++p_phase[t];
             tc_fence_after();
             issue_pv(t, vi % NS, j > 0);
             if (j + 1 < n) {
               if (t == 0) wait_full(kn);
               issue_qk(t, kn % NS);
-              mma_commit(&s_full[t]);
+              if (lane == 0) trace_ev(p, 11 + 2 * t, p_phase[t] - 1);
+              commit_one(&s_full[t]);
             }
           }
-          mma_commit(&kv_empty[vi % NS]);
+          commit_one(&kv_empty[vi % NS]);
           if (j + 1 < n) {
-            mma_commit(&kv_empty[kn % NS]);
-            if (j + 2 == n) mma_commit(q_empty);
+            commit_one(&kv_empty[kn % NS]);
+            if (j + 2 == n) commit_one(q_empty);
           }
         }
 #pragma unroll
-        for (int t = 0; t < NQ; ++t) mma_commit(&o_full[t]);
+        for (int t = 0; t < NQ; ++t) commit_one(&o_full[t]);
         kv_it += 2 * n;
       }
     }
   }
 
+  }  // producer warpgroup
+  if (warp == C::kTmaWarp && lane == 0) {
+    // The last CTA to finish claiming resets the tickets for the next launch.
+    if (atomicAdd(&p.sched[1], 1) == static_cast<int>(gridDim.x) - 1) {
+      p.sched[0] = 0;
+      p.sched[1] = 0;
+      __threadfence();
+    }
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -395,10 +552,10 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS>::kThreads, 1)
 }
 
 // --------------------------------------------------------------- launchers
-template <int NQ, int HS>
+template <int NQ, int HS, int POLY>
 static cudaError_t launch_impl(const FwdParams& p, int grid, cudaStream_t stream) {
-  using C = FwdCfg<NQ, HS>;
-  auto kern = fa_fwd_sm100_kernel<NQ, HS>;
+  using C = FwdCfg<NQ, HS, POLY>;
+  auto kern = fa_fwd_sm100_kernel<NQ, HS, POLY>;
   static bool attr_set = false;  // per instantiation; set before first launch
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -410,14 +567,33 @@ static cudaError_t launch_impl(const FwdParams& p, int grid, cudaStream_t stream
   return cudaGetLastError();
 }
 
+// Fraction of softmax exponentials on the FMA-pipe polynomial: POLY/8.
+static int poly_setting() {
+  static int v = [] {
+    const char* e = getenv("USP_FA_POLY");
+    return e ? atoi(e) : 2;
+  }();
+  return v;
+}
+
+template <int NQ, int HS>
+static cudaError_t launch_poly(const FwdParams& p, int grid, cudaStream_t stream) {
+  switch (poly_setting()) {
+    case 0: return launch_impl<NQ, HS, 0>(p, grid, stream);
+    case 3: return launch_impl<NQ, HS, 3>(p, grid, stream);
+    case 4: return launch_impl<NQ, HS, 4>(p, grid, stream);
+    default: return launch_impl<NQ, HS, 2>(p, grid, stream);
+  }
+}
+
 cudaError_t launch_fa_fwd(const FwdParams& p, int nq, int hs, int grid, cudaStream_t stream) {
-  if (nq == 2 && hs == 128) return launch_impl<2, 128>(p, grid, stream);
-  if (nq == 1 && hs == 128) return launch_impl<1, 128>(p, grid, stream);
-  if (nq == 2 && hs == 64) return launch_impl<2, 64>(p, grid, stream);
-  if (nq == 1 && hs == 64) return launch_impl<1, 64>(p, grid, stream);
+  if (nq == 2 && hs == 128) return launch_poly<2, 128>(p, grid, stream);
+  if (nq == 1 && hs == 128) return launch_poly<1, 128>(p, grid, stream);
+  if (nq == 2 && hs == 64) return launch_poly<2, 64>(p, grid, stream);
+  if (nq == 1 && hs == 64) return launch_poly<1, 64>(p, grid, stream);
   return cudaErrorInvalidValue;
 }
 
-int fa_fwd_threads(int nq) { return 32 * (4 * nq + 2); }
+int fa_fwd_threads(int nq) { return nq == 2 ? 32 * 12 : 32 * 6; }
 
 }  // namespace uspb200

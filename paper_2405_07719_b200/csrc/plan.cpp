@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <numeric>
 #include <sstream>
 
@@ -171,7 +172,8 @@ int64_t visible_pairs(const std::vector<int64_t>& q_pos, const std::vector<int64
 }
 
 StepPlan plan_step(const std::vector<int64_t>& q_pos, const std::vector<int64_t>& k_pos,
-                   bool causal, int64_t batch, int head_pairs, bool include_empty) {
+                   bool causal, int64_t batch, int head_pairs, bool include_empty,
+                   int pairs_per_kv) {
   StepPlan p;
   p.q_len = static_cast<int>(q_pos.size());
   p.k_len = static_cast<int>(k_pos.size());
@@ -220,18 +222,31 @@ StepPlan plan_step(const std::vector<int64_t>& q_pos, const std::vector<int64_t>
     }
     p.tile_off[qt + 1] = static_cast<int32_t>(p.tile_list.size());
   }
-  // Work units in longest-processing-time-first order; ties broken by
-  // (q tile, batch, head pair) so CTAs that start together share K/V tiles.
+  // Work units in longest-processing-time-first order. Order 1 (default)
+  // is kv-head-major: all CTAs resident at a time stream the SAME kv head's
+  // K/V tiles, so each tile is fetched from HBM about once per wave and
+  // re-read from L2 by the other CTAs; within a kv head, units go longest
+  // first (LPT) so the static round-robin assignment stays balanced.
+  // Order 0 is plain LPT over (q tile, batch, head pair).
+  static const int order = [] {
+    const char* e = std::getenv("USP_UNIT_ORDER");
+    return e ? std::atoi(e) : 1;
+  }();
   struct U {
-    int cost, qt, b, hp;
+    int cost, qt, b, hp, kvh;
   };
   std::vector<U> us;
   for (int qt = 0; qt < p.n_q_tiles; ++qt) {
     if (cost[qt] == 0 && !include_empty) continue;
     for (int64_t b = 0; b < batch; ++b)
-      for (int hp = 0; hp < head_pairs; ++hp) us.push_back({cost[qt], qt, static_cast<int>(b), hp});
+      for (int hp = 0; hp < head_pairs; ++hp)
+        us.push_back({cost[qt], qt, static_cast<int>(b), hp, hp / std::max(pairs_per_kv, 1)});
   }
   std::stable_sort(us.begin(), us.end(), [](const U& a, const U& b) {
+    if (order == 1) {
+      if (a.b != b.b) return a.b < b.b;
+      if (a.kvh != b.kvh) return a.kvh < b.kvh;
+    }
     if (a.cost != b.cost) return a.cost > b.cost;
     if (a.qt != b.qt) return a.qt < b.qt;
     if (a.b != b.b) return a.b < b.b;

@@ -86,8 +86,12 @@ struct StepPlan {
 // visible (BlockMask::none). include_empty keeps query tiles with no visible
 // key tile in the unit list (needed by first/last ring steps so every row is
 // written). head_pairs = local q heads / NQ.
+// pairs_per_kv = head pairs sharing one kv head (GQA group / NQ); the unit
+// order keeps CTAs that run concurrently on the same kv head (L2 reuse of
+// the streamed K/V tiles) — see plan.cpp.
 StepPlan plan_step(const std::vector<int64_t>& q_pos, const std::vector<int64_t>& k_pos,
-                   bool causal, int64_t batch, int head_pairs, bool include_empty);
+                   bool causal, int64_t batch, int head_pairs, bool include_empty,
+                   int pairs_per_kv = 1);
 
 // Exact unmasked (q, k) pair count of one block, summed over the block
 // (causal_pair_counts semantics, partition.cpp:52-72) — for FLOP accounting.

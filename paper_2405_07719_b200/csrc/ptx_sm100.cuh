@@ -21,6 +21,17 @@ __device__ __forceinline__ uint32_t lane_id() {
   return l;
 }
 
+// One lane of a converged warp (elect.sync); the others get false.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // ---------------------------------------------------------------- mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
@@ -52,9 +63,13 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar_addr, uint32_t parity
   return ok != 0;
 }
 // Blocks until the phase with the given parity has completed.
+// A pipeline deadlock traps (the launch fails with an error) instead of
+// hanging the GPU; the bound is far beyond any legitimate wait.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
+  uint32_t spins = 0;
   while (!mbar_try_wait(a, parity)) {
+    if (++spins == (1u << 28)) __trap();
   }
 }
 
@@ -131,6 +146,82 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// ---- batched MMA issue: one asm block per K/V tile and Q tile, so the
+// compiler converts the operands to uniform registers once per block
+// instead of once per instruction (issue overhead was the MMA warp's limit).
+// S[128 x 128] (+)= Q[128 x HS] K[128 x HS]^T over HS/16 k-steps. Descriptors
+// advance 32 B inside a 128-byte swizzle row and 16 KB to the next 64-column
+// block (units of 16 bytes in the descriptor's start-address field).
+__device__ __forceinline__ void mma_qk_hs128(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p0, p1;\n\t.reg .b64 ra, rb;\n\t"
+      "setp.ne.b32 p0, %4, 0;\n\t"
+      "setp.eq.u32 p1, 1, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p0;\n\t"
+      "add.s64 ra, %1, 2;\n\tadd.s64 rb, %2, 2;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 4;\n\tadd.s64 rb, %2, 4;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 6;\n\tadd.s64 rb, %2, 6;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 1024;\n\tadd.s64 rb, %2, 1024;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 1026;\n\tadd.s64 rb, %2, 1026;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 1028;\n\tadd.s64 rb, %2, 1028;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 1030;\n\tadd.s64 rb, %2, 1030;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "}"
+      ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_qk_hs64(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p0, p1;\n\t.reg .b64 ra, rb;\n\t"
+      "setp.ne.b32 p0, %4, 0;\n\t"
+      "setp.eq.u32 p1, 1, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p0;\n\t"
+      "add.s64 ra, %1, 2;\n\tadd.s64 rb, %2, 2;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 4;\n\tadd.s64 rb, %2, 4;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 6;\n\tadd.s64 rb, %2, 6;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "}"
+      ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// O[128 x N] (+)= P[128 x 128] V[128 x N]: P (bf16) from TMEM, 8 columns per
+// 16-key step; V MN-major, 16 rows (2 KB) per step.
+__device__ __forceinline__ void mma_pv_chain(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p0, p1;\n\t.reg .b64 rb;\n\t.reg .b32 ta;\n\t"
+      "setp.ne.b32 p0, %4, 0;\n\t"
+      "setp.eq.u32 p1, 1, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p0;\n\t"
+      "add.u32 ta, %1, 8;\n\tadd.s64 rb, %2, 128;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], rb, %3, p1;\n\t"
+      "add.u32 ta, %1, 16;\n\tadd.s64 rb, %2, 256;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], rb, %3, p1;\n\t"
+      "add.u32 ta, %1, 24;\n\tadd.s64 rb, %2, 384;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], rb, %3, p1;\n\t"
+      "add.u32 ta, %1, 32;\n\tadd.s64 rb, %2, 512;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], rb, %3, p1;\n\t"
+      "add.u32 ta, %1, 40;\n\tadd.s64 rb, %2, 640;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], rb, %3, p1;\n\t"
+      "add.u32 ta, %1, 48;\n\tadd.s64 rb, %2, 768;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], rb, %3, p1;\n\t"
+      "add.u32 ta, %1, 56;\n\tadd.s64 rb, %2, 896;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], rb, %3, p1;\n\t"
+      "}"
+      ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // Arrives on `bar` once every previously issued tcgen05 op of this thread has
 // completed (implies tcgen05.fence::before_thread_sync).
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -208,6 +299,61 @@ __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+// Packed fp32x2 arithmetic (sm_100 FFMA2 / FADD2): one issue slot per pair.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\t"
+      "mov.b64 rb, {%4, %5};\n\t"
+      "mov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\t"
+      "mov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\t"
+      "mov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\t"
+      "mov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+// 2^x on the FMA pipe for a pair (x <= ~126, clamped below at -127):
+// 2^x = 2^round(x) * p(r), r = x - round(x) in [-0.5, 0.5], p a degree-3
+// minimax polynomial (max rel. error 7.7e-5, below bf16's 3.9e-3). Offloads
+// a fraction of the softmax exponentials from the 16/clk/SM MUFU unit.
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
+  const float2 t = fadd2(x, magic);                           // round(x) in the low bits
+  const float2 f = fadd2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 r = fadd2(x, make_float2(-f.x, -f.y));
+  float2 p = ffma2(make_float2(0.05508876592f, 0.05508876592f), r,
+                   make_float2(0.24260465801f, 0.24260465801f));
+  p = ffma2(p, r, make_float2(0.69327628613f, 0.69327628613f));
+  p = ffma2(p, r, make_float2(0.99992889166f, 0.99992889166f));
+  const uint32_t bx = __float_as_uint(p.x) + (__float_as_uint(t.x) << 23);
+  const uint32_t by = __float_as_uint(p.y) + (__float_as_uint(t.y) << 23);
+  return make_float2(__uint_as_float(bx), __uint_as_float(by));
+}
+// bf16x2 packing of two NON-NEGATIVE finite floats on the integer pipes:
+// round half up (+0x8000 on the bit pattern; differs from RNE only at exact
+// ties) and keep the high halves with one PRMT. cvt.rn.bf16x2.f32 (F2FP)
+// issues on the same 16-lane/clk/SM pipe as MUFU.EX2, so in the softmax it
+// would compete with the exponentials.
+__device__ __forceinline__ uint32_t pack_bf16x2_pos(float lo, float hi) {
+  const uint32_t a = __float_as_uint(lo) + 0x8000u;
+  const uint32_t b = __float_as_uint(hi) + 0x8000u;
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
 }
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;

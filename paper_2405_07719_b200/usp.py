@@ -283,6 +283,19 @@ class UspAttention:
     def last_launches(self) -> int:
         return int(lib().usp_engine_last_launches(self._h))
 
+    def enable_timing(self, on: bool = True) -> None:
+        """Record CUDA events around every attention-kernel launch."""
+        check(lib().usp_engine_enable_timing(self._h, int(on)))
+
+    def kernel_times(self) -> list[float]:
+        """Durations (ms) of the attention launches since the last call."""
+        cap = 1 << 16
+        buf = (ctypes.c_float * cap)()
+        n = int(lib().usp_engine_kernel_times(self._h, buf, cap))
+        if n < 0:
+            check(3)
+        return list(buf[:min(n, cap)])
+
     def _check_tensors(self, q, k, v, out, lse):
         import torch
 
