@@ -571,7 +571,7 @@ static cudaError_t launch_impl(const FwdParams& p, int grid, cudaStream_t stream
 static int poly_setting() {
   static int v = [] {
     const char* e = getenv("USP_FA_POLY");
-    return e ? atoi(e) : 2;
+    return e ? atoi(e) : 0;
   }();
   return v;
 }
@@ -582,7 +582,8 @@ static cudaError_t launch_poly(const FwdParams& p, int grid, cudaStream_t stream
     case 0: return launch_impl<NQ, HS, 0>(p, grid, stream);
     case 3: return launch_impl<NQ, HS, 3>(p, grid, stream);
     case 4: return launch_impl<NQ, HS, 4>(p, grid, stream);
-    default: return launch_impl<NQ, HS, 2>(p, grid, stream);
+    case 2: return launch_impl<NQ, HS, 2>(p, grid, stream);
+    default: return launch_impl<NQ, HS, 0>(p, grid, stream);
   }
 }
 
