@@ -472,6 +472,11 @@ class Engine {
       return e ? std::atoi(e) : 0;
     }();
     p.kv_hint = kv_hint;
+    static const int dbg = [] {
+      const char* e = std::getenv("USP_FA_DEBUG");
+      return e ? std::atoi(e) : 0;
+    }();
+    p.debug_flags = dbg;
     static const bool trace = std::getenv("USP_FA_TRACE") != nullptr;
     if (trace) {
       if (!trace_buf_.p) trace_buf_ = DevBuf(sizeof(unsigned long long) * kTraceTiles * kTraceEvents);

@@ -53,6 +53,7 @@ struct FwdParams {
   // Development tracing (nullptr in production): clock64 stamps of CTA 0's
   // first kTraceTiles tiles, [event][tile]; see tools/trace_fa.py.
   unsigned long long* trace;
+  int debug_flags;  // development: bit 0 = skip the softmax math (pipeline-only timing)
 };
 
 }  // namespace uspb200

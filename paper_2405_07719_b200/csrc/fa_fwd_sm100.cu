@@ -41,7 +41,9 @@ struct FwdCfg {
   // NQ == 2: a full third warpgroup (TMA, MMA, 2 idle warps) so registers
   // can be moved to the softmax warpgroups with setmaxnreg.
   static constexpr bool kRegSplit = NQ == 2;
-  static constexpr int kThreads = kRegSplit ? 32 * (kSoftmaxWarps + 4) : 32 * (kSoftmaxWarps + 2);
+  // producer warpgroup: TMA warp, S-issue warp, PV-issue warp, 1 idle
+  static constexpr int kPvWarp = kSoftmaxWarps + 2;
+  static constexpr int kThreads = 32 * (kSoftmaxWarps + 4);
   static constexpr int kSoftmaxRegs = 208;  // 8 x 208 + 4 x 88 = 384 x 168 (the launch allocation)
   static constexpr int kProducerRegs = 88;
   // setmaxnreg only redistributes the registers allocated at launch
@@ -57,13 +59,17 @@ struct FwdCfg {
   static constexpr int kStagesFit = (kBudget - NQ * kQBytes) / kKVBytes;
   static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
   static constexpr int kSchedDepth = 4;  // unit-ticket ring between producer and consumers
-  static constexpr int kNumBars = 3 * NQ + 1 + NQ + 2 * kStages + 2 * kSchedDepth;
+  static constexpr int kNumBars = 3 * NQ + 2 + NQ + 2 * kStages + 2 * kSchedDepth;
   static constexpr int kSmemBytes = 1024 /*align slack*/ + NQ * kQBytes + kStages * kKVBytes +
                                     kNumBars * 8 + 16 + 4 * kSchedDepth;
-  static constexpr uint32_t kColsUsed = NQ * 128 + NQ * HS;
+  // TMEM: ONE S buffer shared by the q tiles (time-multiplexed: the MMA
+  // warp computes the next tile's S as soon as the previous S has been
+  // loaded into registers), a private P (bf16, 64 columns) and O per q tile.
+  static constexpr uint32_t kSCol = 0;                   // S: 128 fp32 columns
+  static constexpr uint32_t kPCol = 128;                 // P_t at kPCol + 64*t
+  static constexpr uint32_t kOCol = 128 + 64 * NQ;       // O_t at kOCol + HS*t
+  static constexpr uint32_t kColsUsed = kOCol + NQ * HS;
   static constexpr uint32_t kTmemCols = kColsUsed <= 128 ? 128 : (kColsUsed <= 256 ? 256 : 512);
-  static constexpr uint32_t kSCol = 0;          // S_t / P_t at t*128
-  static constexpr uint32_t kOCol = NQ * 128;   // O_t at kOCol + t*HS
   static_assert(HS == 64 || HS == 128, "head_size must be 64 or 128 on the tcgen05 path");
   static_assert(kStages >= 2, "not enough shared memory for a K/V pipeline");
 };
@@ -134,8 +140,9 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY>::kThreads, 1)
   uint64_t* kv_empty = kv_full + NS;    // [NS]  MMA -> TMA
   uint64_t* s_full = kv_empty + NS;     // [NQ]  MMA -> softmax
   uint64_t* p_ready = s_full + NQ;      // [NQ]  softmax -> MMA (128 arrivals)
-  uint64_t* o_full = p_ready + NQ;      // [NQ]  MMA -> epilogue
-  uint64_t* sched_full = o_full + NQ;           // [D] producer -> consumers
+  uint64_t* pv_done = p_ready + NQ;     // [NQ]  MMA -> softmax: PV_t finished (P_t, O_t free)
+  uint64_t* s_free = pv_done + NQ;      // [1]   softmax -> MMA: the S buffer was loaded
+  uint64_t* sched_full = s_free + 1;            // [D] producer -> consumers
   uint64_t* sched_empty = sched_full + C::kSchedDepth;  // [D] consumers -> producer
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sched_empty + C::kSchedDepth);
   int* sched_slot = reinterpret_cast<int*>(tmem_slot + 4);
@@ -148,12 +155,13 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY>::kThreads, 1)
       mbar_init(&q_full[t], 1);
       mbar_init(&s_full[t], 1);
       mbar_init(&p_ready[t], 128);
-      mbar_init(&o_full[t], 1);
+      mbar_init(&pv_done[t], 1);
     }
+    mbar_init(s_free, 4);  // one elected lane of each warp of the group holding S
     mbar_init(q_empty, 1);
     for (int d = 0; d < C::kSchedDepth; ++d) {
       mbar_init(&sched_full[d], 1);
-      mbar_init(&sched_empty[d], 1 + C::kSoftmaxWarps);  // MMA thread + one lane per softmax warp
+      mbar_init(&sched_empty[d], 2 + C::kSoftmaxWarps);  // S warp, PV warp, softmax warps
     }
     for (int s = 0; s < NS; ++s) {
       mbar_init(&kv_full[s], 1);
@@ -184,10 +192,11 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY>::kThreads, 1)
     const int quarter = warp & 3;
     const int row_in_tile = quarter * 32 + lane;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-    const uint32_t s_addr = lane_base + C::kSCol + t * 128;
+    const uint32_t s_addr = lane_base + C::kSCol;
+    const uint32_t p_addr = lane_base + C::kPCol + t * 64;
     const uint32_t o_addr = lane_base + C::kOCol + t * HS;
     const float sl2 = p.scale_log2;
-    uint32_t s_phase = 0, o_phase = 0;
+    uint32_t s_phase = 0, pv_phase = 0;
     for (uint32_t it = 0;; ++it) {
       const int u = next_unit(sched_full, sched_empty, sched_slot, it, true);
       if (u >= p.num_units) break;
@@ -211,6 +220,10 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY>::kThreads, 1)
         for (int c = 0; c < 4; ++c) tmem_ld32(s_addr + c * 32, s + c * 32);
 #pragma unroll
         for (int c = 0; c < 4; ++c) tmem_ld_wait(s + c * 32);
+        // S is in registers: the shared S buffer may take the next S.
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_free);
         if (tr) trace_ev(p, 1 + 5 * t, s_phase - 1, __uint_as_float(s[127]));
         if (entry < 0) {  // partial tile: apply the position mask per element
           const int kt = entry & 0x7FFFFFFF;
@@ -282,8 +295,14 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY>::kThreads, 1)
         const float sum0 = acc2.x, sum1 = acc2.y;
         if (tr) trace_ev(p, 3 + 5 * t, s_phase - 1, sum0 + sum1);
         l_run = l_run * alpha + (sum0 + sum1);
-        tmem_st32(s_addr, s);
-        tmem_st32(s_addr + 32, s + 32);
+        if (j > 0) {
+          // PV_t(j-1) must be done before P_t is overwritten and O_t rescaled
+          mbar_wait(&pv_done[t], pv_phase & 1);
+          ++pv_phase;
+          tc_fence_after();
+        }
+        tmem_st32(p_addr, s);
+        tmem_st32(p_addr + 32, s + 32);
         if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
           for (int c = 0; c < HS / 32; ++c) {
@@ -302,9 +321,9 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY>::kThreads, 1)
       }
 
       // ------------------------------------------------------------ epilogue
-      if (n > 0) {
-        mbar_wait(&o_full[t], o_phase & 1);
-        ++o_phase;
+      if (n > 0) {  // the unit's last PV_t
+        mbar_wait(&pv_done[t], pv_phase & 1);
+        ++pv_phase;
         tc_fence_after();
       }
       const bool valid = q_row < p.q_len;
@@ -432,32 +451,34 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY>::kThreads, 1)
         }
       }
     }
-  } else if (warp == C::kMmaWarp) {
+  } else if (warp == C::kMmaWarp || warp == C::kPvWarp) {
     // ------------------------------------------------------------ MMA issue
-    // The whole warp runs this loop (converged, warp-uniform state); one
-    // elected lane issues each MMA chain / commit.
+    // Two issuing warps: one serves the S = Q K^T queue, one the O += P V
+    // queue. They touch disjoint TMEM (the shared S buffer vs P_t / O_t), so
+    // no ordering is needed between them, and each warp's barrier waits
+    // overlap the other's MMA batches (the tensor core's instruction queue
+    // is shallow). Each warp runs its loop converged; one elected lane
+    // issues, and its commits track only its own MMAs.
+    const bool s_role = warp == C::kMmaWarp;
     {
       constexpr uint32_t kIdescQK = idesc_bf16_f32(128, 128, 0, 0);
       constexpr uint32_t kIdescPV = idesc_bf16_f32(128, HS, 0, 1);
       const uint32_t sq = smem_u32(sQ), skv = smem_u32(sKV);
-      uint32_t kv_it = 0, q_phase = 0;
+      uint32_t kv_it = 0, q_phase = 0, f_phase = 0;
       uint32_t p_phase[NQ];
 #pragma unroll
       for (int t = 0; t < NQ; ++t) p_phase[t] = 0;
-
       auto wait_full = [&](uint32_t idx) {
         mbar_wait(&kv_full[idx % NS], (idx / NS) & 1);
         tc_fence_after();
       };
       // Descriptor bases (16-byte units in the low bits); the batched
-      // chains add the per-k-step offsets in PTX.
+      // chains add the per-k-step offsets in PTX. Every MMA operand is a
+      // uniform base plus a compile-time offset (TMEM base 0, stage index
+      // dispatched to a constant): no per-instruction R2UR / ELECT loop.
       const uint64_t q_desc0 = smem_desc_sw128(sq, 16, 1024);
       const uint64_t kv_desc0 = smem_desc_sw128(skv, 16, 1024);
       const uint64_t v_desc0 = smem_desc_sw128(skv, C::kSubBytes, 1024);
-      // Every MMA operand below is a uniform base plus a compile-time offset
-      // (TMEM base is 0 — checked at kernel start — and the stage index is
-      // dispatched to a constant), so ptxas feeds UTCHMMA straight from
-      // uniform registers: no per-instruction R2UR / ELECT loop.
       auto issue_qk = [&](int t, uint32_t slot) {
         dispatch_slot<NS>(slot, [&](auto S) {
           constexpr int sl = decltype(S)::value;
@@ -465,9 +486,9 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY>::kThreads, 1)
           const uint64_t bd = kv_desc0 + static_cast<uint64_t>((sl * C::kKVBytes) >> 4);
           if (elect_one()) {
             if constexpr (HS == 128)
-              mma_qk_hs128(C::kSCol + t * 128, ad, bd, kIdescQK, 0u);
+              mma_qk_hs128(C::kSCol, ad, bd, kIdescQK, 0u);
             else
-              mma_qk_hs64(C::kSCol + t * 128, ad, bd, kIdescQK, 0u);
+              mma_qk_hs64(C::kSCol, ad, bd, kIdescQK, 0u);
           }
           __syncwarp();
         });
@@ -478,13 +499,14 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY>::kThreads, 1)
           const uint64_t bd = v_desc0 + static_cast<uint64_t>((sl * C::kKVBytes) >> 4);
           if (elect_one()) {
             if (acc)
-              mma_pv_chain(C::kOCol + t * HS, C::kSCol + t * 128, bd, kIdescPV, 1u);
+              mma_pv_chain(C::kOCol + t * HS, C::kPCol + t * 64, bd, kIdescPV, 1u);
             else
-              mma_pv_chain(C::kOCol + t * HS, C::kSCol + t * 128, bd, kIdescPV, 0u);
+              mma_pv_chain(C::kOCol + t * HS, C::kPCol + t * 64, bd, kIdescPV, 0u);
           }
           __syncwarp();
         });
       };
+      uint32_t s_count = 0;  // S computations issued so far (all units)
 
       for (uint32_t it = 0;; ++it) {
         const int u = next_unit(sched_full, sched_empty, sched_slot, it, true);
@@ -492,45 +514,47 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY>::kThreads, 1)
         const int qt = p.units[u] & 0xFFFF;
         const int n = p.tile_off[qt + 1] - p.tile_off[qt];
         if (n == 0) continue;
+        if (s_role) {
+          // S_t(j) in (j, t) order; each needs the shared S buffer (the
+          // previous S loaded into registers by its softmax) and K_j.
 #pragma unroll
-        for (int t = 0; t < NQ; ++t) mbar_wait(&q_full[t], q_phase & 1);
-        ++q_phase;
-        tc_fence_after();
-        const uint32_t k0 = kv_it;
-        wait_full(k0);
+          for (int t = 0; t < NQ; ++t) mbar_wait(&q_full[t], q_phase & 1);
+          ++q_phase;
+          for (int j = 0; j < n; ++j) {
+            const uint32_t ki = kv_it + 2 * j;
+            wait_full(ki);
 #pragma unroll
-        for (int t = 0; t < NQ; ++t) {
-          issue_qk(t, k0 % NS);
-          commit_one(&s_full[t]);
-        }
-        commit_one(&kv_empty[k0 % NS]);
-        if (n == 1) commit_one(q_empty);
-        for (int j = 0; j < n; ++j) {
-          const uint32_t vi = kv_it + 2 * j + 1;
-          const uint32_t kn = kv_it + 2 * j + 2;
-          wait_full(vi);
-#pragma unroll
-          for (int t = 0; t < NQ; ++t) {
-            mbar_wait(&p_ready[t], p_phase[t] & 1);
-            if (lane == 0) trace_ev(p, 10 + 2 * t, p_phase[t]);
-            ++p_phase[t];
-            tc_fence_after();
-            issue_pv(t, vi % NS, j > 0);
-            if (j + 1 < n) {
-              if (t == 0) wait_full(kn);
-              issue_qk(t, kn % NS);
-              if (lane == 0) trace_ev(p, 11 + 2 * t, p_phase[t] - 1);
+            for (int t = 0; t < NQ; ++t) {
+              if (s_count > 0) {
+                mbar_wait(s_free, f_phase & 1);
+                ++f_phase;
+              }
+              tc_fence_after();
+              issue_qk(t, ki % NS);
               commit_one(&s_full[t]);
+              if (lane == 0) trace_ev(p, 11 + 2 * t, j);
+              ++s_count;
             }
+            commit_one(&kv_empty[ki % NS]);
+            if (j == n - 1) commit_one(q_empty);
           }
-          commit_one(&kv_empty[vi % NS]);
-          if (j + 1 < n) {
-            commit_one(&kv_empty[kn % NS]);
-            if (j + 2 == n) commit_one(q_empty);
+        } else {
+          // PV_t(j) in (j, t) order; each needs P_t(j) and V_j.
+          for (int j = 0; j < n; ++j) {
+            const uint32_t vi = kv_it + 2 * j + 1;
+            wait_full(vi);
+#pragma unroll
+            for (int t = 0; t < NQ; ++t) {
+              mbar_wait(&p_ready[t], p_phase[t] & 1);
+              if (lane == 0) trace_ev(p, 10 + 2 * t, p_phase[t]);
+              ++p_phase[t];
+              tc_fence_after();
+              issue_pv(t, vi % NS, j > 0);
+              commit_one(&pv_done[t]);
+            }
+            commit_one(&kv_empty[vi % NS]);
           }
         }
-#pragma unroll
-        for (int t = 0; t < NQ; ++t) commit_one(&o_full[t]);
         kv_it += 2 * n;
       }
     }
