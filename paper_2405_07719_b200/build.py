@@ -30,8 +30,9 @@ def nvcc() -> str:
 
 
 def _flags() -> list[str]:
+    extra = ["-DUSPB_TRACE"] if os.environ.get("USPB_TRACE_BUILD") else []
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
-                   "-I", os.path.join(ROOT, "include"), "-I", CSRC, "--expt-relaxed-constexpr"]
+                   "-I", os.path.join(ROOT, "include"), "-I", CSRC, "--expt-relaxed-constexpr"] + extra
 
 
 def _compile(src: str) -> str:

@@ -74,9 +74,15 @@ struct FwdCfg {
   static_assert(kStages >= 2, "not enough shared memory for a K/V pipeline");
 };
 
-// Development trace: event ev of tile i, CTA 0 only.
+// Development trace: event ev of tile i, CTA 0 only. Compiled in only with
+// -DUSPB_TRACE (tools/trace_fa.py builds that variant); the production
+// kernel carries no instrumentation (it costs issue slots and I-cache).
 // `dep` orders the clock read after the value it depends on.
 __device__ __forceinline__ void trace_ev(const FwdParams& p, int ev, uint32_t i, float dep = 0.f) {
+#ifndef USPB_TRACE
+  (void)p, (void)ev, (void)i, (void)dep;
+  return;
+#endif
   if (p.trace != nullptr && blockIdx.x == 0 && i < static_cast<uint32_t>(kTraceTiles)) {
     unsigned long long c;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(c) : "f"(dep));
