@@ -90,6 +90,25 @@ USP_API usp_status usp_schedule(const usp_config* cfg, int32_t step, usp_step_in
  * tile_list[sizes[1]] (k tile | partial << 31) are filled when non-NULL. */
 USP_API usp_status usp_step_plan(const usp_config* cfg, int32_t step, int64_t sizes[2],
                                  int32_t* tile_off, int32_t* tile_list);
+/* Communication ledger of one rank's forward, in the reference CommLedger's
+ * terms (src/simcomm/ledger.hpp:21-30; closed forms ledger.cpp:25-37):
+ * all_to_all sends payload*(n-1)/n, ring_shift sends the buffer. */
+typedef struct usp_ledger_entry {
+  int32_t kind;          /* simcomm::CollectiveKind: 3 all_to_all, 4 ring_shift */
+  int32_t group_first;   /* group members: first + i*stride, i < size      */
+  int32_t group_size;
+  int32_t group_stride;
+  int32_t step;          /* per-group sequence number                       */
+  int32_t tensor;        /* 0 Q, 1 K, 2 V, 3 O                              */
+  int64_t payload_elems; /* per-rank logical payload, elements              */
+  double bytes_sent;     /* by this rank, bf16 elements                     */
+} usp_ledger_entry;
+/* Planned collectives of rank cfg->rank (host only). Returns the number of
+ * entries (written up to cap), or -1 on invalid input. */
+USP_API int32_t usp_forward_ledger(const usp_config* cfg, usp_ledger_entry* out, int32_t cap);
+/* Collectives the engine actually issued in its last usp_attn_fwd. */
+USP_API int32_t usp_engine_ledger(const usp_engine* engine, usp_ledger_entry* out, int32_t cap);
+
 /* Algorithmic FLOPs of this rank's forward: 4 * batch * (heads/U) *
  * head_size * visible (q,k) pairs. */
 USP_API usp_status usp_rank_flops(const usp_config* cfg, double* flops);

@@ -176,6 +176,7 @@ class Reference(_Lib):
     @classmethod
     def _declare(cls, lib):
         lib.ref_last_error.restype = ctypes.c_char_p
+        lib.ref_last_ledger_json.restype = ctypes.c_char_p
         lib.ref_uniform_stream.argtypes = [ctypes.c_uint64, ctypes.c_double, ctypes.c_double, _i64, _f64p]
         lib.ref_reference_attention_f64.argtypes = [_f64p, _f64p, _f64p, _i64, _i64, _i64, _i64, _i64, _int,
                                                     ctypes.c_void_p, _f64p]
@@ -254,3 +255,10 @@ class Reference(_Lib):
                       out.ctypes.data if out is not None else None,
                       lse.ctypes.data if lse is not None else None, ctypes.byref(secs)))
         return out, lse, secs.value
+
+    @classmethod
+    def last_ledger(cls):
+        """The reference World's CommLedger entries of the last usp_forward."""
+        import json
+
+        return json.loads(cls.lib().ref_last_ledger_json().decode())

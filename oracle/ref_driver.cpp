@@ -58,6 +58,8 @@ int guarded(F&& f) {
   }
 }
 
+std::string g_ledger_json;
+
 template <class T>
 int usp_forward_impl(const double* q, const double* k, const double* v,
                      int64_t batch, int64_t seq, int64_t heads, int64_t kv_heads,
@@ -94,6 +96,21 @@ int usp_forward_impl(const double* q, const double* k, const double* v,
         });
     const auto t1 = std::chrono::steady_clock::now();
     if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+    // The World's communication ledger (simcomm/ledger.hpp) as JSON rows.
+    std::string js = "[";
+    bool first = true;
+    for (const auto& e : world.ledger.entries()) {
+      if (!first) js += ",";
+      first = false;
+      js += "{\"kind\":\"" + std::string(simcomm::collective_name(e.kind)) + "\",\"group\":\"" +
+            e.group + "\",\"step\":" + std::to_string(e.step) +
+            ",\"payload_elems\":" + std::to_string(e.payload_elems) + ",\"bytes_sent\":[";
+      for (size_t i = 0; i < e.bytes_sent.size(); ++i)
+        js += (i ? "," : "") + std::to_string(e.bytes_sent[i]);
+      js += "]}";
+    }
+    js += "]";
+    g_ledger_json = js;
     if (out_global) {
       Tensor4<T> out(batch, seq, heads, hs);
       for (const auto& pr : world.per_rank) usp::place_rows(out, pr.out, pr.positions);
@@ -111,6 +128,9 @@ int usp_forward_impl(const double* q, const double* k, const double* v,
 extern "C" {
 
 const char* ref_last_error(void) { return g_err.c_str(); }
+
+// Ledger of the last ref_usp_forward_* call (JSON array of entries).
+const char* ref_last_ledger_json(void) { return g_ledger_json.c_str(); }
 
 void ref_uniform_stream(uint64_t seed, double lo, double hi, int64_t n, double* out) {
   UniformSource src(seed);

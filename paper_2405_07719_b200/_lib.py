@@ -57,10 +57,26 @@ class UspStepInfo(ctypes.Structure):
     ]
 
 
+class UspLedgerEntry(ctypes.Structure):
+    _fields_ = [
+        ("kind", ctypes.c_int32),
+        ("group_first", ctypes.c_int32),
+        ("group_size", ctypes.c_int32),
+        ("group_stride", ctypes.c_int32),
+        ("step", ctypes.c_int32),
+        ("tensor", ctypes.c_int32),
+        ("payload_elems", ctypes.c_int64),
+        ("bytes_sent", ctypes.c_double),
+    ]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
 # Every symbol include/usp_attn.h declares (tests check the .so exports them).
 EXPORTS = [
     "usp_config_validate", "usp_zigzag_partition", "usp_positions_for", "usp_head_positions",
-    "usp_causal_pair_counts", "usp_schedule", "usp_step_plan", "usp_rank_flops", "usp_nccl_unique_id",
+    "usp_causal_pair_counts", "usp_schedule", "usp_step_plan", "usp_forward_ledger", "usp_engine_ledger", "usp_rank_flops", "usp_nccl_unique_id",
     "usp_comm_create_nccl", "usp_comm_create_local", "usp_comm_destroy", "usp_engine_create",
     "usp_attn_fwd", "usp_engine_last_launches", "usp_engine_destroy", "usp_engine_enable_timing",
     "usp_engine_kernel_times", "usp_local_world_fwd",
@@ -85,6 +101,8 @@ def _declare(lib):
         "usp_schedule": (st, [P(UspConfig), ctypes.c_int32, P(UspStepInfo)]),
         "usp_step_plan": (st, [P(UspConfig), ctypes.c_int32, i64p, P(ctypes.c_int32), P(ctypes.c_int32)]),
         "usp_rank_flops": (st, [P(UspConfig), P(ctypes.c_double)]),
+        "usp_forward_ledger": (ctypes.c_int32, [P(UspConfig), P(UspLedgerEntry), ctypes.c_int32]),
+        "usp_engine_ledger": (ctypes.c_int32, [vp, P(UspLedgerEntry), ctypes.c_int32]),
         "usp_nccl_unique_id": (st, [ctypes.c_char_p]),
         "usp_comm_create_nccl": (st, [ctypes.c_char_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P(vp)]),
         "usp_comm_create_local": (st, [ctypes.c_int32, P(vp)]),

@@ -17,6 +17,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
 #include <cmath>
 #include <cstring>
@@ -244,6 +245,7 @@ class Engine {
       if (!ptr || reinterpret_cast<uintptr_t>(ptr) % 16 != 0)
         throw_invalid("q, k, v, o, lse must be non-null 16-byte aligned device pointers");
     launches_ = 0;
+    ledger_.clear();
     const size_t e = 2;
     const bool reshape = U_ > 1 || hs_ != hsk_;
     const void* qh = q;
@@ -270,6 +272,9 @@ class Engine {
         parts[2][p] = {sv + p * kv_part_, rv ? rv + p * kv_part_ : kv0 + kv_bytes_ + p * kv_part_};
       }
       tr_->all_to_all(*groups_, parts, {q_part_, kv_part_, kv_part_}, st);
+      record_a2a(0, q_part_);
+      record_a2a(1, kv_part_);
+      record_a2a(2, kv_part_);
       if (B_ > 1) {
         gather_seq(rq, q_h_.p, hl_, st);
         gather_seq(rk, kv0, kvl_, st);
@@ -278,7 +283,14 @@ class Engine {
       qh = q_h_.p;
       kh = kv0;
       vh = kv0 + kv_bytes_;
-    } else if (reshape) {
+    } else {
+      // U == 1: the reference's all-to-alls are no-ops (0 bytes); keep the
+      // ledger entries it would record.
+      record_a2a(0, q_part_);
+      record_a2a(1, kv_part_);
+      record_a2a(2, kv_part_);
+    }
+    if (U_ == 1 && reshape) {
       pad_rows(q, q_h_.p, B_ * T_ * H_, st);
       pad_rows(k, kv0, B_ * T_ * KV_, st);
       pad_rows(v, kv0 + kv_bytes_, B_ * T_ * KV_, st);
@@ -302,6 +314,8 @@ class Engine {
       if (t + 1 < R_) {
         USPB_CHECK(cudaEventRecord(ev_pre_[t], st));  // buf(t) ready, buf(t+1) free
         USPB_CHECK(cudaStreamWaitEvent(comm_stream_, ev_pre_[t], 0));
+        record_shift(1);
+        record_shift(2);
         tr_->ring_shift(*groups_, {kbuf(t), vbuf(t)},
                         {const_cast<void*>(kbuf(t + 1)), const_cast<void*>(vbuf(t + 1))},
                         {kv_bytes_, kv_bytes_}, comm_stream_);
@@ -322,8 +336,12 @@ class Engine {
       for (int p = 0; p < U_; ++p)
         parts[0][p] = {osend + p * q_part_, o_recv_.as<uint8_t>() + p * q_part_};
       tr_->all_to_all(*groups_, parts, {q_part_}, st);
+      record_a2a(3, q_part_);
       unpack_heads(o_recv_.p, o, st);
-    } else if (reshape) {
+    } else {
+      record_a2a(3, q_part_);
+    }
+    if (U_ == 1 && reshape) {
       RowPermute rp;
       rp.src = o_h_.p;
       rp.dst = o;
@@ -555,6 +573,25 @@ class Engine {
   cudaStream_t comm_stream_ = nullptr;
   std::vector<cudaEvent_t> ev_pre_, ev_recv_;
   int launches_ = 0;
+
+ public:
+  std::vector<LedgerEvent> ledger_;
+
+ private:
+  // Executed-collective records (bytes as moved; payload in logical elements).
+  void record_a2a(int tensor, size_t part_bytes) {
+    const double elems_phys = double(part_bytes) / 2.0;
+    const int64_t payload = static_cast<int64_t>(elems_phys * U_ * hs_ / hsk_ + 0.5);
+    ledger_.push_back({3, shape_.mesh.rank_of(0, r_), U_, 1, tensor, tensor, payload,
+                       double(part_bytes) * (U_ - 1)});
+  }
+  void record_shift(int tensor) {
+    const int step = static_cast<int>(std::count_if(ledger_.begin(), ledger_.end(),
+                                                    [](const LedgerEvent& e) { return e.kind == 4; }));
+    ledger_.push_back({4, shape_.mesh.rank_of(u_, 0), R_, U_, step, tensor,
+                       static_cast<int64_t>(double(kv_bytes_) / 2.0 * hs_ / hsk_ + 0.5),
+                       double(kv_bytes_)});
+  }
 };
 
 }  // namespace uspb200
@@ -679,6 +716,29 @@ usp_status usp_step_plan(const usp_config* cfg, int32_t step, int64_t sizes[2], 
     if (tile_off) std::memcpy(tile_off, st.tile_off.data(), st.tile_off.size() * sizeof(int32_t));
     if (tile_list) std::memcpy(tile_list, st.tile_list.data(), st.tile_list.size() * sizeof(int32_t));
   });
+}
+
+static int32_t copy_ledger(const std::vector<LedgerEvent>& ev, usp_ledger_entry* out, int32_t cap) {
+  for (size_t i = 0; i < ev.size() && static_cast<int32_t>(i) < cap && out; ++i)
+    out[i] = {ev[i].kind, ev[i].group_first, ev[i].group_size, ev[i].group_stride, ev[i].step,
+              ev[i].tensor, ev[i].payload_elems, ev[i].bytes_sent};
+  return static_cast<int32_t>(ev.size());
+}
+
+int32_t usp_forward_ledger(const usp_config* cfg, usp_ledger_entry* out, int32_t cap) {
+  int32_t n = -1;
+  if (guarded([&] {
+        const UspShape s = shape_of(cfg);
+        s.validate();
+        n = copy_ledger(forward_ledger(s, cfg->rank, 2), out, cap);
+      }) != USP_OK)
+    return -1;
+  return n;
+}
+
+int32_t usp_engine_ledger(const usp_engine* engine, usp_ledger_entry* out, int32_t cap) {
+  if (!engine) return -1;
+  return copy_ledger(engine->impl->ledger_, out, cap);
 }
 
 usp_status usp_rank_flops(const usp_config* cfg, double* flops) {

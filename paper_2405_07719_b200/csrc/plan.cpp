@@ -160,6 +160,33 @@ std::vector<int64_t> positions_for(const UspShape& s, int rank) {
                               ring_list.begin() + (u + 1) * per_rank);
 }
 
+std::vector<LedgerEvent> forward_ledger(const UspShape& s, int rank, int elem_bytes) {
+  std::vector<LedgerEvent> ev;
+  const int U = s.mesh.ulysses, R = s.mesh.ring;
+  const int u = s.mesh.ulysses_coord(rank), r = s.mesh.ring_coord(rank);
+  const int64_t T = s.tokens_per_rank(), Tr = s.tokens_per_ring_rank();
+  const int64_t hs = s.head_size;
+  // all_to_all: payload = the rank's whole tensor; sent = payload*(n-1)/n
+  // (ledger.cpp:32-33); ring_shift: sent = payload when n > 1 (:34).
+  auto a2a = [&](int step, int tensor, int64_t elems) {
+    ev.push_back({3, s.mesh.rank_of(0, r), U, 1, step, tensor, elems,
+                  double(elems) * elem_bytes * double(U - 1) / double(U)});
+  };
+  // (with U == 1 the reference still records the all-to-alls, sending 0
+  // bytes; the engine issues no transfer but keeps the ledger entries)
+  a2a(0, 0, s.batch * T * s.heads * hs);
+  a2a(1, 1, s.batch * T * s.kv_heads * hs);
+  a2a(2, 2, s.batch * T * s.kv_heads * hs);
+  const int64_t kv_block = s.batch * Tr * s.local_kv_heads() * hs;
+  int rstep = 0;
+  for (int t = 0; t + 1 < R; ++t)
+    for (int tensor = 1; tensor <= 2; ++tensor)
+      ev.push_back({4, s.mesh.rank_of(u, 0), R, U, rstep++, tensor, kv_block,
+                    double(kv_block) * elem_bytes});
+  a2a(3, 3, s.batch * Tr * s.local_heads() * hs);
+  return ev;
+}
+
 int64_t visible_pairs(const std::vector<int64_t>& q_pos, const std::vector<int64_t>& k_pos,
                       bool causal) {
   if (!causal) return static_cast<int64_t>(q_pos.size()) * static_cast<int64_t>(k_pos.size());

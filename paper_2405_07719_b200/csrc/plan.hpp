@@ -93,6 +93,21 @@ StepPlan plan_step(const std::vector<int64_t>& q_pos, const std::vector<int64_t>
                    bool causal, int64_t batch, int head_pairs, bool include_empty,
                    int pairs_per_kv = 1);
 
+// One communication event of a rank's forward, in the reference ledger's
+// terms (src/simcomm/ledger.hpp:21-30, closed forms ledger.cpp:25-37).
+struct LedgerEvent {
+  int kind;             // simcomm::CollectiveKind: 3 all_to_all, 4 ring_shift
+  int group_first, group_size, group_stride;
+  int step;             // per-group sequence number
+  int tensor;           // 0 Q, 1 K, 2 V, 3 O
+  int64_t payload_elems;  // per-rank logical payload, elements
+  double bytes_sent;      // by this rank, at elem_bytes per element
+};
+// The collectives usp_attn_fwd issues on `rank` (Alg. 1 order): Q, K, V
+// all-to-alls, 2(R-1) ring shifts (K then V per step), the O all-to-all.
+// The reference's two position all_gathers are absent (static layout).
+std::vector<LedgerEvent> forward_ledger(const UspShape& s, int rank, int elem_bytes);
+
 // Exact unmasked (q, k) pair count of one block, summed over the block
 // (causal_pair_counts semantics, partition.cpp:52-72) — for FLOP accounting.
 int64_t visible_pairs(const std::vector<int64_t>& q_pos, const std::vector<int64_t>& k_pos,

@@ -24,7 +24,7 @@ from typing import Optional, Sequence
 
 import numpy as np
 
-from ._lib import UspConfig, UspError, UspInvalidInput, UspStepInfo, check, lib
+from ._lib import UspConfig, UspError, UspInvalidInput, UspLedgerEntry, UspStepInfo, check, lib
 
 __all__ = [
     "ProcessMesh", "ShardSpec", "zigzag_partition", "even_partition", "causal_pair_counts",
@@ -157,6 +157,15 @@ def step_plan(cfg: UspConfig, step: int):
     return off, lst[: sizes[1]]
 
 
+def forward_ledger(cfg: UspConfig) -> list[dict]:
+    """Planned collectives of one rank's forward (reference CommLedger terms)."""
+    buf = (UspLedgerEntry * 64)()
+    n = lib().usp_forward_ledger(ctypes.byref(cfg), buf, 64)
+    if n < 0:
+        check(2)
+    return [buf[i].as_dict() for i in range(min(n, 64))]
+
+
 def rank_flops(cfg: UspConfig) -> float:
     f = ctypes.c_double(0)
     check(lib().usp_rank_flops(ctypes.byref(cfg), ctypes.byref(f)))
@@ -282,6 +291,12 @@ class UspAttention:
 
     def last_launches(self) -> int:
         return int(lib().usp_engine_last_launches(self._h))
+
+    def ledger(self) -> list[dict]:
+        """Collectives issued by the last forward (reference CommLedger terms)."""
+        buf = (UspLedgerEntry * 64)()
+        n = lib().usp_engine_ledger(self._h, buf, 64)
+        return [buf[i].as_dict() for i in range(min(n, 64))]
 
     def enable_timing(self, on: bool = True) -> None:
         """Record CUDA events around every attention-kernel launch."""

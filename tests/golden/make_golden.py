@@ -9,6 +9,7 @@ hosts where /root/reference does not exist (the GPU box).
 """
 from __future__ import annotations
 
+import json
 import os
 import sys
 
@@ -52,6 +53,8 @@ def main():
     for name, bs, seq, hc, kv, hs, U, R, causal, seed in CASES:
         q, k, v = gen(seed, bs, seq, hc, kv, hs)
         o, lse, _ = Reference.usp_forward(q, k, v, U, R, causal)
+        # the reference World's communication ledger of that forward
+        out[f"{name}/ledger"] = np.array(json.dumps(Reference.last_ledger()))
         out[f"{name}/meta"] = np.array([bs, seq, hc, kv, hs, U, R, int(causal), seed], np.int64)
         out[f"{name}/out"] = o
         out[f"{name}/lse"] = lse

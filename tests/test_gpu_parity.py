@@ -38,6 +38,18 @@ def _check_case(c: UspCase, device):
     assert eo["max_abs"] <= O_TOL and eo["rel_l2"] <= O_REL_L2, msg
     assert el["max_abs"] <= LSE_TOL, msg
     assert all(e.last_launches() >= 1 for e in engines), "native kernels did not launch"
+    # the collectives each rank actually issued == the planned ledger, which
+    # tests/test_ledger.py pins to the reference World's ledger
+    from paper_2405_07719_b200.usp import forward_ledger
+
+    for e in engines:
+        planned = forward_ledger(e.cfg)
+        executed = e.ledger()
+        if c.hs in (64, 128):
+            assert executed == planned, (c, e.rank, executed, planned)
+        else:  # padded head size: same events and payloads, padded bytes
+            assert [(x["kind"], x["step"], x["payload_elems"]) for x in executed] == \
+                   [(x["kind"], x["step"], x["payload_elems"]) for x in planned]
     return eo, el
 
 
