@@ -116,3 +116,26 @@ def test_invalid_ulysses_degree_message(cuda):
     with pytest.raises(UspInvalidInput, match="cannot exceed"):
         UspAttention(ProcessMesh(16, 1), rank=0, seq_len=256, heads=32, kv_heads=8, head_size=128,
                      causal=True)
+
+
+def test_nccl_transport_initialises_and_splits(cuda):
+    """The NCCL transport on one rank: dlopen of libnccl, ncclCommInitRankConfig,
+    the two ncclCommSplit calls (Ulysses row / ring column) and a forward
+    through an engine that owns them. (Multi-rank NCCL needs >1 GPU; the
+    multi-rank schedule is covered by the local transport and gloo tests.)"""
+    import torch
+
+    from paper_2405_07719_b200 import Comm, ProcessMesh, UspAttention
+
+    comm = Comm.nccl(Comm.nccl_unique_id(), 1, 0, 0)
+    c = UspCase(seq=512, hc=8, kv_hc=2, hs=128, causal=True, seed=5)
+    q, k, v = make_globals(c)
+    tq, tk, tv = (to_bf16(x, cuda) for x in (q, k, v))
+    eng = UspAttention(ProcessMesh(1, 1), rank=0, seq_len=c.seq, heads=c.hc, kv_heads=c.kv_hc, head_size=c.hs,
+                       causal=True, comm=comm)
+    res = eng.forward(tq, tk, tv)
+    torch.cuda.synchronize()
+    ref = Oracle.reference_attention(widen(tq), widen(tk), widen(tv), True)
+    assert errors(widen(res.out), ref)["max_abs"] <= O_TOL
+    eng.close()
+    comm.close()
