@@ -99,14 +99,21 @@ typedef struct usp_ledger_entry {
   int32_t group_size;
   int32_t group_stride;
   int32_t step;          /* per-group sequence number                       */
-  int32_t tensor;        /* 0 Q, 1 K, 2 V, 3 O                              */
+  int32_t tensor;        /* 0 Q, 1 K, 2 V, 3 O, 4 dO, 5 dQ, 6 dK, 7 dV      */
   int64_t payload_elems; /* per-rank logical payload, elements              */
-  double bytes_sent;     /* by this rank, bf16 elements                     */
+  double bytes_sent;     /* by this rank: bf16 elements, fp32 for the
+                            circulating dK/dV partials                     */
 } usp_ledger_entry;
 /* Planned collectives of rank cfg->rank (host only). Returns the number of
  * entries (written up to cap), or -1 on invalid input. */
 USP_API int32_t usp_forward_ledger(const usp_config* cfg, usp_ledger_entry* out, int32_t cap);
-/* Collectives the engine actually issued in its last usp_attn_fwd. */
+/* Planned collectives of one rank's forward followed by its backward
+ * (usp_attention.cpp:68-89, ring_attention.cpp:79-155): the dO all-to-all,
+ * per ring step the K/V shifts (steps < R-1) and the circulating dK/dV
+ * partial shifts (steps >= 1), then the dQ, dK, dV all-to-alls. */
+USP_API int32_t usp_backward_ledger(const usp_config* cfg, usp_ledger_entry* out, int32_t cap);
+/* Collectives the engine actually issued in its last usp_attn_fwd (and the
+ * usp_attn_bwd that followed it, if any). */
 USP_API int32_t usp_engine_ledger(const usp_engine* engine, usp_ledger_entry* out, int32_t cap);
 
 /* Algorithmic FLOPs of this rank's forward: 4 * batch * (heads/U) *
@@ -135,7 +142,29 @@ USP_API usp_status usp_engine_create(const usp_config* cfg, usp_comm* comm, usp_
  * default stream). */
 USP_API usp_status usp_attn_fwd(usp_engine* engine, const void* q, const void* k, const void* v,
                         void* o, float* lse, void* stream);
-/* Launches of the engine's own kernels in the last usp_attn_fwd. */
+/* Backward of the engine's last usp_attn_fwd: the reference's
+ * usp_attention_backward<T> (src/usp/usp_attention.cpp:68-89) over
+ * ring_attention_backward (src/usp/ring_attention.cpp:79-155).
+ *   q, k, v, o : the tensors of the preceding usp_attn_fwd on this engine
+ *                (the head-sharded activations it saved are reused, as
+ *                UspForward carries them);
+ *   lse        : that forward's head-sharded logsumexp;
+ *   dout       : dO, sequence-sharded like o (bf16);
+ *   dq, dk, dv : bf16 gradients, sequence-sharded like q, k, v.
+ * dK/dV partials circulate the ring in fp32 and dQ accumulates in fp32; the
+ * casts to bf16 happen once at the end. Asynchronous on `stream`.
+ * USP_INVALID_INPUT when no forward preceded it. */
+USP_API usp_status usp_attn_bwd(usp_engine* engine, const void* q, const void* k, const void* v,
+                                const void* o, const float* lse, const void* dout, void* dq,
+                                void* dk, void* dv, void* stream);
+/* usp_attn_bwd on every rank of a local world (one host thread per rank). */
+USP_API usp_status usp_local_world_bwd(usp_engine* const* engines, int32_t world_size,
+                                       const void* const* q, const void* const* k,
+                                       const void* const* v, const void* const* o,
+                                       const float* const* lse, const void* const* dout,
+                                       void* const* dq, void* const* dk, void* const* dv,
+                                       void* const* streams);
+/* Launches of the engine's own kernels in the last usp_attn_fwd / _bwd. */
 USP_API int32_t usp_engine_last_launches(const usp_engine* engine);
 USP_API void usp_engine_destroy(usp_engine* engine);
 /* Optional per-launch timing of the attention kernel: CUDA events recorded

@@ -262,3 +262,66 @@ class Reference(_Lib):
         import json
 
         return json.loads(cls.lib().ref_last_ledger_json().decode())
+
+
+# ---- backward -------------------------------------------
+
+def _declare_bwd(lib, prefix):
+    fp, ip = _f64p, ctypes.c_void_p
+    if prefix == "uo":
+        lib.uo_reference_attention_grad.argtypes = [fp, fp, fp, fp, _i64, _i64, _i64, _i64, _i64, _int, ip,
+                                                    fp, fp, fp]
+        lib.uo_usp_backward.argtypes = [fp, fp, fp, fp, _i64, _i64, _i64, _i64, _i64, _int, _int, _int,
+                                        fp, fp, fp]
+    else:
+        lib.ref_reference_attention_grad_f64.argtypes = [fp, fp, fp, fp, _i64, _i64, _i64, _i64, _i64, _int, ip,
+                                                         fp, fp, fp]
+        lib.ref_usp_fwd_bwd_f64.argtypes = [fp, fp, fp, fp, _i64, _i64, _i64, _i64, _i64, _int, _int, _int,
+                                            fp, fp, fp]
+
+
+def _grad_call(fn, q, k, v, dout, causal, positions=None, mesh=None):
+    q, k, v, dout = _as(q), _as(k), _as(v), _as(dout)
+    b, s, h, d = q.shape
+    dq, dk, dv = np.empty_like(q), np.empty_like(k), np.empty_like(v)
+    if mesh is None:
+        pos = _as(positions, np.int64) if positions is not None else None
+        rc = fn(q, k, v, dout, b, s, h, k.shape[2], d, int(causal), pos.ctypes.data if pos is not None else None,
+                dq, dk, dv)
+    else:
+        rc = fn(q, k, v, dout, b, s, h, k.shape[2], d, mesh[0], mesh[1], int(causal), dq, dk, dv)
+    return rc, (dq, dk, dv)
+
+
+def oracle_reference_attention_grad(q, k, v, dout, causal, positions=None):
+    lib = Oracle.lib()
+    _declare_bwd(lib, "uo")
+    rc, g = _grad_call(lib.uo_reference_attention_grad, q, k, v, dout, causal, positions)
+    if rc != 0:
+        raise ValueError("bad attention shapes")
+    return g
+
+
+def oracle_usp_backward(q, k, v, dout, ulysses, ring, causal):
+    lib = Oracle.lib()
+    _declare_bwd(lib, "uo")
+    rc, g = _grad_call(lib.uo_usp_backward, q, k, v, dout, causal, mesh=(ulysses, ring))
+    if rc != 0:
+        raise ValueError("usp constraint violated")
+    return g
+
+
+def reference_attention_grad(q, k, v, dout, causal, positions=None):
+    lib = Reference.lib()
+    _declare_bwd(lib, "ref")
+    rc, g = _grad_call(lib.ref_reference_attention_grad_f64, q, k, v, dout, causal, positions)
+    Reference._check(rc)
+    return g
+
+
+def reference_usp_fwd_bwd(q, k, v, dout, ulysses, ring, causal):
+    lib = Reference.lib()
+    _declare_bwd(lib, "ref")
+    rc, g = _grad_call(lib.ref_usp_fwd_bwd_f64, q, k, v, dout, causal, mesh=(ulysses, ring))
+    Reference._check(rc)
+    return g

@@ -60,6 +60,23 @@ int guarded(F&& f) {
 
 std::string g_ledger_json;
 
+// The World's communication ledger (simcomm/ledger.hpp) as JSON rows.
+template <class Ledger>
+std::string ledger_json(const Ledger& ledger) {
+  std::string js = "[";
+  bool first = true;
+  for (const auto& e : ledger.entries()) {
+    if (!first) js += ",";
+    first = false;
+    js += "{\"kind\":\"" + std::string(simcomm::collective_name(e.kind)) + "\",\"group\":\"" +
+          e.group + "\",\"step\":" + std::to_string(e.step) +
+          ",\"payload_elems\":" + std::to_string(e.payload_elems) + ",\"bytes_sent\":[";
+    for (size_t i = 0; i < e.bytes_sent.size(); ++i) js += (i ? "," : "") + std::to_string(e.bytes_sent[i]);
+    js += "]}";
+  }
+  return js + "]";
+}
+
 template <class T>
 int usp_forward_impl(const double* q, const double* k, const double* v,
                      int64_t batch, int64_t seq, int64_t heads, int64_t kv_heads,
@@ -96,21 +113,7 @@ int usp_forward_impl(const double* q, const double* k, const double* v,
         });
     const auto t1 = std::chrono::steady_clock::now();
     if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
-    // The World's communication ledger (simcomm/ledger.hpp) as JSON rows.
-    std::string js = "[";
-    bool first = true;
-    for (const auto& e : world.ledger.entries()) {
-      if (!first) js += ",";
-      first = false;
-      js += "{\"kind\":\"" + std::string(simcomm::collective_name(e.kind)) + "\",\"group\":\"" +
-            e.group + "\",\"step\":" + std::to_string(e.step) +
-            ",\"payload_elems\":" + std::to_string(e.payload_elems) + ",\"bytes_sent\":[";
-      for (size_t i = 0; i < e.bytes_sent.size(); ++i)
-        js += (i ? "," : "") + std::to_string(e.bytes_sent[i]);
-      js += "]}";
-    }
-    js += "]";
-    g_ledger_json = js;
+    g_ledger_json = ledger_json(world.ledger);
     if (out_global) {
       Tensor4<T> out(batch, seq, heads, hs);
       for (const auto& pr : world.per_rank) usp::place_rows(out, pr.out, pr.positions);
@@ -222,3 +225,62 @@ int ref_usp_forward_f32(const double* q, const double* k, const double* v, int64
 }
 
 }  // extern "C"
+
+// Forward + backward (src/api/commands.cpp:108-121 minus the report):
+// global dq, dk, dv in original token order.
+extern "C" int ref_usp_fwd_bwd_f64(const double* q, const double* k, const double* v,
+                                   const double* dout, int64_t batch, int64_t seq, int64_t heads,
+                                   int64_t kv_heads, int64_t hs, int ulysses, int ring, int causal,
+                                   double* dq_g, double* dk_g, double* dv_g) {
+  return guarded([&] {
+    const simcomm::ProcessMesh mesh(ulysses, ring);
+    const usp::ShardSpec shard(mesh, seq, /*zigzag=*/causal != 0);
+    const auto gq = make<double>(q, batch, seq, heads, hs);
+    const auto gk = make<double>(k, batch, seq, kv_heads, hs);
+    const auto gv = make<double>(v, batch, seq, kv_heads, hs);
+    const auto gdo = make<double>(dout, batch, seq, heads, hs);
+    struct PerRank {
+      Tensor4<double> dq, dk, dv;
+      std::vector<int64_t> positions;
+    };
+    auto world = simcomm::World::run<PerRank>(mesh.world_size(), [&](simcomm::RankCtx& ctx) {
+      const auto positions = shard.positions_for(ctx.rank());
+      const auto q_s = usp::extract_rows(gq, positions);
+      const auto k_s = usp::extract_rows(gk, positions);
+      const auto v_s = usp::extract_rows(gv, positions);
+      const auto do_s = usp::extract_rows(gdo, positions);
+      auto fwd = usp::usp_attention(ctx, mesh, q_s, k_s, v_s, positions, causal != 0);
+      auto g = usp::usp_attention_backward(ctx, mesh, fwd, do_s, causal != 0);
+      return PerRank{std::move(g.dq), std::move(g.dk), std::move(g.dv), positions};
+    });
+    g_ledger_json = ledger_json(world.ledger);
+    Tensor4<double> dq(batch, seq, heads, hs), dk(batch, seq, kv_heads, hs), dv(batch, seq, kv_heads, hs);
+    for (const auto& pr : world.per_rank) {
+      usp::place_rows(dq, pr.dq, pr.positions);
+      usp::place_rows(dk, pr.dk, pr.positions);
+      usp::place_rows(dv, pr.dv, pr.positions);
+    }
+    unload(dq, dq_g);
+    unload(dk, dk_g);
+    unload(dv, dv_g);
+  });
+}
+
+extern "C" int ref_reference_attention_grad_f64(const double* q, const double* k, const double* v,
+                                                const double* dout, int64_t batch, int64_t seq,
+                                                int64_t heads, int64_t kv_heads, int64_t hs,
+                                                int causal, const int64_t* positions, double* dq,
+                                                double* dk, double* dv) {
+  return guarded([&] {
+    const auto tq = make<double>(q, batch, seq, heads, hs);
+    const auto tk = make<double>(k, batch, seq, kv_heads, hs);
+    const auto tv = make<double>(v, batch, seq, kv_heads, hs);
+    const auto td = make<double>(dout, batch, seq, heads, hs);
+    std::span<const int64_t> pos;
+    if (positions) pos = std::span<const int64_t>(positions, static_cast<size_t>(seq));
+    const auto g = numerics::reference_attention_grad(tq, tk, tv, td, causal != 0, pos);
+    unload(g.dq, dq);
+    unload(g.dk, dk);
+    unload(g.dv, dv);
+  });
+}

@@ -359,3 +359,240 @@ int uo_usp_forward(const double* q, const double* k, const double* v,
   free(oh);
   return 0;
 }
+
+/* ---------------------------------------------------------------------- */
+/* backward                                               */
+
+int uo_reference_attention_grad(const double* q, const double* k, const double* v,
+                                const double* dout, int64_t batch, int64_t seq,
+                                int64_t heads, int64_t kv_heads, int64_t hs, int causal,
+                                const int64_t* positions, double* dq, double* dk,
+                                double* dv) {
+  /* reference_attention_grad (attention.cpp:95-170), same loop order */
+  if (kv_heads <= 0 || heads % kv_heads != 0) return -1;
+  const int64_t heads_per_kv = heads / kv_heads;
+  const double inv_scale = 1.0 / sqrt((double)hs);
+  memset(dq, 0, sizeof(double) * (size_t)(batch * seq * heads * hs));
+  memset(dk, 0, sizeof(double) * (size_t)(batch * seq * kv_heads * hs));
+  memset(dv, 0, sizeof(double) * (size_t)(batch * seq * kv_heads * hs));
+  double* p = (double*)malloc(sizeof(double) * (size_t)seq);
+  double* dp = (double*)malloc(sizeof(double) * (size_t)seq);
+  for (int64_t b = 0; b < batch; ++b) {
+    for (int64_t i = 0; i < seq; ++i) {
+      const int64_t qp = positions ? positions[i] : i;
+      for (int64_t h = 0; h < heads; ++h) {
+        const int64_t kv_h = h / heads_per_kv;
+        const double* q_row = q + ((b * seq + i) * heads + h) * hs;
+        const double* do_row = dout + ((b * seq + i) * heads + h) * hs;
+        double row_max = -INFINITY; /* :126-131 */
+        for (int64_t j = 0; j < seq; ++j) {
+          if (causal && (positions ? positions[j] : j) > qp) continue;
+          p[j] = dot_d(q_row, k + ((b * seq + j) * kv_heads + kv_h) * hs, hs) * inv_scale;
+          row_max = max_d(row_max, p[j]);
+        }
+        double norm = 0; /* :132-140 */
+        for (int64_t j = 0; j < seq; ++j) {
+          if (causal && (positions ? positions[j] : j) > qp) {
+            p[j] = 0;
+            continue;
+          }
+          p[j] = exp(p[j] - row_max);
+          norm += p[j];
+        }
+        double pdp = 0; /* :142-151 */
+        for (int64_t j = 0; j < seq; ++j) {
+          if (p[j] == 0.0) {
+            dp[j] = 0;
+            continue;
+          }
+          p[j] /= norm;
+          dp[j] = dot_d(do_row, v + ((b * seq + j) * kv_heads + kv_h) * hs, hs);
+          pdp += p[j] * dp[j];
+        }
+        double* dq_row = dq + ((b * seq + i) * heads + h) * hs; /* :153-165 */
+        for (int64_t j = 0; j < seq; ++j) {
+          if (p[j] == 0.0) continue;
+          const double ds = p[j] * (dp[j] - pdp) * inv_scale;
+          const double* k_row = k + ((b * seq + j) * kv_heads + kv_h) * hs;
+          double* dk_row = dk + ((b * seq + j) * kv_heads + kv_h) * hs;
+          double* dv_row = dv + ((b * seq + j) * kv_heads + kv_h) * hs;
+          for (int64_t s = 0; s < hs; ++s) {
+            dq_row[s] += ds * k_row[s];
+            dk_row[s] += ds * q_row[s];
+            dv_row[s] += p[j] * do_row[s];
+          }
+        }
+      }
+    }
+  }
+  free(p);
+  free(dp);
+  return 0;
+}
+
+/* attention_block_backward (attention.cpp:282-324): dq accumulates,
+ * dk_blk / dv_blk are zeroed by the caller. */
+static void block_backward(const double* q, const double* k, const double* v,
+                           const double* dout, const double* delta, const double* lse,
+                           int64_t batch, int64_t q_len, int64_t k_len, int64_t heads,
+                           int64_t kv_heads, int64_t hs, int causal, const int64_t* q_pos,
+                           const int64_t* k_pos, double* dq, double* dk, double* dv) {
+  const int64_t heads_per_kv = heads / kv_heads;
+  const double inv_scale = 1.0 / sqrt((double)hs);
+  for (int64_t b = 0; b < batch; ++b)
+    for (int64_t i = 0; i < q_len; ++i)
+      for (int64_t h = 0; h < heads; ++h) {
+        const int64_t kv_h = h / heads_per_kv;
+        const size_t r = (size_t)((b * q_len + i) * heads + h);
+        const double* q_row = q + r * (size_t)hs;
+        const double* do_row = dout + r * (size_t)hs;
+        double* dq_row = dq + r * (size_t)hs;
+        for (int64_t j = 0; j < k_len; ++j) {
+          if (causal && k_pos[j] > q_pos[i]) continue;
+          const double* k_row = k + ((b * k_len + j) * kv_heads + kv_h) * hs;
+          const double* v_row = v + ((b * k_len + j) * kv_heads + kv_h) * hs;
+          const double s = dot_d(q_row, k_row, hs) * inv_scale;
+          const double p = exp(s - lse[r]);
+          const double dp = dot_d(do_row, v_row, hs);
+          const double ds = p * (dp - delta[r]) * inv_scale;
+          double* dk_row = dk + ((b * k_len + j) * kv_heads + kv_h) * hs;
+          double* dv_row = dv + ((b * k_len + j) * kv_heads + kv_h) * hs;
+          for (int64_t x = 0; x < hs; ++x) {
+            dq_row[x] += ds * k_row[x];
+            dk_row[x] += ds * q_row[x];
+            dv_row[x] += p * do_row[x];
+          }
+        }
+      }
+}
+
+int uo_usp_backward(const double* q, const double* k, const double* v, const double* dout,
+                    int64_t batch, int64_t seq, int64_t heads, int64_t kv_heads, int64_t hs,
+                    int ulysses, int ring, int causal, double* dq_g, double* dk_g,
+                    double* dv_g) {
+  /* usp_attention_backward (usp_attention.cpp:68-89) after the forward
+   * (:43-65), over every rank of the mesh; ring_attention_backward's
+   * circulation (ring_attention.cpp:79-155) is replayed in the same
+   * summation order so the result is bitwise the reference's. */
+  if (kv_heads % ulysses != 0 || ulysses > kv_heads || heads % ulysses != 0) return -1;
+  if (heads % kv_heads != 0) return -1;
+  if (causal && seq % (2 * ring) != 0) return -1;
+  if (seq % ring != 0 || (seq / ring) % ulysses != 0) return -1;
+  const int64_t per_ring = seq / ring;
+  const int64_t hl = heads / ulysses, kvl = kv_heads / ulysses;
+  int64_t* lists = (int64_t*)malloc(sizeof(int64_t) * (size_t)seq);
+  if (causal) uo_zigzag_partition(seq, ring, lists);
+  else uo_even_partition(seq, ring, lists);
+  const size_t qsz = (size_t)(batch * per_ring * hl * hs), ksz = (size_t)(batch * per_ring * kvl * hs);
+  const size_t rows = (size_t)(batch * per_ring * hl);
+  double* qh = (double*)malloc(sizeof(double) * qsz * ring);
+  double* oh = (double*)malloc(sizeof(double) * qsz * ring);
+  double* doh = (double*)malloc(sizeof(double) * qsz * ring);
+  double* dqh = (double*)calloc(qsz * ring, sizeof(double));
+  double* lse = (double*)malloc(sizeof(double) * rows * ring);
+  double* delta = (double*)malloc(sizeof(double) * rows * ring);
+  double* kh = (double*)malloc(sizeof(double) * ksz * ring);
+  double* vh = (double*)malloc(sizeof(double) * ksz * ring);
+  double* contrib_k = (double*)malloc(sizeof(double) * ksz * ring * ring); /* [rank r][block src] */
+  double* contrib_v = (double*)malloc(sizeof(double) * ksz * ring * ring);
+  for (int u = 0; u < ulysses; ++u) {
+    for (int r = 0; r < ring; ++r) {
+      const int64_t* pos = lists + (int64_t)r * per_ring;
+      for (int64_t b = 0; b < batch; ++b)
+        for (int64_t t = 0; t < per_ring; ++t) {
+          for (int64_t h = 0; h < hl; ++h) {
+            const size_t dst = (size_t)r * qsz + (size_t)(((b * per_ring + t) * hl + h) * hs);
+            const size_t src = (size_t)(((b * seq + pos[t]) * heads + u * hl + h) * hs);
+            memcpy(qh + dst, q + src, sizeof(double) * (size_t)hs);
+            memcpy(doh + dst, dout + src, sizeof(double) * (size_t)hs);
+          }
+          for (int64_t h = 0; h < kvl; ++h) {
+            const size_t dst = (size_t)r * ksz + (size_t)(((b * per_ring + t) * kvl + h) * hs);
+            const size_t src = (size_t)(((b * seq + pos[t]) * kv_heads + u * kvl + h) * hs);
+            memcpy(kh + dst, k + src, sizeof(double) * (size_t)hs);
+            memcpy(vh + dst, v + src, sizeof(double) * (size_t)hs);
+          }
+        }
+    }
+    /* forward per ring rank: out_heads + logsumexp */
+    for (int r = 0; r < ring; ++r) {
+      sm_state st;
+      sm_init(&st, batch, per_ring, hl, hs);
+      for (int step = 0; step < ring; ++step) {
+        const int src = (r - step + ring) % ring;
+        sm_update(&st, qh + (size_t)r * qsz, kh + (size_t)src * ksz, vh + (size_t)src * ksz,
+                  per_ring, kvl, causal, lists + (int64_t)r * per_ring, lists + (int64_t)src * per_ring);
+      }
+      sm_finish(&st, oh + (size_t)r * qsz, lse + (size_t)r * rows);
+      sm_free(&st);
+      for (size_t rr = 0; rr < rows; ++rr) /* output_dot_rows (attention.cpp:266-280) */
+        delta[(size_t)r * rows + rr] =
+            dot_d(oh + (size_t)r * qsz + rr * (size_t)hs, doh + (size_t)r * qsz + rr * (size_t)hs, hs);
+    }
+    /* ring backward: every rank's block contributions */
+    for (int r = 0; r < ring; ++r)
+      for (int step = 0; step < ring; ++step) {
+        const int src = (r - step + ring) % ring;
+        double* ck = contrib_k + ((size_t)r * ring + src) * ksz;
+        double* cv = contrib_v + ((size_t)r * ring + src) * ksz;
+        memset(ck, 0, sizeof(double) * ksz);
+        memset(cv, 0, sizeof(double) * ksz);
+        block_backward(qh + (size_t)r * qsz, kh + (size_t)src * ksz, vh + (size_t)src * ksz,
+                       doh + (size_t)r * qsz, delta + (size_t)r * rows, lse + (size_t)r * rows,
+                       batch, per_ring, per_ring, hl, kvl, hs, causal, lists + (int64_t)r * per_ring,
+                       lists + (int64_t)src * per_ring, dqh + (size_t)r * qsz, ck, cv);
+      }
+    /* circulation order (ring_attention.cpp:466-500): block o's partial is
+     * acc_1 = c(o+1); acc_s = c(o+s) + acc_{s-1}; final = (0 + acc) + c(o) */
+    double* acc_k = (double*)malloc(sizeof(double) * ksz);
+    double* acc_v = (double*)malloc(sizeof(double) * ksz);
+    for (int o = 0; o < ring; ++o) {
+      double* fk = (double*)calloc(ksz, sizeof(double));
+      double* fv = (double*)calloc(ksz, sizeof(double));
+      if (ring > 1) {
+        for (int s = 1; s < ring; ++s) {
+          const int rr = (o + s) % ring;
+          const double* ck = contrib_k + ((size_t)rr * ring + o) * ksz;
+          const double* cv = contrib_v + ((size_t)rr * ring + o) * ksz;
+          for (size_t e = 0; e < ksz; ++e) {
+            acc_k[e] = (s == 1) ? ck[e] : ck[e] + acc_k[e];
+            acc_v[e] = (s == 1) ? cv[e] : cv[e] + acc_v[e];
+          }
+        }
+        for (size_t e = 0; e < ksz; ++e) {
+          fk[e] += acc_k[e];
+          fv[e] += acc_v[e];
+        }
+      }
+      const double* ok = contrib_k + ((size_t)o * ring + o) * ksz;
+      const double* ov = contrib_v + ((size_t)o * ring + o) * ksz;
+      for (size_t e = 0; e < ksz; ++e) {
+        fk[e] += ok[e];
+        fv[e] += ov[e];
+      }
+      /* inverse all-to-alls + place_rows */
+      const int64_t* pos = lists + (int64_t)o * per_ring;
+      for (int64_t b = 0; b < batch; ++b)
+        for (int64_t t = 0; t < per_ring; ++t) {
+          for (int64_t h = 0; h < kvl; ++h) {
+            const size_t src = (size_t)(((b * per_ring + t) * kvl + h) * hs);
+            const size_t dst = (size_t)(((b * seq + pos[t]) * kv_heads + u * kvl + h) * hs);
+            memcpy(dk_g + dst, fk + src, sizeof(double) * (size_t)hs);
+            memcpy(dv_g + dst, fv + src, sizeof(double) * (size_t)hs);
+          }
+          for (int64_t h = 0; h < hl; ++h)
+            memcpy(dq_g + ((b * seq + pos[t]) * heads + u * hl + h) * hs,
+                   dqh + (size_t)o * qsz + (size_t)(((b * per_ring + t) * hl + h) * hs),
+                   sizeof(double) * (size_t)hs);
+        }
+      free(fk);
+      free(fv);
+    }
+    free(acc_k);
+    free(acc_v);
+    memset(dqh, 0, sizeof(double) * qsz * ring);
+  }
+  free(lists); free(qh); free(oh); free(doh); free(dqh); free(lse); free(delta);
+  free(kh); free(vh); free(contrib_k); free(contrib_v);
+  return 0;
+}

@@ -85,6 +85,21 @@ int uo_usp_forward(const double* q, const double* k, const double* v,
                    int64_t head_size, int ulysses, int ring, int causal,
                    double* out_global, double* lse);
 
+/* reference_attention_grad<double> (attention.cpp:95-170). */
+int uo_reference_attention_grad(const double* q, const double* k, const double* v,
+                                const double* dout, int64_t batch, int64_t seq,
+                                int64_t heads, int64_t kv_heads, int64_t head_size,
+                                int causal, const int64_t* positions, double* dq,
+                                double* dk, double* dv);
+
+/* usp_attention_backward<double> (usp_attention.cpp:68-89,
+ * ring_attention.cpp:79-155, attention.cpp:266-324) after the forward, over
+ * every rank of a U x R mesh; global dq, dk, dv in original token order. */
+int uo_usp_backward(const double* q, const double* k, const double* v, const double* dout,
+                    int64_t batch, int64_t seq, int64_t heads, int64_t kv_heads,
+                    int64_t head_size, int ulysses, int ring, int causal, double* dq,
+                    double* dk, double* dv);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,4 +1,4 @@
-"""B200-native Unified Sequence Parallelism (USP) attention forward.
+"""B200-native Unified Sequence Parallelism (USP) attention forward and backward.
 
 The product is libusp_b200.so (hand-written sm_100a CUDA + NCCL, C ABI in
 include/usp_attn.h); this package is its host-side mirror of the reference
@@ -11,8 +11,10 @@ from .usp import (  # noqa: F401
     ShardSpec,
     UspAttention,
     UspForward,
+    UspGrads,
     causal_pair_counts,
     even_partition,
+    local_world_backward,
     local_world_forward,
     usp_attention,
     zigzag_partition,

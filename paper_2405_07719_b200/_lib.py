@@ -79,7 +79,8 @@ EXPORTS = [
     "usp_causal_pair_counts", "usp_schedule", "usp_step_plan", "usp_forward_ledger", "usp_engine_ledger", "usp_rank_flops", "usp_nccl_unique_id",
     "usp_comm_create_nccl", "usp_comm_create_local", "usp_comm_destroy", "usp_engine_create",
     "usp_attn_fwd", "usp_engine_last_launches", "usp_engine_destroy", "usp_engine_enable_timing",
-    "usp_engine_kernel_times", "usp_local_world_fwd",
+    "usp_engine_kernel_times", "usp_local_world_fwd", "usp_attn_bwd", "usp_local_world_bwd",
+    "usp_backward_ledger",
     "usp_last_error", "usp_version",
 ]
 
@@ -103,6 +104,9 @@ def _declare(lib):
         "usp_rank_flops": (st, [P(UspConfig), P(ctypes.c_double)]),
         "usp_forward_ledger": (ctypes.c_int32, [P(UspConfig), P(UspLedgerEntry), ctypes.c_int32]),
         "usp_engine_ledger": (ctypes.c_int32, [vp, P(UspLedgerEntry), ctypes.c_int32]),
+        "usp_backward_ledger": (ctypes.c_int32, [P(UspConfig), P(UspLedgerEntry), ctypes.c_int32]),
+        "usp_attn_bwd": (st, [vp] * 11),
+        "usp_local_world_bwd": (st, [P(vp), ctypes.c_int32] + [P(vp)] * 10),
         "usp_nccl_unique_id": (st, [ctypes.c_char_p]),
         "usp_comm_create_nccl": (st, [ctypes.c_char_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P(vp)]),
         "usp_comm_create_local": (st, [ctypes.c_int32, P(vp)]),

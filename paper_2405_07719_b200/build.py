@@ -18,7 +18,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libusp_b200.so")
 OBJ = os.path.join(HERE, "build")
-SOURCES = ["fa_fwd_sm100.cu", "reshard.cu", "engine.cu", "plan.cpp", "transport.cpp"]
+SOURCES = ["fa_fwd_sm100.cu", "fa_bwd_sm100.cu", "reshard.cu", "engine.cu", "plan.cpp", "transport.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

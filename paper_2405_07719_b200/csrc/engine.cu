@@ -29,6 +29,7 @@
 #include <vector>
 
 #include "../../include/usp_attn.h"
+#include "fa_bwd.hpp"
 #include "fa_fwd.hpp"
 #include "plan.hpp"
 #include "reshard.hpp"
@@ -221,6 +222,7 @@ class Engine {
     for (auto e : event_pool_) cudaEventDestroy(e);
     for (auto e : ev_pre_) cudaEventDestroy(e);
     for (auto e : ev_recv_) cudaEventDestroy(e);
+    for (auto e : ev_acc_) cudaEventDestroy(e);
     if (comm_stream_) cudaStreamDestroy(comm_stream_);
   }
 
@@ -246,6 +248,7 @@ class Engine {
         throw_invalid("q, k, v, o, lse must be non-null 16-byte aligned device pointers");
     launches_ = 0;
     ledger_.clear();
+    have_fwd_ = false;
     const size_t e = 2;
     const bool reshape = U_ > 1 || hs_ != hsk_;
     const void* qh = q;
@@ -352,6 +355,155 @@ class Engine {
       permute(rp, st);
     }
     (void)e;
+    have_fwd_ = true;
+    fwd_ledger_size_ = ledger_.size();
+  }
+
+  // ---------------------------------------------------------------- backward
+  // usp_attention_backward (usp_attention.cpp:68-89): dO all-to-all in,
+  // ring backward over the saved head-sharded Q, K, V, O, LSE, then the dQ,
+  // dK, dV all-to-alls out. The ring (ring_attention.cpp:79-155): step t runs
+  // the dK/dV kernel on K/V block src=(r-t) mod R and the dQ kernel; the
+  // rank's own block contribution (t=0) stays home, the partial of the block
+  // being visited circulates: created at t=1, accumulated (blk + acc) at
+  // t>=2, shifted after every t>=1, so after R-1 hops each rank holds the sum
+  // of the other ranks' contributions to its own block; dK = acc + own.
+  void bwd(const void* q, const void* k, const void* v, const void* o, const float* lse,
+           const void* dout, void* dq, void* dk, void* dv, cudaStream_t st) {
+    USPB_CHECK(cudaSetDevice(cfg_.device));
+    for (const void* ptr : {q, k, v, o, static_cast<const void*>(lse), dout, static_cast<const void*>(dq),
+                            static_cast<const void*>(dk), static_cast<const void*>(dv)})
+      if (!ptr || reinterpret_cast<uintptr_t>(ptr) % 16 != 0)
+        throw_invalid("q, k, v, o, lse, dout, dq, dk, dv must be non-null 16-byte aligned device pointers");
+    if (!have_fwd_) throw_invalid("logsumexp does not match the forward shard (missing forward artifacts?)");
+    ensure_bwd_buffers();
+    launches_ = 0;
+    ledger_.resize(fwd_ledger_size_);  // drop a previous backward's events, keep the forward's
+    const bool reshape = U_ > 1 || hs_ != hsk_;
+    const void* qh = reshape ? q_h_.p : q;
+    const void* kh = reshape ? kv0_.p : k;
+    const void* vh = reshape ? static_cast<const void*>(kv0_.as<uint8_t>() + kv_bytes_) : v;
+    const void* oh = reshape ? o_h_.p : o;
+    const void* doh = dout;
+    // -- 1. dO: sequence-sharded -> head-sharded (all_to_all_4d(.,2,1), :79)
+    if (U_ > 1) {
+      uint8_t* sq = send_.as<uint8_t>();
+      pack_heads(dout, sq, H_, hl_, st);
+      uint8_t* rq = B_ > 1 ? recv_.as<uint8_t>() : nullptr;
+      std::vector<std::vector<A2APart>> parts(1, std::vector<A2APart>(U_));
+      for (int p = 0; p < U_; ++p)
+        parts[0][p] = {sq + p * q_part_, rq ? rq + p * q_part_ : do_h_.as<uint8_t>() + p * q_part_};
+      tr_->all_to_all(*groups_, parts, {q_part_}, st);
+      if (B_ > 1) gather_seq(rq, do_h_.p, hl_, st);
+      doh = do_h_.p;
+    } else if (reshape) {
+      pad_rows(dout, do_h_.p, B_ * T_ * H_, st);
+      doh = do_h_.p;
+    }
+    record_a2a(4, q_part_);
+    // delta = rowsum(dO * O) (output_dot_rows, attention.cpp:266-280)
+    USPB_CHECK(launch_bwd_delta(oh, doh, delta_.as<float>(), B_ * Tr_ * hl_, hsk_, st));
+    ++launches_;
+
+    // -- 2. ring backward
+    const CUtensorMap tm_q = make_tmap(qh, hsk_, hl_, Tr_, B_);
+    const CUtensorMap tm_do = make_tmap(doh, hsk_, hl_, Tr_, B_);
+    auto kbuf = [&](int t) -> const void* { return t == 0 ? kh : kv_ring_[(t - 1) & 1].p; };
+    auto vbuf = [&](int t) -> const void* {
+      return t == 0 ? vh : static_cast<const void*>(kv_ring_[(t - 1) & 1].as<uint8_t>() + kv_bytes_);
+    };
+    const size_t gkv = size_t(B_) * Tr_ * kvl_ * hsk_;  // fp32 elements of one of dK / dV
+    float* own = own_dkv_.as<float>();
+    int cur = 0;  // acc_dkv_[cur] holds the circulating partial
+    for (int t = 0; t < R_; ++t) {
+      if (t + 1 < R_) {
+        USPB_CHECK(cudaEventRecord(ev_pre_[t], st));
+        USPB_CHECK(cudaStreamWaitEvent(comm_stream_, ev_pre_[t], 0));
+        record_shift(1);
+        record_shift(2);
+        tr_->ring_shift(*groups_, {kbuf(t), vbuf(t)},
+                        {const_cast<void*>(kbuf(t + 1)), const_cast<void*>(vbuf(t + 1))},
+                        {kv_bytes_, kv_bytes_}, comm_stream_);
+        USPB_CHECK(cudaEventRecord(ev_recv_[t], comm_stream_));
+      }
+      if (t > 0) USPB_CHECK(cudaStreamWaitEvent(st, ev_recv_[t - 1], 0));  // K/V(t) (and acc) landed
+      const BwdStep& bs = bwd_steps_[t];
+      float* tgt = t == 0 ? own : acc_dkv_[cur].as<float>();
+      launch_bwd_kernel(false, bs.dkdv, tm_q, tm_do, kbuf(t), vbuf(t), lse, nullptr, tgt, tgt + gkv,
+                        t >= 2, st);
+      if (t >= 1) {
+        // ship the partial to the next ring rank (overlaps the dQ kernel)
+        USPB_CHECK(cudaEventRecord(ev_acc_[t], st));
+        USPB_CHECK(cudaStreamWaitEvent(comm_stream_, ev_acc_[t], 0));
+        record_shift(6, 4);
+        record_shift(7, 4);
+        float* a = acc_dkv_[cur].as<float>();
+        float* b = acc_dkv_[cur ^ 1].as<float>();
+        tr_->ring_shift(*groups_, {a, a + gkv}, {b, b + gkv}, {gkv * 4, gkv * 4}, comm_stream_);
+        cur ^= 1;
+        // the next step's kernels wait on ev_recv_[t], recorded after this shift
+        if (t + 1 < R_) {
+          USPB_CHECK(cudaEventRecord(ev_recv_[t], comm_stream_));
+        } else {
+          USPB_CHECK(cudaEventRecord(ev_acc_[0], comm_stream_));
+        }
+      }
+      launch_bwd_kernel(true, bs.dq, tm_q, tm_do, kbuf(t), vbuf(t), lse, dq_acc_.as<float>(), nullptr,
+                        nullptr, t > 0, st);
+    }
+    if (R_ > 1) USPB_CHECK(cudaStreamWaitEvent(st, ev_acc_[0], 0));
+
+    // -- 3. casts (+ dK = acc + own) and the dQ, dK, dV all-to-alls out
+    const float* acc = R_ > 1 ? acc_dkv_[cur].as<float>() : nullptr;
+    const float* dk_a = R_ > 1 ? acc : own;
+    const float* dk_b = R_ > 1 ? own : nullptr;
+    const float* dv_a = R_ > 1 ? acc + gkv : own + gkv;
+    const float* dv_b = R_ > 1 ? own + gkv : nullptr;
+    if (U_ == 1) {
+      cast(dq_acc_.as<float>(), nullptr, dq, B_ * T_ * H_, st);
+      cast(dk_a, dk_b, dk, B_ * T_ * KV_, st);
+      cast(dv_a, dv_b, dv, B_ * T_ * KV_, st);
+      record_a2a(5, q_part_);
+      record_a2a(6, kv_part_);
+      record_a2a(7, kv_part_);
+      return;
+    }
+    // head-sharded bf16 gradients -> [peer][b][T][local] -> a2a -> (b, T, heads, hs)
+    uint8_t* gq = grad_h_.as<uint8_t>();
+    uint8_t* gk = gq + U_ * q_part_;
+    uint8_t* gv = gk + U_ * kv_part_;
+    const int64_t qrows = B_ * Tr_ * hl_, kvrows = B_ * Tr_ * kvl_;
+    USPB_CHECK(launch_cast_rows(dq_acc_.as<float>(), nullptr, gq, qrows, hsk_, hsk_, st));
+    USPB_CHECK(launch_cast_rows(dk_a, dk_b, gk, kvrows, hsk_, hsk_, st));
+    USPB_CHECK(launch_cast_rows(dv_a, dv_b, gv, kvrows, hsk_, hsk_, st));
+    launches_ += 3;
+    uint8_t* sq = gq;
+    uint8_t* sk = gk;
+    uint8_t* sv = gv;
+    if (B_ > 1) {
+      sq = send_.as<uint8_t>();
+      sk = sq + U_ * q_part_;
+      sv = sk + U_ * kv_part_;
+      split_seq(gq, sq, st, hl_);
+      split_seq(gk, sk, st, kvl_);
+      split_seq(gv, sv, st, kvl_);
+    }
+    uint8_t* rq = grad_recv_.as<uint8_t>();
+    uint8_t* rk = rq + U_ * q_part_;
+    uint8_t* rv = rk + U_ * kv_part_;
+    std::vector<std::vector<A2APart>> parts(3, std::vector<A2APart>(U_));
+    for (int p = 0; p < U_; ++p) {
+      parts[0][p] = {sq + p * q_part_, rq + p * q_part_};
+      parts[1][p] = {sk + p * kv_part_, rk + p * kv_part_};
+      parts[2][p] = {sv + p * kv_part_, rv + p * kv_part_};
+    }
+    tr_->all_to_all(*groups_, parts, {q_part_, kv_part_, kv_part_}, st);
+    record_a2a(5, q_part_);
+    record_a2a(6, kv_part_);
+    record_a2a(7, kv_part_);
+    unpack_heads(rq, dq, st, H_, hl_);
+    unpack_heads(rk, dk, st, KV_, kvl_);
+    unpack_heads(rv, dv, st, KV_, kvl_);
   }
 
   double rank_flops() const {
@@ -406,42 +558,45 @@ class Engine {
     rp.hs_src = rp.hs_dst = hsk_;
     permute(rp, st);
   }
-  // (b, U*T, hl) -> [dst][b][T][hl]   (bs > 1 send staging for O)
-  void split_seq(const void* src, void* dst, cudaStream_t st) {
+  // (b, U*T, local) -> [dst][b][T][local]   (bs > 1 send staging for O)
+  void split_seq(const void* src, void* dst, cudaStream_t st, int local = 0) {
+    if (!local) local = hl_;
     RowPermute rp;
     rp.src = src;
     rp.dst = dst;
     rp.dims[0] = U_;
     rp.dims[1] = B_;
     rp.dims[2] = T_;
-    rp.dims[3] = hl_;
-    rp.src_stride[0] = T_ * hl_;
-    rp.src_stride[1] = Tr_ * hl_;
-    rp.src_stride[2] = hl_;
+    rp.dims[3] = local;
+    rp.src_stride[0] = T_ * local;
+    rp.src_stride[1] = Tr_ * local;
+    rp.src_stride[2] = local;
     rp.src_stride[3] = 1;
-    rp.dst_stride[0] = B_ * T_ * hl_;
-    rp.dst_stride[1] = T_ * hl_;
-    rp.dst_stride[2] = hl_;
+    rp.dst_stride[0] = B_ * T_ * local;
+    rp.dst_stride[1] = T_ * local;
+    rp.dst_stride[2] = local;
     rp.dst_stride[3] = 1;
     rp.hs_src = rp.hs_dst = hsk_;
     permute(rp, st);
   }
-  // [src][b][T][hl][hsk] -> (b, T, H, hs), heads [src*hl, (src+1)*hl)
-  void unpack_heads(const void* src, void* dst, cudaStream_t st) {
+  // [src][b][T][local][hsk] -> (b, T, heads, hs), heads [src*local, (src+1)*local)
+  void unpack_heads(const void* src, void* dst, cudaStream_t st, int heads = 0, int local = 0) {
+    if (!heads) heads = H_;
+    if (!local) local = hl_;
     RowPermute rp;
     rp.src = src;
     rp.dst = dst;
     rp.dims[0] = U_;
     rp.dims[1] = B_;
     rp.dims[2] = T_;
-    rp.dims[3] = hl_;
-    rp.src_stride[0] = B_ * T_ * hl_;
-    rp.src_stride[1] = T_ * hl_;
-    rp.src_stride[2] = hl_;
+    rp.dims[3] = local;
+    rp.src_stride[0] = B_ * T_ * local;
+    rp.src_stride[1] = T_ * local;
+    rp.src_stride[2] = local;
     rp.src_stride[3] = 1;
-    rp.dst_stride[0] = hl_;
-    rp.dst_stride[1] = T_ * H_;
-    rp.dst_stride[2] = H_;
+    rp.dst_stride[0] = local;
+    rp.dst_stride[1] = T_ * heads;
+    rp.dst_stride[2] = heads;
     rp.dst_stride[3] = 1;
     rp.hs_src = hsk_;
     rp.hs_dst = hs_;
@@ -456,6 +611,107 @@ class Engine {
     rp.hs_src = hs_;
     rp.hs_dst = hsk_;
     permute(rp, st);
+  }
+
+  void cast(const float* a, const float* b, void* dst, int64_t rows, cudaStream_t st) {
+    USPB_CHECK(launch_cast_rows(a, b, dst, rows, hsk_, hs_, st));
+    ++launches_;
+  }
+
+  struct BwdStep {
+    DevStep dq, dkdv;
+  };
+  static void upload_plan(DevStep& d, StepPlan&& h) {
+    d.host = std::move(h);
+    d.q_pos = upload(d.host.q_pos);
+    d.k_pos = upload(d.host.k_pos);
+    d.tile_off = upload(d.host.tile_off);
+    d.tile_list = upload(d.host.tile_list);
+    d.units = upload(d.host.units);
+  }
+
+  void ensure_bwd_buffers() {
+    if (!bwd_steps_.empty()) return;
+    const bool reshape = U_ > 1 || hs_ != hsk_;
+    const size_t q_heads = size_t(B_) * Tr_ * hl_ * hsk_;
+    const size_t kv_heads = size_t(B_) * Tr_ * kvl_ * hsk_;
+    if (reshape) do_h_ = DevBuf(q_heads * 2);
+    delta_ = DevBuf(size_t(B_) * Tr_ * hl_ * sizeof(float));
+    dq_acc_ = DevBuf(q_heads * sizeof(float));
+    own_dkv_ = DevBuf(2 * kv_heads * sizeof(float));
+    if (R_ > 1) {
+      acc_dkv_[0] = DevBuf(2 * kv_heads * sizeof(float));
+      acc_dkv_[1] = DevBuf(2 * kv_heads * sizeof(float));
+      for (int t = 0; t < R_; ++t) {
+        cudaEvent_t a;
+        USPB_CHECK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+        ev_acc_.push_back(a);
+      }
+    }
+    if (U_ > 1) {
+      grad_h_ = DevBuf(U_ * (q_part_ + 2 * kv_part_));
+      grad_recv_ = DevBuf(U_ * (q_part_ + 2 * kv_part_));
+    }
+    const int group = hl_ / kvl_;
+    const auto my_pos = head_positions(shape_, cfg_.rank);
+    for (int t = 0; t < R_; ++t) {
+      const int src = ring_source(r_, t, R_);
+      const auto k_pos = head_positions(shape_, shape_.mesh.rank_of(u_, src));
+      BwdStep bs;
+      // dQ: t = 0 writes every row (empties included), later steps accumulate
+      StepPlan fq = plan_step(my_pos, k_pos, shape_.causal, B_, hl_, t == 0, group);
+      // dK/dV: t = 0 (own) and t = 1 (new partial) write every key row
+      upload_plan(bs.dkdv, transpose_plan(fq, B_, kvl_, t <= 1));
+      upload_plan(bs.dq, std::move(fq));
+      bwd_steps_.push_back(std::move(bs));
+    }
+  }
+
+  void launch_bwd_kernel(bool is_dq, const DevStep& s, const CUtensorMap& tm_q, const CUtensorMap& tm_do,
+                         const void* kb, const void* vb, const float* lse, float* dq, float* dk, float* dv,
+                         bool accumulate, cudaStream_t st) {
+    if (s.host.units.empty()) return;
+    BwdParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.tm_q = tm_q;
+    p.tm_do = tm_do;
+    p.tm_k = make_tmap(kb, hsk_, kvl_, Tr_, B_);
+    p.tm_v = make_tmap(vb, hsk_, kvl_, Tr_, B_);
+    p.lse = lse;
+    p.delta = delta_.as<float>();
+    p.dq = dq;
+    p.dk = dk;
+    p.dv = dv;
+    p.units = s.units.as<uint32_t>();
+    p.tile_off = s.tile_off.as<int32_t>();
+    p.tile_list = s.tile_list.as<int32_t>();
+    p.q_pos = s.q_pos.as<int32_t>();
+    p.k_pos = s.k_pos.as<int32_t>();
+    p.sched = sched_.as<int>() + (is_dq ? 4 : 8);
+    p.num_units = static_cast<int>(s.host.units.size());
+    p.batch = static_cast<int>(B_);
+    p.q_len = static_cast<int>(Tr_);
+    p.k_len = static_cast<int>(Tr_);
+    p.heads = hl_;
+    p.kv_heads = kvl_;
+    p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(double(hs_)));
+    p.inv_scale = static_cast<float>(1.0 / std::sqrt(double(hs_)));
+    p.accumulate = accumulate ? 1 : 0;
+    const int reserve = (R_ > 1 && tr_) ? tr_->reserved_sms() : 0;
+    const int slots = std::max(1, num_sms_ - reserve);
+    const int grid = std::min(p.num_units, slots);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timing_) {
+      e0 = timing_event(2 * timed_.size());
+      e1 = timing_event(2 * timed_.size() + 1);
+      USPB_CHECK(cudaEventRecord(e0, st));
+    }
+    USPB_CHECK(is_dq ? launch_bwd_dq(p, hsk_, grid, st) : launch_bwd_dkdv(p, hsk_, grid, st));
+    ++launches_;
+    if (timing_) {
+      USPB_CHECK(cudaEventRecord(e1, st));
+      timed_.push_back({e0, e1});
+    }
   }
 
   void launch_step(int t, const CUtensorMap& tm_q, const void* kb, const void* vb, void* o_heads,
@@ -562,6 +818,13 @@ class Engine {
   size_t q_part_ = 0, kv_part_ = 0, kv_bytes_ = 0;
   DevBuf q_h_, kv0_, o_h_, send_, recv_, o_send_, o_recv_, o_acc_, lse_acc_;
   DevBuf kv_ring_[2];
+  // backward (allocated by the first usp_attn_bwd)
+  DevBuf do_h_, delta_, dq_acc_, own_dkv_, grad_h_, grad_recv_;
+  DevBuf acc_dkv_[2];
+  std::vector<BwdStep> bwd_steps_;
+  std::vector<cudaEvent_t> ev_acc_;
+  bool have_fwd_ = false;
+  size_t fwd_ledger_size_ = 0;
   DevBuf sched_;  // unit tickets of the attention kernel (self-resetting)
   DevBuf trace_buf_;  // USP_FA_TRACE development stamps
 
@@ -585,12 +848,12 @@ class Engine {
     ledger_.push_back({3, shape_.mesh.rank_of(0, r_), U_, 1, tensor, tensor, payload,
                        double(part_bytes) * (U_ - 1)});
   }
-  void record_shift(int tensor) {
+  void record_shift(int tensor, int elem_bytes = 2) {
     const int step = static_cast<int>(std::count_if(ledger_.begin(), ledger_.end(),
                                                     [](const LedgerEvent& e) { return e.kind == 4; }));
     ledger_.push_back({4, shape_.mesh.rank_of(u_, 0), R_, U_, step, tensor,
                        static_cast<int64_t>(double(kv_bytes_) / 2.0 * hs_ / hsk_ + 0.5),
-                       double(kv_bytes_)});
+                       double(kv_bytes_) / 2.0 * elem_bytes});
   }
 };
 
@@ -736,6 +999,17 @@ int32_t usp_forward_ledger(const usp_config* cfg, usp_ledger_entry* out, int32_t
   return n;
 }
 
+int32_t usp_backward_ledger(const usp_config* cfg, usp_ledger_entry* out, int32_t cap) {
+  int32_t n = -1;
+  if (guarded([&] {
+        const UspShape s = shape_of(cfg);
+        s.validate();
+        n = copy_ledger(backward_ledger(s, cfg->rank, 2, 4), out, cap);
+      }) != USP_OK)
+    return -1;
+  return n;
+}
+
 int32_t usp_engine_ledger(const usp_engine* engine, usp_ledger_entry* out, int32_t cap) {
   if (!engine) return -1;
   return copy_ledger(engine->impl->ledger_, out, cap);
@@ -801,6 +1075,14 @@ usp_status usp_attn_fwd(usp_engine* engine, const void* q, const void* k, const 
   });
 }
 
+usp_status usp_attn_bwd(usp_engine* engine, const void* q, const void* k, const void* v, const void* o,
+                        const float* lse, const void* dout, void* dq, void* dk, void* dv, void* stream) {
+  return guarded([&] {
+    if (!engine) throw_invalid("engine is null");
+    engine->impl->bwd(q, k, v, o, lse, dout, dq, dk, dv, static_cast<cudaStream_t>(stream));
+  });
+}
+
 // Development: copies the USP_FA_TRACE stamps (kTraceEvents x kTraceTiles)
 // to host memory; returns 0 when tracing is off.
 extern "C" USP_API int usp_engine_trace_copy(const usp_engine* engine, unsigned long long* host) {
@@ -839,6 +1121,29 @@ usp_status usp_local_world_fwd(usp_engine* const* engines, int32_t world_size,
   for (int i = 0; i < world_size; ++i) {
     th.emplace_back([&, i] {
       rc[i] = usp_attn_fwd(engines[i], q[i], k[i], v[i], o[i], lse[i],
+                           streams ? streams[i] : nullptr);
+      if (rc[i] != USP_OK) err[i] = g_last_error;
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int i = 0; i < world_size; ++i)
+    if (rc[i] != USP_OK) {
+      g_last_error = "rank " + std::to_string(i) + ": " + err[i];
+      return rc[i];
+    }
+  return USP_OK;
+}
+
+usp_status usp_local_world_bwd(usp_engine* const* engines, int32_t world_size, const void* const* q,
+                               const void* const* k, const void* const* v, const void* const* o,
+                               const float* const* lse, const void* const* dout, void* const* dq,
+                               void* const* dk, void* const* dv, void* const* streams) {
+  std::vector<usp_status> rc(world_size, USP_OK);
+  std::vector<std::string> err(world_size);
+  std::vector<std::thread> th;
+  for (int i = 0; i < world_size; ++i) {
+    th.emplace_back([&, i] {
+      rc[i] = usp_attn_bwd(engines[i], q[i], k[i], v[i], o[i], lse[i], dout[i], dq[i], dk[i], dv[i],
                            streams ? streams[i] : nullptr);
       if (rc[i] != USP_OK) err[i] = g_last_error;
     });

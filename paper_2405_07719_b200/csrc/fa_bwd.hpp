@@ -1,0 +1,50 @@
+// fa_bwd.hpp — host/device contract of the attention backward kernels
+// (SURVEY §8(f) #1). Restates the reference's per-block backward
+// attention_block_backward (src/numerics/attention.cpp:282-324):
+//   p  = exp(s - lse),           s = q.k / sqrt(hs)  (masked -> 0)
+//   dp = dO . v,  ds = p (dp - delta) / sqrt(hs),  delta = rowsum(dO * O)
+//   dQ += ds K,  dK += ds^T Q,  dV += p^T dO
+// as two tcgen05 kernels (dQ per query tile; dK/dV per key tile, summed over
+// the GQA group's query heads) accumulating in fp32.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace uspb200 {
+
+struct BwdParams {
+  CUtensorMap tm_q, tm_k, tm_v, tm_do;  // (hs, heads, len, batch) bf16, box (64,1,128,1), SW128
+  const float* lse;    // natural-log LSE (batch, q_len, heads)
+  const float* delta;  // rowsum(dO * O) (batch, q_len, heads)
+  float* dq;           // fp32 (batch, q_len, heads, hs)      [dq kernel]
+  float* dk;           // fp32 (batch, k_len, kv_heads, hs)   [dkdv kernel]
+  float* dv;
+
+  const uint32_t* units;     // dq: q_tile | head << 16 | b << 24; dkdv: k_tile | kv_head << 16 | b << 24
+  const int32_t* tile_off;   // CSR over the unit's tile dimension
+  const int32_t* tile_list;  // other-dimension tile | partial << 31
+  const int32_t* q_pos;      // effective positions (see StepPlan), padded to 128
+  const int32_t* k_pos;
+  int* sched;                // unit tickets, zero between launches
+
+  int num_units;
+  int batch, q_len, k_len, heads, kv_heads;
+  float scale_log2;  // log2(e) / sqrt(head_size)
+  float inv_scale;   // 1 / sqrt(head_size)
+  int accumulate;    // 0: write the fp32 outputs, 1: add into them
+};
+
+cudaError_t launch_bwd_dq(const BwdParams& p, int hs, int grid, cudaStream_t stream);
+cudaError_t launch_bwd_dkdv(const BwdParams& p, int hs, int grid, cudaStream_t stream);
+// delta[row] = sum_s o[row][s] * dout[row][s]  (output_dot_rows, attention.cpp:266-280)
+cudaError_t launch_bwd_delta(const void* o, const void* dout, float* delta, int64_t rows, int hs,
+                             cudaStream_t stream);
+// dst = bf16(src [+ src2]), rows of hs_src -> hs_dst (drops padding);
+// the sum is (src + src2) in that order (ring_attention.cpp:145-150).
+cudaError_t launch_cast_rows(const float* src, const float* src2, void* dst, int64_t rows, int hs_src,
+                             int hs_dst, cudaStream_t stream);
+
+}  // namespace uspb200

@@ -187,6 +187,33 @@ std::vector<LedgerEvent> forward_ledger(const UspShape& s, int rank, int elem_by
   return ev;
 }
 
+std::vector<LedgerEvent> backward_ledger(const UspShape& s, int rank, int elem_bytes, int grad_bytes) {
+  std::vector<LedgerEvent> ev = forward_ledger(s, rank, elem_bytes);
+  const int U = s.mesh.ulysses, R = s.mesh.ring;
+  const int u = s.mesh.ulysses_coord(rank), r = s.mesh.ring_coord(rank);
+  const int64_t T = s.tokens_per_rank(), Tr = s.tokens_per_ring_rank();
+  const int64_t hs = s.head_size;
+  auto a2a = [&](int step, int tensor, int64_t elems) {
+    ev.push_back({3, s.mesh.rank_of(0, r), U, 1, step, tensor, elems,
+                  double(elems) * elem_bytes * double(U - 1) / double(U)});
+  };
+  a2a(4, 4, s.batch * T * s.heads * hs);
+  const int64_t kv_block = s.batch * Tr * s.local_kv_heads() * hs;
+  int rstep = static_cast<int>(std::count_if(ev.begin(), ev.end(), [](const LedgerEvent& e) { return e.kind == 4; }));
+  for (int t = 0; t < R; ++t) {
+    if (t + 1 < R)
+      for (int tensor = 1; tensor <= 2; ++tensor)
+        ev.push_back({4, s.mesh.rank_of(u, 0), R, U, rstep++, tensor, kv_block, double(kv_block) * elem_bytes});
+    if (t >= 1)
+      for (int tensor = 6; tensor <= 7; ++tensor)
+        ev.push_back({4, s.mesh.rank_of(u, 0), R, U, rstep++, tensor, kv_block, double(kv_block) * grad_bytes});
+  }
+  a2a(5, 5, s.batch * Tr * s.local_heads() * hs);
+  a2a(6, 6, s.batch * Tr * s.local_kv_heads() * hs);
+  a2a(7, 7, s.batch * Tr * s.local_kv_heads() * hs);
+  return ev;
+}
+
 int64_t visible_pairs(const std::vector<int64_t>& q_pos, const std::vector<int64_t>& k_pos,
                       bool causal) {
   if (!causal) return static_cast<int64_t>(q_pos.size()) * static_cast<int64_t>(k_pos.size());
@@ -285,6 +312,50 @@ StepPlan plan_step(const std::vector<int64_t>& q_pos, const std::vector<int64_t>
                       (static_cast<uint32_t>(x.b) << 24));
   p.visible_pairs = visible_pairs(q_pos, k_pos, causal);
   return p;
+}
+
+StepPlan transpose_plan(const StepPlan& f, int64_t batch, int kv_heads, bool include_empty) {
+  StepPlan t;
+  t.q_len = f.q_len;
+  t.k_len = f.k_len;
+  t.n_q_tiles = f.n_q_tiles;
+  t.n_k_tiles = f.n_k_tiles;
+  t.q_pos = f.q_pos;
+  t.k_pos = f.k_pos;
+  t.full_tiles = f.full_tiles;
+  t.partial_tiles = f.partial_tiles;
+  t.visible_pairs = f.visible_pairs;
+  std::vector<std::vector<int32_t>> by_k(f.n_k_tiles);
+  for (int qt = 0; qt < f.n_q_tiles; ++qt)
+    for (int e = f.tile_off[qt]; e < f.tile_off[qt + 1]; ++e) {
+      const uint32_t entry = static_cast<uint32_t>(f.tile_list[e]);
+      by_k[entry & 0x7FFFFFFFu].push_back(static_cast<int32_t>((entry & 0x80000000u) | uint32_t(qt)));
+    }
+  t.tile_off.assign(f.n_k_tiles + 1, 0);
+  for (int kt = 0; kt < f.n_k_tiles; ++kt) {
+    t.tile_list.insert(t.tile_list.end(), by_k[kt].begin(), by_k[kt].end());
+    t.tile_off[kt + 1] = static_cast<int32_t>(t.tile_list.size());
+  }
+  struct U {
+    int cost, kt, b, kvh;
+  };
+  std::vector<U> us;
+  for (int kt = 0; kt < f.n_k_tiles; ++kt) {
+    const int cost = static_cast<int>(by_k[kt].size());
+    if (cost == 0 && !include_empty) continue;
+    for (int64_t b = 0; b < batch; ++b)
+      for (int h = 0; h < kv_heads; ++h) us.push_back({cost, kt, static_cast<int>(b), h});
+  }
+  std::stable_sort(us.begin(), us.end(), [](const U& a, const U& b) {
+    if (a.b != b.b) return a.b < b.b;
+    if (a.kvh != b.kvh) return a.kvh < b.kvh;
+    if (a.cost != b.cost) return a.cost > b.cost;
+    return a.kt < b.kt;
+  });
+  for (const U& x : us)
+    t.units.push_back(static_cast<uint32_t>(x.kt) | (static_cast<uint32_t>(x.kvh) << 16) |
+                      (static_cast<uint32_t>(x.b) << 24));
+  return t;
 }
 
 }  // namespace uspb200

@@ -93,6 +93,13 @@ StepPlan plan_step(const std::vector<int64_t>& q_pos, const std::vector<int64_t>
                    bool causal, int64_t batch, int head_pairs, bool include_empty,
                    int pairs_per_kv = 1);
 
+// The same block transposed for the dK/dV kernel: CSR over KEY tiles
+// (tile_list = q tile | partial << 31, same partial flags), units
+// k_tile | kv_head << 16 | batch << 24 in kv-head-major LPT order.
+// include_empty keeps key tiles no query sees (their dK/dV rows are
+// written as zeros when the kernel does not accumulate).
+StepPlan transpose_plan(const StepPlan& fwd, int64_t batch, int kv_heads, bool include_empty);
+
 // One communication event of a rank's forward, in the reference ledger's
 // terms (src/simcomm/ledger.hpp:21-30, closed forms ledger.cpp:25-37).
 struct LedgerEvent {
@@ -107,6 +114,12 @@ struct LedgerEvent {
 // all-to-alls, 2(R-1) ring shifts (K then V per step), the O all-to-all.
 // The reference's two position all_gathers are absent (static layout).
 std::vector<LedgerEvent> forward_ledger(const UspShape& s, int rank, int elem_bytes);
+// forward_ledger followed by the backward's collectives
+// (usp_attention.cpp:68-89, ring_attention.cpp:79-155): dO all-to-all;
+// per ring step t: K, V shifts (t < R-1), then the circulating dK, dV
+// partial shifts (t >= 1, at grad_bytes per element); dQ, dK, dV
+// all-to-alls. Tensor ids 4 dO, 5 dQ, 6 dK, 7 dV.
+std::vector<LedgerEvent> backward_ledger(const UspShape& s, int rank, int elem_bytes, int grad_bytes);
 
 // Exact unmasked (q, k) pair count of one block, summed over the block
 // (causal_pair_counts semantics, partition.cpp:52-72) — for FLOP accounting.

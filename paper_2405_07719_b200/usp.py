@@ -166,6 +166,16 @@ def forward_ledger(cfg: UspConfig) -> list[dict]:
     return [buf[i].as_dict() for i in range(min(n, 64))]
 
 
+def backward_ledger(cfg: UspConfig) -> list[dict]:
+    """Planned collectives of one rank's forward + backward
+    (usp_attention.cpp:68-89, ring_attention.cpp:79-155)."""
+    buf = (UspLedgerEntry * 256)()
+    n = lib().usp_backward_ledger(ctypes.byref(cfg), buf, 256)
+    if n < 0:
+        check(2)
+    return [buf[i].as_dict() for i in range(min(n, 256))]
+
+
 def rank_flops(cfg: UspConfig) -> float:
     f = ctypes.c_double(0)
     check(lib().usp_rank_flops(ctypes.byref(cfg), ctypes.byref(f)))
@@ -237,6 +247,20 @@ class UspForward:
     out: "object"
     logsumexp: "object"
     head_positions: list
+    # the forward's inputs (the engine keeps their head-sharded copies)
+    q: "object" = None
+    k: "object" = None
+    v: "object" = None
+
+
+@dataclass
+class UspGrads:
+    """Backward results (usp_attention.hpp:26-31): dq, dk, dv sequence-sharded
+    like q, k, v (bf16)."""
+
+    dq: "object"
+    dk: "object"
+    dv: "object"
 
 
 def _ptr(t) -> int:
@@ -341,9 +365,46 @@ class UspAttention:
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         check(lib().usp_attn_fwd(self._h, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse),
                                  ctypes.c_void_p(s.cuda_stream)))
-        return UspForward(out, lse, self.head_positions())
+        return UspForward(out, lse, self.head_positions(), q, k, v)
 
     __call__ = forward
+
+    def alloc_grads(self):
+        import torch
+
+        dev = torch.device("cuda", self.device)
+        return (torch.empty(self.q_shape(), dtype=torch.bfloat16, device=dev),
+                torch.empty(self.kv_shape(), dtype=torch.bfloat16, device=dev),
+                torch.empty(self.kv_shape(), dtype=torch.bfloat16, device=dev))
+
+    def _check_bwd(self, fwd: UspForward, dout, dq, dk, dv):
+        import torch
+
+        if fwd.q is None:
+            raise UspInvalidInput(2, "logsumexp does not match the forward shard (missing forward artifacts?)")
+        self._check_tensors(fwd.q, fwd.k, fwd.v, fwd.out, fwd.logsumexp)
+        for name, t, shape in (("dout", dout, self.q_shape()), ("dq", dq, self.q_shape()),
+                               ("dk", dk, self.kv_shape()), ("dv", dv, self.kv_shape())):
+            if tuple(t.shape) != tuple(shape) or t.dtype != torch.bfloat16 or not t.is_cuda \
+                    or not t.is_contiguous():
+                what = "dO must be sequence-sharded like the forward output" if name == "dout" else \
+                    f"{name} must be a contiguous bfloat16 CUDA tensor of shape {shape}"
+                raise UspInvalidInput(2, f"{what}, got {tuple(t.shape)} {t.dtype} on {t.device}")
+
+    def backward(self, fwd: UspForward, dout, dq=None, dk=None, dv=None, stream=None) -> UspGrads:
+        """usp_attention_backward (usp_attention.cpp:68-89) of the engine's
+        most recent forward ``fwd``; collective over the mesh."""
+        import torch
+
+        if dq is None or dk is None or dv is None:
+            a, b, c = self.alloc_grads()
+            dq, dk, dv = (dq if dq is not None else a), (dk if dk is not None else b), (dv if dv is not None else c)
+        self._check_bwd(fwd, dout, dq, dk, dv)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        check(lib().usp_attn_bwd(self._h, _ptr(fwd.q), _ptr(fwd.k), _ptr(fwd.v), _ptr(fwd.out),
+                                 _ptr(fwd.logsumexp), _ptr(dout), _ptr(dq), _ptr(dk), _ptr(dv),
+                                 ctypes.c_void_p(s.cuda_stream)))
+        return UspGrads(dq, dk, dv)
 
     def close(self) -> None:
         if self._h:
@@ -365,6 +426,18 @@ def local_world_forward(engines: Sequence[UspAttention], qs, ks, vs, outs, lses,
     check(lib().usp_local_world_fwd(arr([e._h.value for e in engines]), n, arr(map(_ptr, qs)),
                                     arr(map(_ptr, ks)), arr(map(_ptr, vs)), arr(map(_ptr, outs)),
                                     arr(map(_ptr, lses)), arr([s.cuda_stream for s in streams])))
+
+
+def local_world_backward(engines: Sequence[UspAttention], fwds: Sequence[UspForward], douts, dqs, dks, dvs,
+                         streams) -> None:
+    """usp_attn_bwd on every rank of an in-process world."""
+    n = len(engines)
+    arr = lambda xs: (ctypes.c_void_p * n)(*[ctypes.c_void_p(x) for x in xs])  # noqa: E731
+    check(lib().usp_local_world_bwd(arr([e._h.value for e in engines]), n, arr(_ptr(f.q) for f in fwds),
+                                    arr(_ptr(f.k) for f in fwds), arr(_ptr(f.v) for f in fwds),
+                                    arr(_ptr(f.out) for f in fwds), arr(_ptr(f.logsumexp) for f in fwds),
+                                    arr(map(_ptr, douts)), arr(map(_ptr, dqs)), arr(map(_ptr, dks)),
+                                    arr(map(_ptr, dvs)), arr([s.cuda_stream for s in streams])))
 
 
 def usp_attention(mesh: ProcessMesh, q, k, v, positions: Sequence[int], causal: bool, *,

@@ -19,7 +19,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
 
-from oracle.oracle import Reference  # noqa: E402
+from oracle.oracle import Reference, reference_attention_grad, reference_usp_fwd_bwd  # noqa: E402
 
 # (name, bs, seq, hc, kv, hs, U, R, causal, seed) — the reference test cases
 CASES = [
@@ -47,6 +47,14 @@ def gen(seed, bs, seq, hc, kv, hs):
             g[nq + nk:].reshape(bs, seq, kv, hs))
 
 
+def gen_with_dout(seed, bs, seq, hc, kv, hs):
+    """Q, K, V, dO from one stream in that order (commands.cpp:90-102)."""
+    nq, nk = bs * seq * hc * hs, bs * seq * kv * hs
+    g = Reference.uniform(seed, 2 * nq + 2 * nk)
+    return (g[:nq].reshape(bs, seq, hc, hs), g[nq:nq + nk].reshape(bs, seq, kv, hs),
+            g[nq + nk:nq + 2 * nk].reshape(bs, seq, kv, hs), g[nq + 2 * nk:].reshape(bs, seq, hc, hs))
+
+
 def main():
     assert Reference.available(), "reference library not built (needs /root/reference)"
     out = {}
@@ -59,6 +67,14 @@ def main():
         out[f"{name}/out"] = o
         out[f"{name}/lse"] = lse
         out[f"{name}/ref_attn"] = Reference.reference_attention(q, k, v, causal)
+    # backward (usp_attention_backward, usp_attention.cpp:68-89) on the same cases
+    for name, bs, seq, hc, kv, hs, U, R, causal, seed in CASES:
+        q, k, v, do = gen_with_dout(seed, bs, seq, hc, kv, hs)
+        dq, dk, dv = reference_usp_fwd_bwd(q, k, v, do, U, R, causal)
+        out[f"{name}/bwd_ledger"] = np.array(json.dumps(Reference.last_ledger()))
+        out[f"{name}/bwd_dq"], out[f"{name}/bwd_dk"], out[f"{name}/bwd_dv"] = dq, dk, dv
+        g = reference_attention_grad(q, k, v, do, causal)
+        out[f"{name}/grad_dq"], out[f"{name}/grad_dk"], out[f"{name}/grad_dv"] = g
     # scrambled positions (test_numerics.cpp:105-117)
     q, k, v = gen(13, 1, 8, 2, 2, 4)
     pos = np.array([3, 0, 7, 4, 1, 6, 2, 5], np.int64)

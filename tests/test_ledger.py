@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 from paper_2405_07719_b200 import ProcessMesh
-from paper_2405_07719_b200.usp import forward_ledger, make_config
+from paper_2405_07719_b200.usp import backward_ledger, forward_ledger, make_config
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "reference_golden.npz")
 REF_ELEM = 8  # the golden forwards ran usp_attention<double>
@@ -64,3 +64,37 @@ def test_closed_forms_gqa_u2r2():
     assert len(a2a) == 4 and len(shifts) == 2 * (2 - 1)
     q, k, v, o = (e["bytes_sent"] for e in a2a)
     assert k == q * 2 / 8 and v == q * 2 / 8 and o == q
+
+
+def _bwd_cases():
+    g = np.load(GOLDEN)
+    return [(k.split("/")[0], g[k.split("/")[0] + "/meta"], json.loads(str(g[k])))
+            for k in g.files if k.endswith("/bwd_ledger")]
+
+
+@pytest.mark.parametrize("name,meta,ref", _bwd_cases(), ids=lambda x: x if isinstance(x, str) else "")
+def test_backward_ledger_matches_reference(name, meta, ref):
+    """Forward + backward collectives (usp_attention.cpp:68-89,
+    ring_attention.cpp:79-155) vs the reference World's ledger; the circulating
+    dK/dV partials travel in fp32 (4 bytes), everything else in bf16."""
+    bs, seq, hc, kv, hs, U, R, causal, _ = [int(x) for x in meta]
+    mesh = ProcessMesh(U, R)
+    ref_ev = [e for e in ref if e["kind"] != "all_gather"]
+    kinds = {3: "all_to_all", 4: "ring_shift"}
+    ours = []
+    for rank in range(U * R):
+        cfg = make_config(mesh, rank=rank, seq_len=seq, heads=hc, kv_heads=kv, head_size=hs, causal=bool(causal),
+                          batch=bs)
+        for e in backward_ledger(cfg):
+            members = [e["group_first"] + i * e["group_stride"] for i in range(e["group_size"])]
+            elem = 4 if e["tensor"] in (6, 7) and e["kind"] == 4 else OUR_ELEM
+            ours.append((e["kind"], ",".join(map(str, members)), e["step"], e["payload_elems"],
+                         e["bytes_sent"] / elem, rank))
+    for grp in sorted({e["group"] for e in ref_ev}):
+        r_seq = sorted((e for e in ref_ev if e["group"] == grp), key=lambda e: e["step"])
+        for m_i, m in enumerate(int(x) for x in grp.split(",")):
+            o_seq = sorted((o for o in ours if o[1] == grp and o[5] == m), key=lambda o: o[2])
+            assert [kinds[o[0]] for o in o_seq] == [e["kind"] for e in r_seq], (name, grp, m)
+            assert [o[3] for o in o_seq] == [e["payload_elems"] for e in r_seq], (name, grp, m)
+            assert [o[4] for o in o_seq] == [e["bytes_sent"][m_i] / REF_ELEM for e in r_seq], (name, grp, m)
+    assert len({(o[1], o[0], o[2]) for o in ours}) == len(ref_ev)

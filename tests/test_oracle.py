@@ -12,7 +12,8 @@ import os
 import numpy as np
 import pytest
 
-from oracle.oracle import Oracle, Reference
+from oracle.oracle import (Oracle, Reference, oracle_reference_attention_grad, oracle_usp_backward,
+                           reference_attention_grad, reference_usp_fwd_bwd)
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "reference_golden.npz")
 
@@ -85,6 +86,69 @@ def test_bitwise_vs_reference_library_random(seed):
         pos = rng.permutation(seq)
         assert np.array_equal(Oracle.reference_attention(q, k, v, causal, pos),
                               Reference.reference_attention(q, k, v, causal, pos))
+
+
+def _gen_do(seed, bs, seq, hc, kv, hs):
+    nq, nk = bs * seq * hc * hs, bs * seq * kv * hs
+    g = Oracle.uniform(seed, 2 * nq + 2 * nk)
+    return (g[:nq].reshape(bs, seq, hc, hs), g[nq:nq + nk].reshape(bs, seq, kv, hs),
+            g[nq + nk:nq + 2 * nk].reshape(bs, seq, kv, hs), g[nq + 2 * nk:].reshape(bs, seq, hc, hs))
+
+
+def test_backward_bitwise_vs_golden(golden):
+    """usp_attention_backward and reference_attention_grad restated
+    (oracle/usp_oracle.c) == the reference's own outputs, bit for bit."""
+    names = sorted({k.split("/")[0] for k in golden.files if k.endswith("/bwd_dq")})
+    assert len(names) >= 10
+    for name in names:
+        bs, seq, hc, kv, hs, U, R, causal, seed = golden[f"{name}/meta"].tolist()
+        q, k, v, do = _gen_do(seed, bs, seq, hc, kv, hs)
+        got = oracle_usp_backward(q, k, v, do, U, R, bool(causal))
+        for g_, key in zip(got, ("dq", "dk", "dv")):
+            assert np.array_equal(g_, golden[f"{name}/bwd_{key}"]), (name, key)
+        got = oracle_reference_attention_grad(q, k, v, do, bool(causal))
+        for g_, key in zip(got, ("dq", "dk", "dv")):
+            assert np.array_equal(g_, golden[f"{name}/grad_{key}"]), (name, key)
+
+
+@pytest.mark.skipif(not Reference.available(), reason="reference sources not present on this host")
+@pytest.mark.parametrize("seed", [5, 6])
+def test_backward_bitwise_vs_reference_library_random(seed):
+    rng = np.random.default_rng(seed)
+    for _ in range(3):
+        U = int(rng.choice([1, 2, 4]))
+        R = int(rng.choice([1, 2, 3]))
+        kv = U * int(rng.choice([1, 2]))
+        hc = kv * int(rng.choice([1, 2, 4]))
+        hs = int(rng.choice([3, 4, 8]))
+        seq = 2 * R * U * int(rng.integers(1, 4))
+        bs = int(rng.choice([1, 2]))
+        causal = bool(rng.integers(0, 2))
+        q, k, v, do = _gen_do(int(rng.integers(0, 1 << 30)), bs, seq, hc, kv, hs)
+        a = oracle_usp_backward(q, k, v, do, U, R, causal)
+        b = reference_usp_fwd_bwd(q, k, v, do, U, R, causal)
+        assert all(np.array_equal(x, y) for x, y in zip(a, b)), (U, R, kv, hc, hs, seq, bs, causal)
+        pos = rng.permutation(seq)
+        a = oracle_reference_attention_grad(q, k, v, do, causal, pos)
+        b = reference_attention_grad(q, k, v, do, causal, pos)
+        assert all(np.array_equal(x, y) for x, y in zip(a, b))
+
+
+def test_backward_matches_finite_differences():
+    """Known answer independent of the reference: d<dO, O>/dQ by central
+    differences on a tiny case."""
+    q, k, v, do = _gen_do(77, 1, 6, 2, 1, 3)
+    dq, dk, dv = oracle_reference_attention_grad(q, k, v, do, True)
+    eps = 1e-6
+    for arr, grad in ((q, dq), (k, dk), (v, dv)):
+        for idx in [(0, 0, 0, 0), (0, 3, 0, 1), (0, 5, 0, 2)]:
+            a0 = arr[idx]
+            arr[idx] = a0 + eps
+            fp = float((Oracle.reference_attention(q, k, v, True) * do).sum())
+            arr[idx] = a0 - eps
+            fm = float((Oracle.reference_attention(q, k, v, True) * do).sum())
+            arr[idx] = a0
+            assert abs((fp - fm) / (2 * eps) - grad[idx]) < 1e-6, idx
 
 
 # ---- known answers from the reference test suite -------------------------

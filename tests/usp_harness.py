@@ -39,6 +39,18 @@ def make_globals(c: UspCase):
     return q, k, v
 
 
+def make_globals_with_dout(c: UspCase):
+    """Q, K, V, dO from one stream in that order (usp_harness.hpp:30-41)."""
+    nq = c.bs * c.seq * c.hc * c.hs
+    nk = c.bs * c.seq * c.kv_hc * c.hs
+    g = Oracle.uniform(c.seed, 2 * nq + 2 * nk)
+    q = g[:nq].reshape(c.bs, c.seq, c.hc, c.hs)
+    k = g[nq:nq + nk].reshape(c.bs, c.seq, c.kv_hc, c.hs)
+    v = g[nq + nk:nq + 2 * nk].reshape(c.bs, c.seq, c.kv_hc, c.hs)
+    do = g[nq + 2 * nk:].reshape(c.bs, c.seq, c.hc, c.hs)
+    return q, k, v, do
+
+
 def to_bf16(x, device):
     import torch
 
@@ -76,6 +88,34 @@ def run_usp_gpu(c: UspCase, q, k, v, device):
     for p, o in zip(pos, outs):
         out[:, p] = o
     return out, [l_ for l_ in lses], engines, comm
+
+
+def run_usp_gpu_fwd_bwd(c: UspCase, q, k, v, dout, device):
+    """Forward then backward on every rank of a local world. Returns
+    (out, dq, dk, dv) global in original token order, and the engines."""
+    import torch
+
+    from paper_2405_07719_b200 import local_world_backward
+
+    out, lses, engines, comm = run_usp_gpu(c, q, k, v, device)
+    pos = [torch.tensor(e.positions(), dtype=torch.long, device=device) for e in engines]
+    fwds = []
+    from paper_2405_07719_b200 import UspForward
+
+    for e, p, l_ in zip(engines, pos, lses):
+        fwds.append(UspForward(out[:, p].contiguous(), l_, [], q[:, p].contiguous(), k[:, p].contiguous(),
+                               v[:, p].contiguous()))
+    douts = [dout[:, p].contiguous() for p in pos]
+    grads = [e.alloc_grads() for e in engines]
+    streams = [torch.cuda.Stream(device) for _ in engines]
+    torch.cuda.synchronize(device)
+    local_world_backward(engines, fwds, douts, [g[0] for g in grads], [g[1] for g in grads],
+                         [g[2] for g in grads], streams)
+    torch.cuda.synchronize(device)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    for p, g in zip(pos, grads):
+        dq[:, p], dk[:, p], dv[:, p] = g
+    return out, dq, dk, dv, engines, comm
 
 
 def errors(got: np.ndarray, want: np.ndarray):
