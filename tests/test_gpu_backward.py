@@ -78,7 +78,7 @@ def test_backward_ring3_llama_heads(cuda):
 def test_backward_ledger_matches_plan(cuda):
     from paper_2405_07719_b200.usp import backward_ledger
 
-    c = UspCase(seq=1024, hc=8, kv_hc=4, hs=128, ulysses=2, ring=3, causal=True, seed=5)
+    c = UspCase(seq=1536, hc=8, kv_hc=4, hs=128, ulysses=2, ring=3, causal=True, seed=5)
     q, k, v, do = make_globals_with_dout(c)
     tq, tk, tv, tdo = (to_bf16(x, cuda) for x in (q, k, v, do))
     _, _, _, _, engines, _ = run_usp_gpu_fwd_bwd(c, tq, tk, tv, tdo, cuda)
