@@ -21,8 +21,12 @@ UNIT = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1, "Tbyte": 1e12}
 def summarise(path):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
-    d = dict(zip(hdr, zip(units, vals)))
+    hdr, units = rows[0], rows[1]
+    outs = [_one(dict(zip(hdr, zip(units, vals)))) for vals in rows[2:]]
+    return outs[0] if len(outs) == 1 else outs
+
+
+def _one(d):
     out = {"kernel": d.get("Kernel Name", ("", ""))[1]}
     for k, m in KEYS.items():
         if m not in d:
