@@ -56,38 +56,95 @@ struct BwdCfg {
   static constexpr int kTileBytes = kTile * HS * 2;  // one 128-row bf16 tile
   static constexpr int kSubBytes = 128 * 128;
   static constexpr int kSub = HS / 64;
-  static constexpr int kThreads = 192;  // 4 compute warps, TMA warp, MMA warp
-  static constexpr int kTmaWarp = 4, kMmaWarp = 5;
+  // 8 compute warps (two per TMEM lane quarter, each owning half of the
+  // tile's columns), the TMA warp and the MMA warp
+  static constexpr int kCompute = 8;
+  static constexpr int kThreads = 32 * (kCompute + 2);
+  static constexpr int kTmaWarp = kCompute, kMmaWarp = kCompute + 1;
   static constexpr int kBudget = 227 * 1024 - 4096;
   static constexpr int kStages = (kBudget - 2 * kTileBytes) / kTileBytes > 6
                                      ? 6
                                      : (kBudget - 2 * kTileBytes) / kTileBytes;
   static constexpr int kSmemBytes = 1024 + 2 * kTileBytes + kStages * kTileBytes + 4096;
   static constexpr uint32_t kIdescSS = idesc_bf16_f32(128, 128, 0, 0);  // S / dP
-  static constexpr uint32_t kIdescTS = idesc_bf16_f32(128, HS, 0, 1);   // acc += X^T-style
+  static constexpr uint32_t kIdescTS = idesc_bf16_f32(128, HS, 0, 1);   // acc += X * tile
   static_assert(kStages >= 2, "smem");
 };
 
+// The 32-column chunks of a tile in the order their packed operands become
+// ready (warp half 0 does chunks 0,1, half 1 does 2,3, concurrently).
+__device__ __forceinline__ int chunk_at(int n) { return ((n & 1) << 1) | (n >> 1); }
+// TMEM column (within an S / dP buffer) of chunk c's packed bf16 result:
+// each warp half writes only inside the 64 columns it reads (half 0 owns
+// [0,64), half 1 [64,128)), after it has consumed them, so the two halves
+// never race.
+__device__ __forceinline__ uint32_t packed_col(int c) { return static_cast<uint32_t>((c >> 1) * 64 + (c & 1) * 16); }
+
+__device__ __forceinline__ void st16(uint32_t addr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(addr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
+// Epilogue helper: rows of one 128-row tile, `cols` fp32 columns from TMEM
+// starting at `col`, scaled, (accumulated into) dst row-major.
+template <int NCOL>
+__device__ __forceinline__ void store_rows(uint32_t lane_base, uint32_t col, bool have, bool valid, float* dst,
+                                           float sc, bool accumulate) {
+#pragma unroll 1
+  for (int c = 0; c < NCOL / 32; ++c) {
+    uint32_t r[32];
+    if (have) {
+      tmem_ld32(lane_base + col + c * 32, r);
+      tmem_ld_wait(r);
+    }
+    if (!valid) continue;
+    float4* d4 = reinterpret_cast<float4*>(dst + c * 32);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float4 v = have ? make_float4(__uint_as_float(r[4 * i]) * sc, __uint_as_float(r[4 * i + 1]) * sc,
+                                    __uint_as_float(r[4 * i + 2]) * sc, __uint_as_float(r[4 * i + 3]) * sc)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (accumulate) {
+        const float4 a = d4[i];
+        v.x += a.x;
+        v.y += a.y;
+        v.z += a.z;
+        v.w += a.w;
+      }
+      d4[i] = v;
+    }
+  }
+}
+
 // ============================================================ dq kernel
-// TMEM: S [0,128) (dS bf16 over its first 64 columns), dP [128,256),
-// dQ [256, 256+HS).
+// TMEM: S0 [0,128), dP [128,256), dQ [256,256+HS), S1 [384,512) (HS = 128;
+// for HS = 64 the same columns). dS (bf16) is written over consumed columns
+// of the S buffer it came from (packed_col). S(j+1) goes to the other S buffer
+// while tile j's elementwise work runs; dQ k-steps are issued per 32-key
+// chunk as soon as that chunk's dS is in TMEM.
 template <int HS>
 __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(const __grid_constant__ BwdParams p) {
   using C = BwdCfg<HS>;
   constexpr int NS = C::kStages;
+  constexpr uint32_t kDP = 128, kDQ = 256, kS1 = 384;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
   uint8_t* sDO = smem + C::kTileBytes;
   uint8_t* sKV = smem + 2 * C::kTileBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + NS * C::kTileBytes);
-  uint64_t* q_full = bars;           // Q + dO landed
+  uint64_t* q_full = bars;            // Q + dO landed
   uint64_t* q_empty = bars + 1;
-  uint64_t* s_full = bars + 2;       // S and dP in TMEM
-  uint64_t* ds_ready = bars + 3;     // dS written (128 arrivals)
-  uint64_t* dq_full = bars + 4;      // unit's last dQ MMA done
-  uint64_t* kv_full = bars + 5;      // [NS]
-  uint64_t* kv_empty = kv_full + NS; // [NS]
+  uint64_t* s_full = bars + 2;        // [2] S buffer b computed
+  uint64_t* dp_full = bars + 4;       // dP computed
+  uint64_t* chunk_ready = bars + 5;   // [4] dS chunk in TMEM (128 arrivals)
+  uint64_t* dq_full = bars + 9;       // unit's last dQ MMA done
+  uint64_t* kv_full = bars + 10;      // [NS]
+  uint64_t* kv_empty = kv_full + NS;  // [NS]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_empty + NS);
   int* unit_slot = reinterpret_cast<int*>(tmem_slot + 2);
   uint64_t* u_full = reinterpret_cast<uint64_t*>(unit_slot + 2);
@@ -97,11 +154,13 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
-    mbar_init(s_full, 1);
-    mbar_init(ds_ready, 128);
+    mbar_init(&s_full[0], 1);
+    mbar_init(&s_full[1], 1);
+    mbar_init(dp_full, 1);
+    for (int c = 0; c < 4; ++c) mbar_init(&chunk_ready[c], 128);
     mbar_init(dq_full, 1);
     mbar_init(u_full, 1);
-    mbar_init(u_empty, 5);  // 4 compute warps + MMA warp
+    mbar_init(u_empty, C::kCompute + 1);
     for (int s = 0; s < NS; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
@@ -116,27 +175,23 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
   if (tmem != 0) __trap();
   const int group = p.heads / p.kv_heads;
 
-  // unit ticket hand-off: producer claims, consumers read (depth 1)
-  auto get_unit = [&](uint32_t it, bool whole_warp) {
+  auto get_unit = [&](uint32_t it) {
     mbar_wait(u_full, it & 1);
     const int u = *reinterpret_cast<volatile int*>(unit_slot);
-    if (whole_warp) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(u_empty);
-    } else {
-      mbar_arrive(u_empty);
-    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(u_empty);
     return u;
   };
 
-  if (warp < 4) {
+  if (warp < C::kCompute) {
     // ---------------------------------------------------- compute warps
-    const int row_in_tile = warp * 32 + lane;
-    const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    const int q4 = warp & 3, hf = warp >> 2;
+    const int row_in_tile = q4 * 32 + lane;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
     const float sl2 = p.scale_log2;
-    uint32_t s_phase = 0, d_phase = 0;
+    uint32_t g = 0, d_phase = 0;  // g: running tile counter (buffer parity, phases)
     for (uint32_t it = 0;; ++it) {
-      const int u = get_unit(it, true);
+      const int u = get_unit(it);
       if (u >= p.num_units) break;
       const uint32_t unit = p.units[u];
       const int qt = unit & 0xFFFF, h = (unit >> 16) & 0xFF, b = unit >> 24;
@@ -147,16 +202,18 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
       const float lse2 = valid ? p.lse[row] * 1.4426950408889634f : 0.f;
       const float dlt = valid ? p.delta[row] : 0.f;
       const int qpos = p.q_pos[q_row];
-      for (int j = 0; j < n; ++j) {
+      for (int j = 0; j < n; ++j, ++g) {
         const int entry = p.tile_list[beg + j];
-        mbar_wait(s_full, s_phase & 1);
-        ++s_phase;
+        const uint32_t sb = (g & 1) ? kS1 : 0u;
+        mbar_wait(&s_full[g & 1], (g >> 1) & 1);
+        mbar_wait(dp_full, g & 1);
         tc_fence_after();
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
+        for (int cc = 0; cc < 2; ++cc) {
+          const int c = 2 * hf + cc;
           uint32_t s[32], dp[32];
-          tmem_ld32(lane_base + c * 32, s);
-          tmem_ld32(lane_base + 128 + c * 32, dp);
+          tmem_ld32(lane_base + sb + c * 32, s);
+          tmem_ld32(lane_base + kDP + c * 32, dp);
           tmem_ld_wait(s);
           tmem_ld_wait(dp);
           if (entry < 0) {
@@ -176,55 +233,22 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
           for (int i = 0; i < 16; ++i) {
             const float p0 = ex2(fmaf(__uint_as_float(s[2 * i]), sl2, -lse2));
             const float p1 = ex2(fmaf(__uint_as_float(s[2 * i + 1]), sl2, -lse2));
-            const float d0 = p0 * (__uint_as_float(dp[2 * i]) - dlt);
-            const float d1 = p1 * (__uint_as_float(dp[2 * i + 1]) - dlt);
-            pk[i] = pack_bf16x2(d0, d1);
+            pk[i] = pack_bf16x2(p0 * (__uint_as_float(dp[2 * i]) - dlt), p1 * (__uint_as_float(dp[2 * i + 1]) - dlt));
           }
-          // dS chunk c -> S columns [16c, 16c+16): already consumed
-          asm volatile(
-              "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
-              "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(lane_base + c * 16),
-              "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3]), "r"(pk[4]), "r"(pk[5]), "r"(pk[6]),
-              "r"(pk[7]), "r"(pk[8]), "r"(pk[9]), "r"(pk[10]), "r"(pk[11]), "r"(pk[12]), "r"(pk[13]),
-              "r"(pk[14]), "r"(pk[15])
-              : "memory");
+          st16(lane_base + sb + packed_col(c), pk);  // dS chunk c, over already-consumed S columns
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(&chunk_ready[c]);
         }
-        tmem_st_wait();
-        tc_fence_before();
-        mbar_arrive(ds_ready);
       }
-      // epilogue: dq (+)= dQ / sqrt(hs)
+      // epilogue: dq (+)= dQ / sqrt(hs); warp half hf stores half the columns
       if (n > 0) {
         mbar_wait(dq_full, d_phase & 1);
         ++d_phase;
         tc_fence_after();
       }
-#pragma unroll 1
-      for (int c = 0; c < HS / 32; ++c) {
-        uint32_t r[32];
-        if (n > 0) {
-          tmem_ld32(lane_base + 256 + c * 32, r);
-          tmem_ld_wait(r);
-        }
-        if (!valid) continue;
-        float4* dst = reinterpret_cast<float4*>(p.dq + row * HS + c * 32);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          float4 v = n > 0 ? make_float4(__uint_as_float(r[4 * i]) * p.inv_scale,
-                                         __uint_as_float(r[4 * i + 1]) * p.inv_scale,
-                                         __uint_as_float(r[4 * i + 2]) * p.inv_scale,
-                                         __uint_as_float(r[4 * i + 3]) * p.inv_scale)
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
-          if (p.accumulate) {
-            const float4 a = dst[i];
-            v.x += a.x;
-            v.y += a.y;
-            v.z += a.z;
-            v.w += a.w;
-          }
-          dst[i] = v;
-        }
-      }
+      store_rows<HS / 2>(lane_base, kDQ + hf * (HS / 2), n > 0, valid, p.dq + row * HS + hf * (HS / 2),
+                         p.inv_scale, p.accumulate != 0);
     }
   } else if (warp == C::kTmaWarp) {
     // ---------------------------------------------------- producer
@@ -274,7 +298,7 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
     const uint64_t do_desc = smem_desc_sw128(smem_u32(sDO), 16, 1024);
     const uint64_t kv_desc0 = smem_desc_sw128(smem_u32(sKV), 16, 1024);
     const uint64_t kvmn_desc0 = smem_desc_sw128(smem_u32(sKV), C::kSubBytes, 1024);
-    uint32_t kv_it = 0, q_phase = 0, ds_phase = 0;
+    uint32_t kv_it = 0, q_phase = 0, g = 0;
     auto ss = [&](uint32_t d, uint64_t ad, uint32_t slot) {  // D = A * B^T, B K-major from slot
       bwd_dispatch_slot<NS>(slot, [&](auto S) {
         constexpr int sl = decltype(S)::value;
@@ -288,36 +312,57 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
         __syncwarp();
       });
     };
+    auto wait_slot = [&](uint32_t i) { mbar_wait(&kv_full[i % NS], (i / NS) & 1); };
     for (uint32_t it = 0;; ++it) {
-      const int u = get_unit(it, true);
+      const int u = get_unit(it);
       if (u >= p.num_units) break;
       const int qt = p.units[u] & 0xFFFF;
       const int n = p.tile_off[qt + 1] - p.tile_off[qt];
       if (n == 0) continue;
       mbar_wait(q_full, q_phase & 1);
       ++q_phase;
+      wait_slot(kv_it);
       tc_fence_after();
-      for (int j = 0; j < n; ++j) {
-        const uint32_t ki = kv_it + 2 * j, vi = ki + 1;
-        mbar_wait(&kv_full[ki % NS], (ki / NS) & 1);
-        mbar_wait(&kv_full[vi % NS], (vi / NS) & 1);
-        tc_fence_after();
-        ss(0, q_desc, ki % NS);     // S  = Q  K^T
-        ss(128, do_desc, vi % NS);  // dP = dO V^T
-        bwd_commit(s_full);
-        if (j == n - 1) bwd_commit(q_empty);
-        mbar_wait(ds_ready, ds_phase & 1);
-        ++ds_phase;
-        tc_fence_after();
-        // dQ += dS K: K tile as the MN-major B operand
+      ss((g & 1) ? kS1 : 0u, q_desc, kv_it % NS);  // S(0)
+      bwd_commit(&s_full[g & 1]);
+      wait_slot(kv_it + 1);
+      tc_fence_after();
+      ss(kDP, do_desc, (kv_it + 1) % NS);  // dP(0)
+      bwd_commit(dp_full);
+      for (int j = 0; j < n; ++j, ++g) {
+        const uint32_t ki = kv_it + 2 * j;
+        if (j + 1 < n) {  // S(j+1) into the other buffer, overlapping tile j's elementwise work
+          wait_slot(ki + 2);
+          tc_fence_after();
+          ss(((g + 1) & 1) ? kS1 : 0u, q_desc, (ki + 2) % NS);
+          bwd_commit(&s_full[(g + 1) & 1]);
+        } else {
+          bwd_commit(q_empty);  // every MMA reading Q / dO has been issued
+        }
+        const uint32_t sb = (g & 1) ? kS1 : 0u;
+        // dQ += dS K, chunk by chunk (K tile as the MN-major B operand)
         bwd_dispatch_slot<NS>(ki % NS, [&](auto S) {
           constexpr int sl = decltype(S)::value;
           const uint64_t bd = kvmn_desc0 + static_cast<uint64_t>((sl * C::kTileBytes) >> 4);
-          if (elect_one()) mma_pv_chain(256, 0, bd, C::kIdescTS, j > 0 ? 1u : 0u);
-          __syncwarp();
+#pragma unroll
+          for (int n4 = 0; n4 < 4; ++n4) {
+            const int c = chunk_at(n4);
+            mbar_wait(&chunk_ready[c], g & 1);
+            tc_fence_after();
+            if (elect_one())
+              mma_ts_k2(kDQ, sb + packed_col(c), bd + static_cast<uint64_t>(c * 256), C::kIdescTS,
+                        (j > 0 || n4 > 0) ? 1u : 0u);
+            __syncwarp();
+          }
         });
         bwd_commit(&kv_empty[ki % NS]);
-        bwd_commit(&kv_empty[vi % NS]);
+        bwd_commit(&kv_empty[(ki + 1) % NS]);
+        if (j + 1 < n) {  // dP(j+1): tile j's dP has been read (all chunks ready)
+          wait_slot(ki + 3);
+          tc_fence_after();
+          ss(kDP, do_desc, (ki + 3) % NS);
+          bwd_commit(dp_full);
+        }
       }
       bwd_commit(dq_full);
       kv_it += 2 * n;
@@ -330,9 +375,11 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
 }
 
 // ============================================================ dk/dv kernel
-// TMEM: S^T [0,128) (P^T bf16 over its first 64 columns), dP^T [128,256)
-// (dS^T bf16 over its first 64), dV [256, 256+HS), dK [256+HS, 256+2HS).
+// TMEM: S^T [0,128) (P^T bf16 over consumed columns), dP^T [128,256)
+// (dS^T bf16 likewise), dV [256, 256+HS), dK [256+HS, 256+2HS).
 // Q / dO tiles stream through the slot ring; K, V stay resident per unit.
+// dV / dK k-steps are issued per 32-query chunk as soon as that chunk's
+// P^T / dS^T are in TMEM.
 template <int HS>
 __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(const __grid_constant__ BwdParams p) {
   using C = BwdCfg<HS>;
@@ -343,12 +390,12 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
   uint8_t* sV = smem + C::kTileBytes;
   uint8_t* sQD = smem + 2 * C::kTileBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sQD + NS * C::kTileBytes);
-  uint64_t* kv_full = bars;         // K + V landed
+  uint64_t* kv_full = bars;          // K + V landed
   uint64_t* kv_empty = bars + 1;
-  uint64_t* s_full = bars + 2;      // S^T and dP^T in TMEM
-  uint64_t* pd_ready = bars + 3;    // P^T, dS^T written (128 arrivals)
-  uint64_t* acc_full = bars + 4;    // unit's last dV/dK MMA done
-  uint64_t* qd_full = bars + 5;     // [NS]
+  uint64_t* s_full = bars + 2;       // S^T and dP^T in TMEM
+  uint64_t* chunk_ready = bars + 3;  // [4] P^T, dS^T chunk written (128 arrivals)
+  uint64_t* acc_full = bars + 7;     // unit's last dV/dK MMA done
+  uint64_t* qd_full = bars + 8;      // [NS]
   uint64_t* qd_empty = qd_full + NS;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qd_empty + NS);
   int* unit_slot = reinterpret_cast<int*>(tmem_slot + 2);
@@ -361,10 +408,10 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
     mbar_init(kv_full, 1);
     mbar_init(kv_empty, 1);
     mbar_init(s_full, 1);
-    mbar_init(pd_ready, 128);
+    for (int c = 0; c < 4; ++c) mbar_init(&chunk_ready[c], 128);
     mbar_init(acc_full, 1);
     mbar_init(u_full, 1);
-    mbar_init(u_empty, 5);
+    mbar_init(u_empty, C::kCompute + 1);
     for (int s = 0; s < NS; ++s) {
       mbar_init(&qd_full[s], 1);
       mbar_init(&qd_empty[s], 1);
@@ -379,54 +426,53 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
   if (tmem != 0) __trap();
   const int group = p.heads / p.kv_heads;
 
-  auto get_unit = [&](uint32_t it, bool whole_warp) {
+  auto get_unit = [&](uint32_t it) {
     mbar_wait(u_full, it & 1);
     const int u = *reinterpret_cast<volatile int*>(unit_slot);
-    if (whole_warp) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(u_empty);
-    } else {
-      mbar_arrive(u_empty);
-    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(u_empty);
     return u;
   };
 
-  if (warp < 4) {
+  if (warp < C::kCompute) {
     // ---------------------------------------------------- compute warps (thread = key row)
-    const int key_in_tile = warp * 32 + lane;
-    const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    const int q4 = warp & 3, hf = warp >> 2;
+    const int key_in_tile = q4 * 32 + lane;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
     const float sl2 = p.scale_log2;
-    uint32_t s_phase = 0, a_phase = 0, vpar = 0;
+    uint32_t g = 0, a_phase = 0;
     for (uint32_t it = 0;; ++it) {
-      const int u = get_unit(it, true);
+      const int u = get_unit(it);
       if (u >= p.num_units) break;
       const uint32_t unit = p.units[u];
       const int kt = unit & 0xFFFF, kvh = (unit >> 16) & 0xFF, b = unit >> 24;
       const int beg = p.tile_off[kt], n = p.tile_off[kt + 1] - beg;
       const int k_row = kt * 128 + key_in_tile;
       const int kpos = p.k_pos[k_row];
-      for (int g = 0; g < group; ++g) {
-        const int h = kvh * group + g;
-        for (int j = 0; j < n; ++j) {
+      for (int gh = 0; gh < group; ++gh) {
+        const int h = kvh * group + gh;
+        for (int j = 0; j < n; ++j, ++g) {
           const int entry = p.tile_list[beg + j];
           const int qt = entry & 0x7FFFFFFF;
           // this q tile's lse2 / delta / q positions -> shared (parity buffer)
-          float* vb = vec + (vpar & 1) * 384;
-          ++vpar;
+          float* vb = vec + (g & 1) * 384;
           {
             const int qr = qt * 128 + key_in_tile;
             const bool ok = qr < p.q_len;
-            const size_t r = (static_cast<size_t>(b) * p.q_len + (ok ? qr : 0)) * p.heads + h;
-            vb[key_in_tile] = ok ? p.lse[r] * 1.4426950408889634f : INFINITY;  // padding rows: p = 0
-            vb[128 + key_in_tile] = ok ? p.delta[r] : 0.f;
-            vb[256 + key_in_tile] = __int_as_float(p.q_pos[qr]);
+            if (hf == 0) {
+              const size_t r = (static_cast<size_t>(b) * p.q_len + (ok ? qr : 0)) * p.heads + h;
+              vb[key_in_tile] = ok ? p.lse[r] * 1.4426950408889634f : INFINITY;  // padding rows: p = 0
+              vb[128 + key_in_tile] = ok ? p.delta[r] : 0.f;
+            } else {
+              vb[256 + key_in_tile] = __int_as_float(p.q_pos[qr]);
+            }
           }
-          bwd_bar_sync(1, 128);
-          mbar_wait(s_full, s_phase & 1);
-          ++s_phase;
+          bwd_bar_sync(1, 32 * C::kCompute);
+          mbar_wait(s_full, g & 1);
           tc_fence_after();
 #pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
+          for (int cc = 0; cc < 2; ++cc) {
+            const int c = 2 * hf + cc;
             uint32_t s[32], dp[32];
             tmem_ld32(lane_base + c * 32, s);
             tmem_ld32(lane_base + 128 + c * 32, dp);
@@ -442,33 +488,19 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
                 if (kpos > __float_as_int(vb[256 + q0])) p0 = 0.f;
                 if (kpos > __float_as_int(vb[256 + q1])) p1 = 0.f;
               }
-              const float d0 = p0 * (__uint_as_float(dp[2 * i]) - vb[128 + q0]);
-              const float d1 = p1 * (__uint_as_float(dp[2 * i + 1]) - vb[128 + q1]);
               pp[i] = pack_bf16x2(p0, p1);
-              pd[i] = pack_bf16x2(d0, d1);
+              pd[i] = pack_bf16x2(p0 * (__uint_as_float(dp[2 * i]) - vb[128 + q0]),
+                                  p1 * (__uint_as_float(dp[2 * i + 1]) - vb[128 + q1]));
             }
-            asm volatile(
-                "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
-                "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(lane_base + c * 16),
-                "r"(pp[0]), "r"(pp[1]), "r"(pp[2]), "r"(pp[3]), "r"(pp[4]), "r"(pp[5]), "r"(pp[6]),
-                "r"(pp[7]), "r"(pp[8]), "r"(pp[9]), "r"(pp[10]), "r"(pp[11]), "r"(pp[12]),
-                "r"(pp[13]), "r"(pp[14]), "r"(pp[15])
-                : "memory");
-            asm volatile(
-                "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
-                "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(lane_base + 128 +
-                                                                                     c * 16),
-                "r"(pd[0]), "r"(pd[1]), "r"(pd[2]), "r"(pd[3]), "r"(pd[4]), "r"(pd[5]), "r"(pd[6]),
-                "r"(pd[7]), "r"(pd[8]), "r"(pd[9]), "r"(pd[10]), "r"(pd[11]), "r"(pd[12]),
-                "r"(pd[13]), "r"(pd[14]), "r"(pd[15])
-                : "memory");
+            st16(lane_base + packed_col(c), pp);
+            st16(lane_base + 128 + packed_col(c), pd);
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&chunk_ready[c]);
           }
-          tmem_st_wait();
-          tc_fence_before();
-          mbar_arrive(pd_ready);
         }
       }
-      // epilogue: dk (+)= dK / sqrt(hs), dv (+)= dV
+      // epilogue: warp half 0 stores dv (+)= dV, half 1 dk (+)= dK / sqrt(hs)
       const bool any = n > 0;
       if (any) {
         mbar_wait(acc_full, a_phase & 1);
@@ -477,36 +509,10 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
       }
       const bool valid = k_row < p.k_len;
       const size_t krow = (static_cast<size_t>(b) * p.k_len + (valid ? k_row : 0)) * p.kv_heads + kvh;
-#pragma unroll 1
-      for (int which = 0; which < 2; ++which) {
-        float* out = which == 0 ? p.dv : p.dk;
-        const float sc = which == 0 ? 1.f : p.inv_scale;
-        const uint32_t col = which == 0 ? 256 : 256 + HS;
-#pragma unroll 1
-        for (int c = 0; c < HS / 32; ++c) {
-          uint32_t r[32];
-          if (any) {
-            tmem_ld32(lane_base + col + c * 32, r);
-            tmem_ld_wait(r);
-          }
-          if (!valid) continue;
-          float4* dst = reinterpret_cast<float4*>(out + krow * HS + c * 32);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            float4 v = any ? make_float4(__uint_as_float(r[4 * i]) * sc, __uint_as_float(r[4 * i + 1]) * sc,
-                                         __uint_as_float(r[4 * i + 2]) * sc, __uint_as_float(r[4 * i + 3]) * sc)
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
-            if (p.accumulate) {
-              const float4 a = dst[i];
-              v.x += a.x;
-              v.y += a.y;
-              v.z += a.z;
-              v.w += a.w;
-            }
-            dst[i] = v;
-          }
-        }
-      }
+      if (hf == 0)
+        store_rows<HS>(lane_base, 256, any, valid, p.dv + krow * HS, 1.f, p.accumulate != 0);
+      else
+        store_rows<HS>(lane_base, 256 + HS, any, valid, p.dk + krow * HS, p.inv_scale, p.accumulate != 0);
     }
   } else if (warp == C::kTmaWarp) {
     // ---------------------------------------------------- producer
@@ -529,8 +535,8 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
           tma_load_4d(sK + sb * C::kSubBytes, &p.tm_k, kv_full, sb * 64, kvh, kt * 128, b);
           tma_load_4d(sV + sb * C::kSubBytes, &p.tm_v, kv_full, sb * 64, kvh, kt * 128, b);
         }
-        for (int g = 0; g < group; ++g) {
-          const int h = kvh * group + g;
+        for (int gh = 0; gh < group; ++gh) {
+          const int h = kvh * group + gh;
           for (int j = 0; j < n; ++j) {
             const int qt = p.tile_list[beg + j] & 0x7FFFFFFF;
             for (int which = 0; which < 2; ++which) {
@@ -558,9 +564,9 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
     const uint64_t v_desc = smem_desc_sw128(smem_u32(sV), 16, 1024);
     const uint64_t qd_desc0 = smem_desc_sw128(smem_u32(sQD), 16, 1024);
     const uint64_t qdmn_desc0 = smem_desc_sw128(smem_u32(sQD), C::kSubBytes, 1024);
-    uint32_t qd_it = 0, kv_phase = 0, pd_phase = 0;
+    uint32_t qd_it = 0, kv_phase = 0, g = 0;
     for (uint32_t it = 0;; ++it) {
-      const int u = get_unit(it, true);
+      const int u = get_unit(it);
       if (u >= p.num_units) break;
       const int kt = p.units[u] & 0xFFFF;
       const int n = p.tile_off[kt + 1] - p.tile_off[kt];
@@ -569,7 +575,7 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
       ++kv_phase;
       tc_fence_after();
       const int total = group * n;
-      for (int i = 0; i < total; ++i) {
+      for (int i = 0; i < total; ++i, ++g) {
         const uint32_t qi = qd_it + 2 * i, di = qi + 1;
         mbar_wait(&qd_full[qi % NS], (qi / NS) & 1);
         mbar_wait(&qd_full[di % NS], (di / NS) & 1);
@@ -597,22 +603,21 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
           __syncwarp();
         });
         bwd_commit(s_full);
-        mbar_wait(pd_ready, pd_phase & 1);
-        ++pd_phase;
-        tc_fence_after();
-        const uint32_t acc = i > 0 ? 1u : 0u;
-        bwd_dispatch_slot<NS>(di % NS, [&](auto S) {  // dV += P^T dO
-          constexpr int sl = decltype(S)::value;
-          const uint64_t bd = qdmn_desc0 + static_cast<uint64_t>((sl * C::kTileBytes) >> 4);
-          if (elect_one()) mma_pv_chain(256, 0, bd, C::kIdescTS, acc);
+        // dV += P^T dO and dK += dS^T Q, chunk by chunk
+        const uint64_t dbd = qdmn_desc0 + static_cast<uint64_t>((((di % NS) * C::kTileBytes)) >> 4);
+        const uint64_t qbd = qdmn_desc0 + static_cast<uint64_t>((((qi % NS) * C::kTileBytes)) >> 4);
+#pragma unroll
+        for (int n4 = 0; n4 < 4; ++n4) {
+          const int c = chunk_at(n4);
+          mbar_wait(&chunk_ready[c], g & 1);
+          tc_fence_after();
+          const uint32_t acc = (i > 0 || n4 > 0) ? 1u : 0u;
+          if (elect_one()) {
+            mma_ts_k2(256, packed_col(c), dbd + static_cast<uint64_t>(c * 256), C::kIdescTS, acc);
+            mma_ts_k2(256 + HS, 128 + packed_col(c), qbd + static_cast<uint64_t>(c * 256), C::kIdescTS, acc);
+          }
           __syncwarp();
-        });
-        bwd_dispatch_slot<NS>(qi % NS, [&](auto S) {  // dK += dS^T Q
-          constexpr int sl = decltype(S)::value;
-          const uint64_t bd = qdmn_desc0 + static_cast<uint64_t>((sl * C::kTileBytes) >> 4);
-          if (elect_one()) mma_pv_chain(256 + HS, 128, bd, C::kIdescTS, acc);
-          __syncwarp();
-        });
+        }
         bwd_commit(&qd_empty[qi % NS]);
         bwd_commit(&qd_empty[di % NS]);
       }

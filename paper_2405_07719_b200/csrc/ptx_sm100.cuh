@@ -234,6 +234,22 @@ __device__ __forceinline__ void mma_pv_chain(uint32_t d_tmem, uint32_t a_tmem, u
       : "memory");
 }
 
+// Two consecutive 16-deep k-steps of a TS MMA: A from TMEM columns a, a+8
+// (bf16 packed), B MN-major 16 rows (2 KB) further per step.
+__device__ __forceinline__ void mma_ts_k2(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p0, p1;\n\t.reg .b64 rb;\n\t.reg .b32 ta;\n\t"
+      "setp.ne.b32 p0, %4, 0;\n\t"
+      "setp.eq.u32 p1, 1, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p0;\n\t"
+      "add.u32 ta, %1, 8;\n\tadd.s64 rb, %2, 128;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], rb, %3, p1;\n\t"
+      "}"
+      ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // Arrives on `bar` once every previously issued tcgen05 op of this thread has
 // completed (implies tcgen05.fence::before_thread_sync).
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
