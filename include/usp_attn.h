@@ -142,6 +142,16 @@ USP_API usp_status usp_engine_create(const usp_config* cfg, usp_comm* comm, usp_
  * default stream). */
 USP_API usp_status usp_attn_fwd(usp_engine* engine, const void* q, const void* k, const void* v,
                         void* o, float* lse, void* stream);
+/* usp_attn_fwd with q, k, v, o, lse in HOST memory (same layouts), the
+ * host<->device copies inside the call — what a host-side caller of
+ * usp_attention (usp_attention.hpp:41-47, whose Tensor4 lives in host
+ * memory) binds. At U = R = 1 the copies are pipelined against the
+ * attention in sequence chunks (H2D of chunk c+1 and D2H of chunk c-1
+ * overlap chunk c's kernel). Pinned (page-locked) buffers are required for
+ * overlap; pageable ones work but serialise. Asynchronous on `stream`: the
+ * outputs are valid once the stream has been synchronised. */
+USP_API usp_status usp_attn_fwd_host(usp_engine* engine, const void* q, const void* k, const void* v,
+                                     void* o, float* lse, void* stream);
 /* Backward of the engine's last usp_attn_fwd: the reference's
  * usp_attention_backward<T> (src/usp/usp_attention.cpp:68-89) over
  * ring_attention_backward (src/usp/ring_attention.cpp:79-155).

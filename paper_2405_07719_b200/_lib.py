@@ -80,7 +80,7 @@ EXPORTS = [
     "usp_comm_create_nccl", "usp_comm_create_local", "usp_comm_destroy", "usp_engine_create",
     "usp_attn_fwd", "usp_engine_last_launches", "usp_engine_destroy", "usp_engine_enable_timing",
     "usp_engine_kernel_times", "usp_local_world_fwd", "usp_attn_bwd", "usp_local_world_bwd",
-    "usp_backward_ledger",
+    "usp_backward_ledger", "usp_attn_fwd_host",
     "usp_last_error", "usp_version",
 ]
 
@@ -113,6 +113,7 @@ def _declare(lib):
         "usp_comm_destroy": (None, [vp]),
         "usp_engine_create": (st, [P(UspConfig), vp, P(vp)]),
         "usp_attn_fwd": (st, [vp, vp, vp, vp, vp, vp, vp]),
+        "usp_attn_fwd_host": (st, [vp, vp, vp, vp, vp, vp, vp]),
         "usp_engine_last_launches": (ctypes.c_int32, [vp]),
         "usp_engine_destroy": (None, [vp]),
         "usp_engine_enable_timing": (st, [vp, ctypes.c_int32]),

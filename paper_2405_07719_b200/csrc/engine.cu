@@ -224,6 +224,12 @@ class Engine {
     for (auto e : ev_recv_) cudaEventDestroy(e);
     for (auto e : ev_acc_) cudaEventDestroy(e);
     if (comm_stream_) cudaStreamDestroy(comm_stream_);
+    for (auto e : ev_chunk_in_) cudaEventDestroy(e);
+    for (auto e : ev_chunk_out_) cudaEventDestroy(e);
+    if (ev_entry_) cudaEventDestroy(ev_entry_);
+    if (ev_drained_) cudaEventDestroy(ev_drained_);
+    if (h2d_stream_) cudaStreamDestroy(h2d_stream_);
+    if (d2h_stream_) cudaStreamDestroy(d2h_stream_);
   }
 
   static UspShape to_shape(const usp_config& c) {
@@ -357,6 +363,128 @@ class Engine {
     (void)e;
     have_fwd_ = true;
     fwd_ledger_size_ = ledger_.size();
+  }
+
+  // ------------------------------------------------------------ host buffers
+  // usp_attn_fwd_host: the same forward with Q/K/V/O/LSE in host memory; the
+  // host<->device copies are part of the call. At U = R = 1 (bs 1, native
+  // head size) the sequence is cut into chunks of C rows: chunk c's Q/K/V
+  // rows go up on h2d_stream_, its attention launch (query rows of chunk c
+  // against keys [0, (c+1)C) when causal — positions are the identity at
+  // U = R = 1 — or all keys otherwise) waits only for them, and its O/LSE
+  // rows go down on d2h_stream_. PCIe traffic then overlaps the attention of
+  // the neighbouring chunks instead of adding to it. Other meshes copy the
+  // whole shard around fwd().
+  void fwd_host(const void* q, const void* k, const void* v, void* o, float* lse, cudaStream_t st) {
+    USPB_CHECK(cudaSetDevice(cfg_.device));
+    for (const void* ptr : {q, k, v, static_cast<const void*>(o), static_cast<const void*>(lse)})
+      if (!ptr) throw_invalid("q, k, v, o, lse must be non-null host pointers");
+    const size_t qb = size_t(B_) * T_ * H_ * hs_ * 2, kvb = size_t(B_) * T_ * KV_ * hs_ * 2;
+    const size_t lb = size_t(B_) * Tr_ * hl_ * sizeof(float);
+    if (!hq_.p) {
+      hq_ = DevBuf(qb);
+      hk_ = DevBuf(kvb);
+      hv_ = DevBuf(kvb);
+      ho_ = DevBuf(qb);
+      hlse_ = DevBuf(lb);
+      USPB_CHECK(cudaStreamCreateWithFlags(&h2d_stream_, cudaStreamNonBlocking));
+      USPB_CHECK(cudaStreamCreateWithFlags(&d2h_stream_, cudaStreamNonBlocking));
+      USPB_CHECK(cudaEventCreateWithFlags(&ev_entry_, cudaEventDisableTiming));
+      USPB_CHECK(cudaEventCreateWithFlags(&ev_drained_, cudaEventDisableTiming));
+    }
+    const bool reshape = U_ > 1 || hs_ != hsk_;
+    const int64_t C = host_chunk_rows();
+    if (U_ > 1 || R_ > 1 || B_ > 1 || reshape || C >= Tr_) {
+      USPB_CHECK(cudaMemcpyAsync(hq_.p, q, qb, cudaMemcpyHostToDevice, st));
+      USPB_CHECK(cudaMemcpyAsync(hk_.p, k, kvb, cudaMemcpyHostToDevice, st));
+      USPB_CHECK(cudaMemcpyAsync(hv_.p, v, kvb, cudaMemcpyHostToDevice, st));
+      fwd(hq_.p, hk_.p, hv_.p, ho_.p, hlse_.as<float>(), st);
+      USPB_CHECK(cudaMemcpyAsync(o, ho_.p, qb, cudaMemcpyDeviceToHost, st));
+      USPB_CHECK(cudaMemcpyAsync(lse, hlse_.p, lb, cudaMemcpyDeviceToHost, st));
+      return;
+    }
+    ensure_chunk_plans(C);
+    launches_ = 0;
+    ledger_.clear();
+    for (int tsr = 0; tsr < 4; ++tsr) record_a2a(tsr, tsr == 0 || tsr == 3 ? q_part_ : kv_part_);
+    const int n = static_cast<int>(chunk_steps_.size());
+    const size_t qrow = size_t(H_) * hs_ * 2, kvrow = size_t(KV_) * hs_ * 2, lrow = size_t(hl_) * 4;
+    auto up = [&](DevBuf& d, const void* h, int64_t r0, int64_t r1, size_t row) {
+      USPB_CHECK(cudaMemcpyAsync(d.as<uint8_t>() + r0 * row, static_cast<const uint8_t*>(h) + r0 * row,
+                                 (r1 - r0) * row, cudaMemcpyHostToDevice, h2d_stream_));
+    };
+    // the previous call's kernels may still read the staging buffers
+    USPB_CHECK(cudaEventRecord(ev_entry_, st));
+    USPB_CHECK(cudaStreamWaitEvent(h2d_stream_, ev_entry_, 0));
+    USPB_CHECK(cudaStreamWaitEvent(d2h_stream_, ev_entry_, 0));
+    if (!shape_.causal) {
+      up(hk_, k, 0, Tr_, kvrow);
+      up(hv_, v, 0, Tr_, kvrow);
+    }
+    for (int c = 0; c < n; ++c) {
+      const int64_t r0 = c * C, r1 = std::min<int64_t>(Tr_, r0 + C);
+      if (shape_.causal) {
+        up(hk_, k, r0, r1, kvrow);
+        up(hv_, v, r0, r1, kvrow);
+      }
+      up(hq_, q, r0, r1, qrow);
+      USPB_CHECK(cudaEventRecord(ev_chunk_in_[c], h2d_stream_));
+      USPB_CHECK(cudaStreamWaitEvent(st, ev_chunk_in_[c], 0));
+      const int64_t k_len = shape_.causal ? r1 : Tr_;
+      const CUtensorMap tm_q = make_tmap(hq_.as<uint8_t>() + r0 * qrow, hsk_, hl_, r1 - r0, B_);
+      launch_plan(chunk_steps_[c], tm_q, hk_.p, hv_.p, ho_.as<uint8_t>() + r0 * qrow,
+                  hlse_.as<float>() + r0 * hl_, r1 - r0, k_len, st);
+      USPB_CHECK(cudaEventRecord(ev_chunk_out_[c], st));
+      USPB_CHECK(cudaStreamWaitEvent(d2h_stream_, ev_chunk_out_[c], 0));
+      USPB_CHECK(cudaMemcpyAsync(static_cast<uint8_t*>(o) + r0 * qrow, ho_.as<uint8_t>() + r0 * qrow,
+                                 (r1 - r0) * qrow, cudaMemcpyDeviceToHost, d2h_stream_));
+      USPB_CHECK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(lse) + r0 * lrow, hlse_.as<uint8_t>() + r0 * lrow,
+                                 (r1 - r0) * lrow, cudaMemcpyDeviceToHost, d2h_stream_));
+    }
+    USPB_CHECK(cudaEventRecord(ev_drained_, d2h_stream_));
+    USPB_CHECK(cudaStreamWaitEvent(st, ev_drained_, 0));
+    have_fwd_ = true;
+    fwd_ledger_size_ = ledger_.size();
+  }
+
+  // Rows per pipelined chunk: 8 chunks (USP_HOST_CHUNKS overrides), whole
+  // 128-row tiles, at least 4096 rows.
+  int64_t host_chunk_rows() const {
+    static const int want = [] {
+      const char* e = std::getenv("USP_HOST_CHUNKS");
+      return e ? std::max(1, std::atoi(e)) : 8;
+    }();
+    int64_t c = (Tr_ + want - 1) / want;
+    c = (c + kTileM - 1) / kTileM * kTileM;
+    return std::max<int64_t>(c, 4096);
+  }
+
+  void ensure_chunk_plans(int64_t C) {
+    if (!chunk_steps_.empty() && chunk_rows_ == C) return;
+    chunk_steps_.clear();
+    for (auto e : ev_chunk_in_) cudaEventDestroy(e);
+    for (auto e : ev_chunk_out_) cudaEventDestroy(e);
+    ev_chunk_in_.clear();
+    ev_chunk_out_.clear();
+    chunk_rows_ = C;
+    const auto pos = head_positions(shape_, cfg_.rank);
+    for (size_t i = 0; i < pos.size(); ++i)
+      if (pos[i] != int64_t(i)) throw Error(ErrorCode::kInternal, "chunked forward needs identity positions");
+    const int group = hl_ / kvl_;
+    for (int64_t r0 = 0; r0 < Tr_; r0 += C) {
+      const int64_t r1 = std::min<int64_t>(Tr_, r0 + C);
+      const std::vector<int64_t> qp(pos.begin() + r0, pos.begin() + r1);
+      const std::vector<int64_t> kp(pos.begin(), pos.begin() + (shape_.causal ? r1 : Tr_));
+      DevStep d;
+      upload_plan(d, plan_step(qp, kp, shape_.causal, B_, hl_ / nq_, true, std::max(1, group / nq_)));
+      d.mode = EpiMode::kSingle;
+      chunk_steps_.push_back(std::move(d));
+      cudaEvent_t a, b;
+      USPB_CHECK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+      USPB_CHECK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+      ev_chunk_in_.push_back(a);
+      ev_chunk_out_.push_back(b);
+    }
   }
 
   // ---------------------------------------------------------------- backward
@@ -716,13 +844,19 @@ class Engine {
 
   void launch_step(int t, const CUtensorMap& tm_q, const void* kb, const void* vb, void* o_heads,
                    float* lse, cudaStream_t st) {
-    const DevStep& s = steps_[t];
+    launch_plan(steps_[t], tm_q, kb, vb, o_heads, lse, Tr_, Tr_, st);
+  }
+
+  // One attention launch over plan s: q_len query rows (tm_q, o, lse start
+  // at the plan's first row) against the first k_len rows of K/V.
+  void launch_plan(const DevStep& s, const CUtensorMap& tm_q, const void* kb, const void* vb,
+                   void* o_heads, float* lse, int64_t q_len, int64_t k_len, cudaStream_t st) {
     if (s.host.units.empty()) return;
     FwdParams p;
     std::memset(&p, 0, sizeof(p));
     p.tm_q = tm_q;
-    p.tm_k = make_tmap(kb, hsk_, kvl_, Tr_, B_);
-    p.tm_v = make_tmap(vb, hsk_, kvl_, Tr_, B_);
+    p.tm_k = make_tmap(kb, hsk_, kvl_, k_len, B_);
+    p.tm_v = make_tmap(vb, hsk_, kvl_, k_len, B_);
     p.o = o_heads;
     p.lse = lse;
     p.o_acc = o_acc_.as<float>();
@@ -735,8 +869,8 @@ class Engine {
     p.sched = sched_.as<int>();
     p.num_units = static_cast<int>(s.host.units.size());
     p.batch = static_cast<int>(B_);
-    p.q_len = static_cast<int>(Tr_);
-    p.k_len = static_cast<int>(Tr_);
+    p.q_len = static_cast<int>(q_len);
+    p.k_len = static_cast<int>(k_len);
     p.heads = hl_;
     p.kv_heads = kvl_;
     p.mode = static_cast<int>(s.mode);
@@ -822,6 +956,13 @@ class Engine {
   DevBuf do_h_, delta_, dq_acc_, own_dkv_, grad_h_, grad_recv_;
   DevBuf acc_dkv_[2];
   std::vector<BwdStep> bwd_steps_;
+  // usp_attn_fwd_host staging and its chunk pipeline
+  DevBuf hq_, hk_, hv_, ho_, hlse_;
+  std::vector<DevStep> chunk_steps_;
+  int64_t chunk_rows_ = 0;
+  cudaStream_t h2d_stream_ = nullptr, d2h_stream_ = nullptr;
+  cudaEvent_t ev_entry_ = nullptr, ev_drained_ = nullptr;
+  std::vector<cudaEvent_t> ev_chunk_in_, ev_chunk_out_;
   std::vector<cudaEvent_t> ev_acc_;
   bool have_fwd_ = false;
   size_t fwd_ledger_size_ = 0;
@@ -1072,6 +1213,14 @@ usp_status usp_attn_fwd(usp_engine* engine, const void* q, const void* k, const 
   return guarded([&] {
     if (!engine) throw_invalid("engine is null");
     engine->impl->fwd(q, k, v, o, lse, static_cast<cudaStream_t>(stream));
+  });
+}
+
+usp_status usp_attn_fwd_host(usp_engine* engine, const void* q, const void* k, const void* v, void* o,
+                             float* lse, void* stream) {
+  return guarded([&] {
+    if (!engine) throw_invalid("engine is null");
+    engine->impl->fwd_host(q, k, v, o, lse, static_cast<cudaStream_t>(stream));
   });
 }
 

@@ -369,6 +369,27 @@ class UspAttention:
 
     __call__ = forward
 
+    def forward_host(self, q, k, v, out, lse, stream=None) -> UspForward:
+        """usp_attn_fwd_host: the forward with q, k, v, out, lse in host
+        memory (pinned CPU tensors for copy/compute overlap); the host<->device
+        copies run inside the call, pipelined against the attention in
+        sequence chunks at U = R = 1. ``out``/``lse`` are valid after the
+        stream is synchronised."""
+        import torch
+
+        for name, t, shape, dt in (("q", q, self.q_shape(), torch.bfloat16),
+                                   ("k", k, self.kv_shape(), torch.bfloat16),
+                                   ("v", v, self.kv_shape(), torch.bfloat16),
+                                   ("out", out, self.q_shape(), torch.bfloat16),
+                                   ("lse", lse, self.lse_shape(), torch.float32)):
+            if tuple(t.shape) != tuple(shape) or t.dtype != dt or t.is_cuda or not t.is_contiguous():
+                raise UspInvalidInput(2, f"{name} must be a contiguous {dt} host tensor of shape {shape}, "
+                                         f"got {tuple(t.shape)} {t.dtype} on {t.device}")
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        check(lib().usp_attn_fwd_host(self._h, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse),
+                                      ctypes.c_void_p(s.cuda_stream)))
+        return UspForward(out, lse, self.head_positions(), None, None, None)
+
     def alloc_grads(self):
         import torch
 
