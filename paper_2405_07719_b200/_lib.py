@@ -83,6 +83,11 @@ EXPORTS = [
     "usp_backward_ledger", "usp_attn_fwd_host",
     "usp_last_error", "usp_version",
 ]
+# Every symbol include/usp_sim.h declares (the reference's uspsim.h ABI).
+SIM_EXPORTS = [
+    "uspsim_run", "uspsim_report_json", "uspsim_report_text", "uspsim_report_ledger_csv",
+    "uspsim_report_exit_code", "uspsim_report_free", "uspsim_last_error", "uspsim_version",
+]
 
 _lib = None
 _lock = threading.Lock()
@@ -120,6 +125,14 @@ def _declare(lib):
         "usp_engine_kernel_times": (ctypes.c_int32, [vp, P(ctypes.c_float), ctypes.c_int32]),
         "usp_local_world_fwd": (st, [P(vp), ctypes.c_int32, P(vp), P(vp), P(vp), P(vp), P(vp), P(vp)]),
         "usp_last_error": (ctypes.c_char_p, []),
+        "uspsim_run": (st, [ctypes.c_char_p, P(vp)]),
+        "uspsim_report_json": (ctypes.c_char_p, [vp]),
+        "uspsim_report_text": (ctypes.c_char_p, [vp]),
+        "uspsim_report_ledger_csv": (ctypes.c_char_p, [vp]),
+        "uspsim_report_exit_code": (ctypes.c_int, [vp]),
+        "uspsim_report_free": (None, [vp]),
+        "uspsim_last_error": (ctypes.c_char_p, []),
+        "uspsim_version": (ctypes.c_char_p, []),
         "usp_version": (ctypes.c_char_p, []),
     }
     for name, (res, args) in sig.items():

@@ -18,7 +18,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libusp_b200.so")
 OBJ = os.path.join(HERE, "build")
-SOURCES = ["fa_fwd_sm100.cu", "fa_bwd_sm100.cu", "reshard.cu", "engine.cu", "plan.cpp", "transport.cpp"]
+SOURCES = ["fa_fwd_sm100.cu", "fa_bwd_sm100.cu", "reshard.cu", "engine.cu", "plan.cpp", "transport.cpp",
+           "simulate.cu", "check_fp64.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -39,7 +40,7 @@ def _compile(src: str) -> str:
     obj = os.path.join(OBJ, os.path.basename(src) + ".o")
     path = os.path.join(CSRC, src)
     deps = [path] + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".hpp", ".cuh", ".h"))]
-    deps.append(os.path.join(ROOT, "include", "usp_attn.h"))
+    deps += [os.path.join(ROOT, "include", h) for h in ("usp_attn.h", "usp_sim.h")]
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps):
         return obj
     lang = [] if src.endswith(".cu") else ["-x", "cu"]
