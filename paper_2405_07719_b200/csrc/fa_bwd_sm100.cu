@@ -66,6 +66,11 @@ struct BwdCfg {
                                      ? 6
                                      : (kBudget - 2 * kTileBytes) / kTileBytes;
   static constexpr int kSmemBytes = 1024 + 2 * kTileBytes + kStages * kTileBytes + 4096;
+  // dq kernel: K tiles in a 3-slot ring (released after the tile's dQ MMAs),
+  // V tiles in a 2-slot ring (released as soon as dP has been computed)
+  static constexpr int kKSlots = 3, kVSlots = 2;
+  static constexpr int kDqSmemBytes = 1024 + (2 + kKSlots + kVSlots) * kTileBytes + 512;
+  static_assert(kDqSmemBytes <= 227 * 1024, "dq smem");
   static constexpr uint32_t kIdescSS = idesc_bf16_f32(128, 128, 0, 0);  // S / dP
   static constexpr uint32_t kIdescTS = idesc_bf16_f32(128, HS, 0, 1);   // acc += X * tile
   static_assert(kStages >= 2, "smem");
@@ -129,41 +134,53 @@ __device__ __forceinline__ void store_rows(uint32_t lane_base, uint32_t col, boo
 template <int HS>
 __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(const __grid_constant__ BwdParams p) {
   using C = BwdCfg<HS>;
-  constexpr int NS = C::kStages;
+  constexpr int NK = C::kKSlots, NV = C::kVSlots;
   constexpr uint32_t kDP = 128, kDQ = 256, kS1 = 384;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
   uint8_t* sDO = smem + C::kTileBytes;
-  uint8_t* sKV = smem + 2 * C::kTileBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + NS * C::kTileBytes);
+  uint8_t* sK = smem + 2 * C::kTileBytes;   // [NK]
+  uint8_t* sV = sK + NK * C::kTileBytes;     // [NV]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + NV * C::kTileBytes);
   uint64_t* q_full = bars;            // Q + dO landed
   uint64_t* q_empty = bars + 1;
   uint64_t* s_full = bars + 2;        // [2] S buffer b computed
   uint64_t* dp_full = bars + 4;       // dP computed
-  uint64_t* chunk_ready = bars + 5;   // [4] dS chunk in TMEM (128 arrivals)
-  uint64_t* dq_full = bars + 9;       // unit's last dQ MMA done
-  uint64_t* kv_full = bars + 10;      // [NS]
-  uint64_t* kv_empty = kv_full + NS;  // [NS]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_empty + NS);
+  // [2][4] dS chunk in TMEM (128 arrivals), by tile parity: the compute
+  // warps may finish tile j+1's chunks before the MMA warp has waited for
+  // tile j's (dP(j+1) is issued ahead of tile j's dQ MMAs)
+  uint64_t* chunk_ready = bars + 5;
+  uint64_t* dq_full = bars + 13;      // unit's last dQ MMA done
+  uint64_t* k_full = bars + 14;       // [NK]
+  uint64_t* k_empty = k_full + NK;    // [NK]
+  uint64_t* v_full = k_empty + NK;    // [NV]
+  uint64_t* v_empty = v_full + NV;    // [NV]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(v_empty + NV);
   int* unit_slot = reinterpret_cast<int*>(tmem_slot + 2);
   uint64_t* u_full = reinterpret_cast<uint64_t*>(unit_slot + 2);
   uint64_t* u_empty = u_full + 1;
+  uint64_t* dp_free = u_empty + 1;    // tile's dP loaded by every compute warp
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
+    mbar_init(dp_free, C::kCompute);
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
     mbar_init(&s_full[0], 1);
     mbar_init(&s_full[1], 1);
     mbar_init(dp_full, 1);
-    for (int c = 0; c < 4; ++c) mbar_init(&chunk_ready[c], 128);
+    for (int c = 0; c < 8; ++c) mbar_init(&chunk_ready[c], 128);
     mbar_init(dq_full, 1);
     mbar_init(u_full, 1);
     mbar_init(u_empty, C::kCompute + 1);
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
+    for (int s = 0; s < NK; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < NV; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
     }
     fence_barrier_init();
   }
@@ -208,14 +225,24 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
         mbar_wait(&s_full[g & 1], (g >> 1) & 1);
         mbar_wait(dp_full, g & 1);
         tc_fence_after();
-#pragma unroll 1
+        // Both of this warp's chunks of S and dP into registers at once, so
+        // the dP buffer is released before the elementwise work: dP(j+1) is
+        // computed while this tile's dS is formed.
+        uint32_t s2[64], dp2[64];
+        tmem_ld32(lane_base + sb + (2 * hf) * 32, s2);
+        tmem_ld32(lane_base + sb + (2 * hf + 1) * 32, s2 + 32);
+        tmem_ld32(lane_base + kDP + (2 * hf) * 32, dp2);
+        tmem_ld32(lane_base + kDP + (2 * hf + 1) * 32, dp2 + 32);
+        tmem_ld_wait(s2);
+        tmem_ld_wait(dp2);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(dp_free);
+#pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
           const int c = 2 * hf + cc;
-          uint32_t s[32], dp[32];
-          tmem_ld32(lane_base + sb + c * 32, s);
-          tmem_ld32(lane_base + kDP + c * 32, dp);
-          tmem_ld_wait(s);
-          tmem_ld_wait(dp);
+          uint32_t* s = s2 + 32 * cc;
+          const uint32_t* dp = dp2 + 32 * cc;
           if (entry < 0) {
             const int kt = entry & 0x7FFFFFFF;
             const int4* kp4 = reinterpret_cast<const int4*>(p.k_pos + kt * 128 + c * 32);
@@ -233,12 +260,12 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
           for (int i = 0; i < 16; ++i) {
             const float p0 = ex2(fmaf(__uint_as_float(s[2 * i]), sl2, -lse2));
             const float p1 = ex2(fmaf(__uint_as_float(s[2 * i + 1]), sl2, -lse2));
-            pk[i] = pack_bf16x2(p0 * (__uint_as_float(dp[2 * i]) - dlt), p1 * (__uint_as_float(dp[2 * i + 1]) - dlt));
+            pk[i] = pack_bf16x2_int(p0 * (__uint_as_float(dp[2 * i]) - dlt), p1 * (__uint_as_float(dp[2 * i + 1]) - dlt));
           }
           st16(lane_base + sb + packed_col(c), pk);  // dS chunk c, over already-consumed S columns
           tmem_st_wait();
           tc_fence_before();
-          mbar_arrive(&chunk_ready[c]);
+          mbar_arrive(&chunk_ready[(g & 1) * 4 + c]);
         }
       }
       // epilogue: dq (+)= dQ / sqrt(hs); warp half hf stores half the columns
@@ -272,18 +299,19 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
           tma_load_4d(sDO + sb * C::kSubBytes, &p.tm_do, q_full, sb * 64, h, qt * 128, b);
         }
         const int kvh = h / group;
-        for (int j = 0; j < n; ++j) {
+        for (int j = 0; j < n; ++j, ++kv_it) {
           const int kt = p.tile_list[beg + j] & 0x7FFFFFFF;
-          for (int which = 0; which < 2; ++which) {
-            const uint32_t slot = kv_it % NS;
-            mbar_wait(&kv_empty[slot], ((kv_it / NS) & 1) ^ 1);
-            ++kv_it;
-            mbar_arrive_expect_tx(&kv_full[slot], C::kTileBytes);
-            const CUtensorMap* tm = which == 0 ? &p.tm_k : &p.tm_v;
-            for (int sb = 0; sb < C::kSub; ++sb)
-              tma_load_4d(sKV + slot * C::kTileBytes + sb * C::kSubBytes, tm, &kv_full[slot], sb * 64,
-                          kvh, kt * 128, b);
-          }
+          const uint32_t ks = kv_it % NK, vs = kv_it % NV;
+          mbar_wait(&k_empty[ks], ((kv_it / NK) & 1) ^ 1);
+          mbar_arrive_expect_tx(&k_full[ks], C::kTileBytes);
+          for (int sb = 0; sb < C::kSub; ++sb)
+            tma_load_4d(sK + ks * C::kTileBytes + sb * C::kSubBytes, &p.tm_k, &k_full[ks], sb * 64, kvh,
+                        kt * 128, b);
+          mbar_wait(&v_empty[vs], ((kv_it / NV) & 1) ^ 1);
+          mbar_arrive_expect_tx(&v_full[vs], C::kTileBytes);
+          for (int sb = 0; sb < C::kSub; ++sb)
+            tma_load_4d(sV + vs * C::kTileBytes + sb * C::kSubBytes, &p.tm_v, &v_full[vs], sb * 64, kvh,
+                        kt * 128, b);
         }
       }
       if (atomicAdd(&p.sched[1], 1) == static_cast<int>(gridDim.x) - 1) {
@@ -296,13 +324,15 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
     // ---------------------------------------------------- MMA issue
     const uint64_t q_desc = smem_desc_sw128(smem_u32(sQ), 16, 1024);
     const uint64_t do_desc = smem_desc_sw128(smem_u32(sDO), 16, 1024);
-    const uint64_t kv_desc0 = smem_desc_sw128(smem_u32(sKV), 16, 1024);
-    const uint64_t kvmn_desc0 = smem_desc_sw128(smem_u32(sKV), C::kSubBytes, 1024);
+    const uint64_t k_desc0 = smem_desc_sw128(smem_u32(sK), 16, 1024);
+    const uint64_t v_desc0 = smem_desc_sw128(smem_u32(sV), 16, 1024);
+    const uint64_t kmn_desc0 = smem_desc_sw128(smem_u32(sK), C::kSubBytes, 1024);
     uint32_t kv_it = 0, q_phase = 0, g = 0;
-    auto ss = [&](uint32_t d, uint64_t ad, uint32_t slot) {  // D = A * B^T, B K-major from slot
-      bwd_dispatch_slot<NS>(slot, [&](auto S) {
+    // D = A * B^T with B K-major: a K tile (S) or a V tile (dP) from its ring
+    auto ss = [&](uint32_t d, uint64_t ad, uint64_t b0, uint32_t slot, auto nslots) {
+      bwd_dispatch_slot<decltype(nslots)::value>(slot, [&](auto S) {
         constexpr int sl = decltype(S)::value;
-        const uint64_t bd = kv_desc0 + static_cast<uint64_t>((sl * C::kTileBytes) >> 4);
+        const uint64_t bd = b0 + static_cast<uint64_t>((sl * C::kTileBytes) >> 4);
         if (elect_one()) {
           if constexpr (HS == 128)
             mma_qk_hs128(d, ad, bd, C::kIdescSS, 0u);
@@ -312,7 +342,20 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
         __syncwarp();
       });
     };
-    auto wait_slot = [&](uint32_t i) { mbar_wait(&kv_full[i % NS], (i / NS) & 1); };
+    using KN = std::integral_constant<int, NK>;
+    using VN = std::integral_constant<int, NV>;
+    auto issue_s = [&](uint32_t t, uint32_t buf) {  // S(t) = Q K(t)^T
+      mbar_wait(&k_full[t % NK], (t / NK) & 1);
+      tc_fence_after();
+      ss(buf, q_desc, k_desc0, t % NK, KN{});
+    };
+    auto issue_dp = [&](uint32_t t) {  // dP(t) = dO V(t)^T; V(t) is free afterwards
+      mbar_wait(&v_full[t % NV], (t / NV) & 1);
+      tc_fence_after();
+      ss(kDP, do_desc, v_desc0, t % NV, VN{});
+      bwd_commit(dp_full);
+      bwd_commit(&v_empty[t % NV]);
+    };
     for (uint32_t it = 0;; ++it) {
       const int u = get_unit(it);
       if (u >= p.num_units) break;
@@ -321,33 +364,31 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
       if (n == 0) continue;
       mbar_wait(q_full, q_phase & 1);
       ++q_phase;
-      wait_slot(kv_it);
-      tc_fence_after();
-      ss((g & 1) ? kS1 : 0u, q_desc, kv_it % NS);  // S(0)
+      issue_s(kv_it, (g & 1) ? kS1 : 0u);  // S(0)
       bwd_commit(&s_full[g & 1]);
-      wait_slot(kv_it + 1);
-      tc_fence_after();
-      ss(kDP, do_desc, (kv_it + 1) % NS);  // dP(0)
-      bwd_commit(dp_full);
+      if (g > 0) mbar_wait(dp_free, (g - 1) & 1);  // the previous tile's dP was loaded
+      issue_dp(kv_it);                              // dP(0)
       for (int j = 0; j < n; ++j, ++g) {
-        const uint32_t ki = kv_it + 2 * j;
-        if (j + 1 < n) {  // S(j+1) into the other buffer, overlapping tile j's elementwise work
-          wait_slot(ki + 2);
-          tc_fence_after();
-          ss(((g + 1) & 1) ? kS1 : 0u, q_desc, (ki + 2) % NS);
+        const uint32_t t = kv_it + j;
+        if (j + 1 < n) {
+          // S(j+1) into the other buffer and dP(j+1) as soon as tile j's dP
+          // is in registers: both overlap tile j's elementwise work
+          issue_s(t + 1, ((g + 1) & 1) ? kS1 : 0u);
           bwd_commit(&s_full[(g + 1) & 1]);
+          mbar_wait(dp_free, g & 1);
+          issue_dp(t + 1);
         } else {
           bwd_commit(q_empty);  // every MMA reading Q / dO has been issued
         }
         const uint32_t sb = (g & 1) ? kS1 : 0u;
         // dQ += dS K, chunk by chunk (K tile as the MN-major B operand)
-        bwd_dispatch_slot<NS>(ki % NS, [&](auto S) {
+        bwd_dispatch_slot<NK>(t % NK, [&](auto S) {
           constexpr int sl = decltype(S)::value;
-          const uint64_t bd = kvmn_desc0 + static_cast<uint64_t>((sl * C::kTileBytes) >> 4);
+          const uint64_t bd = kmn_desc0 + static_cast<uint64_t>((sl * C::kTileBytes) >> 4);
 #pragma unroll
           for (int n4 = 0; n4 < 4; ++n4) {
             const int c = chunk_at(n4);
-            mbar_wait(&chunk_ready[c], g & 1);
+            mbar_wait(&chunk_ready[(g & 1) * 4 + c], (g >> 1) & 1);
             tc_fence_after();
             if (elect_one())
               mma_ts_k2(kDQ, sb + packed_col(c), bd + static_cast<uint64_t>(c * 256), C::kIdescTS,
@@ -355,17 +396,10 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
             __syncwarp();
           }
         });
-        bwd_commit(&kv_empty[ki % NS]);
-        bwd_commit(&kv_empty[(ki + 1) % NS]);
-        if (j + 1 < n) {  // dP(j+1): tile j's dP has been read (all chunks ready)
-          wait_slot(ki + 3);
-          tc_fence_after();
-          ss(kDP, do_desc, (ki + 3) % NS);
-          bwd_commit(dp_full);
-        }
+        bwd_commit(&k_empty[t % NK]);
       }
       bwd_commit(dq_full);
-      kv_it += 2 * n;
+      kv_it += n;
     }
   }
   tc_fence_before();
@@ -401,7 +435,8 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
   int* unit_slot = reinterpret_cast<int*>(tmem_slot + 2);
   uint64_t* u_full = reinterpret_cast<uint64_t*>(unit_slot + 2);
   uint64_t* u_empty = u_full + 1;
-  float* vec = reinterpret_cast<float*>(u_empty + 1);  // [2 parity][lse2 128 | delta 128 | qpos 128]
+  // [2 parity][lse2 128 | delta 128 | qpos 128], addressed in the shared window
+  const uint32_t vec_s = (smem_u32(u_empty + 1) + 15u) & ~15u;  // 16-byte aligned for ld.shared.v4
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -449,55 +484,79 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
       const int beg = p.tile_off[kt], n = p.tile_off[kt + 1] - beg;
       const int k_row = kt * 128 + key_in_tile;
       const int kpos = p.k_pos[k_row];
-      for (int gh = 0; gh < group; ++gh) {
-        const int h = kvh * group + gh;
-        for (int j = 0; j < n; ++j, ++g) {
-          const int entry = p.tile_list[beg + j];
-          const int qt = entry & 0x7FFFFFFF;
-          // this q tile's lse2 / delta / q positions -> shared (parity buffer)
-          float* vb = vec + (g & 1) * 384;
-          {
-            const int qr = qt * 128 + key_in_tile;
-            const bool ok = qr < p.q_len;
-            if (hf == 0) {
-              const size_t r = (static_cast<size_t>(b) * p.q_len + (ok ? qr : 0)) * p.heads + h;
-              vb[key_in_tile] = ok ? p.lse[r] * 1.4426950408889634f : INFINITY;  // padding rows: p = 0
-              vb[128 + key_in_tile] = ok ? p.delta[r] : 0.f;
-            } else {
-              vb[256 + key_in_tile] = __int_as_float(p.q_pos[qr]);
-            }
-          }
-          bwd_bar_sync(1, 32 * C::kCompute);
-          mbar_wait(s_full, g & 1);
-          tc_fence_after();
+      // Per q tile, lse2 / delta / q positions of its 128 rows go through
+      // shared memory (a parity-double-buffered 3 x 128 vector). Their global
+      // loads are issued one q tile ahead, so the L2 latency hides behind
+      // the previous tile's MMAs and elementwise work.
+      const int total = group * n;
+      auto fetch = [&](int i, float& fl, float& fd, int& fq) {
+        const int h = kvh * group + i / n;
+        const int qt = p.tile_list[beg + i % n] & 0x7FFFFFFF;
+        const int qr = qt * 128 + key_in_tile;
+        const bool ok = qr < p.q_len;
+        const size_t r = (static_cast<size_t>(b) * p.q_len + (ok ? qr : 0)) * p.heads + h;
+        if (hf == 0) {
+          fl = ok ? p.lse[r] * 1.4426950408889634f : INFINITY;  // padding rows: p = 0
+          fd = ok ? p.delta[r] : 0.f;
+        } else {
+          fq = p.q_pos[qr];
+        }
+      };
+      float nl = 0.f, nd = 0.f;
+      int nq = 0;
+      if (total > 0) fetch(0, nl, nd, nq);
+      for (int i = 0; i < total; ++i, ++g) {
+        const int entry = p.tile_list[beg + i % n];
+        const uint32_t vb = vec_s + (g & 1) * (384 * 4);
+        if (hf == 0) {
+          sts_f32(vb + key_in_tile * 4, nl);
+          sts_f32(vb + (128 + key_in_tile) * 4, nd);
+        } else {
+          sts_f32(vb + (256 + key_in_tile) * 4, __int_as_float(nq));
+        }
+        if (i + 1 < total) fetch(i + 1, nl, nd, nq);
+        bwd_bar_sync(1, 32 * C::kCompute);
+        mbar_wait(s_full, g & 1);
+        tc_fence_after();
 #pragma unroll 1
-          for (int cc = 0; cc < 2; ++cc) {
-            const int c = 2 * hf + cc;
-            uint32_t s[32], dp[32];
-            tmem_ld32(lane_base + c * 32, s);
-            tmem_ld32(lane_base + 128 + c * 32, dp);
-            tmem_ld_wait(s);
-            tmem_ld_wait(dp);
-            uint32_t pp[16], pd[16];
+        for (int cc = 0; cc < 2; ++cc) {
+          const int c = 2 * hf + cc;
+          uint32_t s[32], dp[32];
+          tmem_ld32(lane_base + c * 32, s);
+          tmem_ld32(lane_base + 128 + c * 32, dp);
+          tmem_ld_wait(s);
+          tmem_ld_wait(dp);
+          uint32_t pp[16], pd[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int q0 = c * 32 + 2 * i, q1 = q0 + 1;
-              float p0 = ex2(fmaf(__uint_as_float(s[2 * i]), sl2, -vb[q0]));
-              float p1 = ex2(fmaf(__uint_as_float(s[2 * i + 1]), sl2, -vb[q1]));
-              if (entry < 0) {
-                if (kpos > __float_as_int(vb[256 + q0])) p0 = 0.f;
-                if (kpos > __float_as_int(vb[256 + q1])) p1 = 0.f;
-              }
-              pp[i] = pack_bf16x2(p0, p1);
-              pd[i] = pack_bf16x2(p0 * (__uint_as_float(dp[2 * i]) - vb[128 + q0]),
-                                  p1 * (__uint_as_float(dp[2 * i + 1]) - vb[128 + q1]));
+          for (int i4 = 0; i4 < 8; ++i4) {
+            const uint32_t col = (c * 32 + 4 * i4) * 4;
+            const float4 L4 = lds_f4(vb + col);
+            const float4 D4 = lds_f4(vb + 512 + col);
+            const float lv[4] = {L4.x, L4.y, L4.z, L4.w};
+            const float dv[4] = {D4.x, D4.y, D4.z, D4.w};
+            float pv[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) pv[e] = ex2(fmaf(__uint_as_float(s[4 * i4 + e]), sl2, -lv[e]));
+            if (entry < 0) {
+              const float4 Q4 = lds_f4(vb + 1024 + col);
+              const int qv[4] = {__float_as_int(Q4.x), __float_as_int(Q4.y), __float_as_int(Q4.z),
+                                 __float_as_int(Q4.w)};
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (kpos > qv[e]) pv[e] = 0.f;
             }
-            st16(lane_base + packed_col(c), pp);
-            st16(lane_base + 128 + packed_col(c), pd);
-            tmem_st_wait();
-            tc_fence_before();
-            mbar_arrive(&chunk_ready[c]);
+#pragma unroll
+            for (int e = 0; e < 4; e += 2) {
+              pp[2 * i4 + e / 2] = pack_bf16x2_pos(pv[e], pv[e + 1]);
+              pd[2 * i4 + e / 2] = pack_bf16x2_int(pv[e] * (__uint_as_float(dp[4 * i4 + e]) - dv[e]),
+                                                   pv[e + 1] * (__uint_as_float(dp[4 * i4 + e + 1]) - dv[e + 1]));
+            }
           }
+          st16(lane_base + packed_col(c), pp);
+          st16(lane_base + 128 + packed_col(c), pd);
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(&chunk_ready[c]);
         }
       }
       // epilogue: warp half 0 stores dv (+)= dV, half 1 dk (+)= dK / sqrt(hs)
@@ -675,13 +734,13 @@ cudaError_t set_smem(K kern, int bytes) {
 
 cudaError_t launch_bwd_dq(const BwdParams& p, int hs, int grid, cudaStream_t stream) {
   if (hs == 128) {
-    static cudaError_t once = set_smem(fa_bwd_dq_kernel<128>, BwdCfg<128>::kSmemBytes);
+    static cudaError_t once = set_smem(fa_bwd_dq_kernel<128>, BwdCfg<128>::kDqSmemBytes);
     if (once != cudaSuccess) return once;
-    fa_bwd_dq_kernel<128><<<grid, BwdCfg<128>::kThreads, BwdCfg<128>::kSmemBytes, stream>>>(p);
+    fa_bwd_dq_kernel<128><<<grid, BwdCfg<128>::kThreads, BwdCfg<128>::kDqSmemBytes, stream>>>(p);
   } else if (hs == 64) {
-    static cudaError_t once = set_smem(fa_bwd_dq_kernel<64>, BwdCfg<64>::kSmemBytes);
+    static cudaError_t once = set_smem(fa_bwd_dq_kernel<64>, BwdCfg<64>::kDqSmemBytes);
     if (once != cudaSuccess) return once;
-    fa_bwd_dq_kernel<64><<<grid, BwdCfg<64>::kThreads, BwdCfg<64>::kSmemBytes, stream>>>(p);
+    fa_bwd_dq_kernel<64><<<grid, BwdCfg<64>::kThreads, BwdCfg<64>::kDqSmemBytes, stream>>>(p);
   } else {
     return cudaErrorInvalidValue;
   }

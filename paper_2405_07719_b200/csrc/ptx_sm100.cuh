@@ -85,6 +85,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Explicit shared-space accesses (a pointer derived from the aligned
+// dynamic-smem base is generic to the compiler; LD.E/ST.E on it cost a
+// long-scoreboard round trip each).
+__device__ __forceinline__ float4 lds_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+
 // --------------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
@@ -383,6 +395,12 @@ __device__ __forceinline__ uint32_t pack_bf16x2_pos(float lo, float hi) {
   asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(r) : "r"(a), "r"(b));
   return r;
 }
+// The same integer-pipe packing for finite floats of either sign: the bit
+// pattern is sign-magnitude, so +0x8000 rounds |x| half up (ties away from
+// zero instead of to even). Used for dS in the backward, where
+// cvt.rn.bf16x2.f32 would double the load on the MUFU pipe the exponentials
+// already saturate.
+__device__ __forceinline__ uint32_t pack_bf16x2_int(float lo, float hi) { return pack_bf16x2_pos(lo, hi); }
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));

@@ -8,6 +8,7 @@
 // defines them (reference src/simcomm/mesh.cpp:41-57).
 #include "transport.hpp"
 
+#include <algorithm>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -212,9 +213,12 @@ class NcclTransport final : public Transport {
     std::memcpy(&uid, id, sizeof(uid));
     ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
     cfg.blocking = 1;
-    max_ctas_ = env_int("USP_NCCL_MAX_CTAS", 4);
-    cfg.maxCTAs = max_ctas_;
-    cfg.minCTAs = 1;
+    // Only the ring communicator runs concurrently with the attention kernel
+    // (whose persistent grid leaves reserved_sms() SMs for it); a K/V block
+    // shift needs a few GB/s to hide behind a ring step, so a couple of CTAs
+    // suffice. The Ulysses all-to-alls run between kernels and get NCCL's
+    // default channel count (full NVLink bandwidth).
+    max_ctas_ = std::max(1, env_int("USP_NCCL_MAX_CTAS", 2));
     nccl_check(api.CommInitRankConfig(&world_, n, uid, rank, &cfg), "ncclCommInitRankConfig");
   }
   ~NcclTransport() override {
@@ -230,15 +234,17 @@ class NcclTransport final : public Transport {
     g->rank = rank;
     g->ulysses = ug;
     g->ring = rg;
-    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
-    cfg.blocking = 1;
-    cfg.maxCTAs = max_ctas_;
-    cfg.minCTAs = 1;
+    ncclConfig_t ucfg = NCCL_CONFIG_INITIALIZER;
+    ucfg.blocking = 1;
+    ncclConfig_t rcfg = NCCL_CONFIG_INITIALIZER;
+    rcfg.blocking = 1;
+    rcfg.maxCTAs = max_ctas_;
+    rcfg.minCTAs = 1;
     ncclComm_t uc = nullptr, rc = nullptr;
     // color = the other mesh coordinate; key = position inside the group.
     const int u = index_of(ug, rank), r = index_of(rg, rank);
-    nccl_check(nccl().CommSplit(world_, /*color=*/r, /*key=*/u, &uc, &cfg), "ncclCommSplit(ulysses)");
-    nccl_check(nccl().CommSplit(world_, /*color=*/u, /*key=*/r, &rc, &cfg), "ncclCommSplit(ring)");
+    nccl_check(nccl().CommSplit(world_, /*color=*/r, /*key=*/u, &uc, &ucfg), "ncclCommSplit(ulysses)");
+    nccl_check(nccl().CommSplit(world_, /*color=*/u, /*key=*/r, &rc, &rcfg), "ncclCommSplit(ring)");
     owned_.push_back(uc);
     owned_.push_back(rc);
     g->ulysses_comm = uc;
@@ -287,7 +293,7 @@ class NcclTransport final : public Transport {
 
  private:
   int n_;
-  int max_ctas_ = 4;
+  int max_ctas_ = 2;
   ncclComm_t world_ = nullptr;
   std::vector<ncclComm_t> owned_;
 };
