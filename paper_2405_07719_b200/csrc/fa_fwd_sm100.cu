@@ -29,6 +29,9 @@
 #include "fa_fwd.hpp"
 #include "ptx_sm100.cuh"
 
+#ifndef USPB_FWD_STAGES
+#define USPB_FWD_STAGES 4  // K/V pipeline depth: measured best at 4 (2 tiles of K+V) on B200
+#endif
 namespace uspb200 {
 
 using namespace ptx;
@@ -57,7 +60,7 @@ struct FwdCfg {
   static constexpr int kKVBytes = kTileN * HS * 2;
   static constexpr int kBudget = 227 * 1024 - 2048;
   static constexpr int kStagesFit = (kBudget - NQ * kQBytes) / kKVBytes;
-  static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
+  static constexpr int kStages = kStagesFit > USPB_FWD_STAGES ? USPB_FWD_STAGES : kStagesFit;
   static constexpr int kSchedDepth = 4;  // unit-ticket ring between producer and consumers
   static constexpr int kNumBars = 3 * NQ + 2 + NQ + 2 * kStages + 2 * kSchedDepth;
   static constexpr int kSmemBytes = 1024 /*align slack*/ + NQ * kQBytes + kStages * kKVBytes +
