@@ -26,6 +26,13 @@
 #include "fa_fwd.hpp"
 #include "ptx_sm100.cuh"
 
+#ifndef USPB_DQ_KSLOTS
+#define USPB_DQ_KSLOTS 3
+#endif
+#ifndef USPB_DKDV_STAGES
+#define USPB_DKDV_STAGES 6
+#endif
+
 namespace uspb200 {
 namespace {
 
@@ -62,13 +69,13 @@ struct BwdCfg {
   static constexpr int kThreads = 32 * (kCompute + 2);
   static constexpr int kTmaWarp = kCompute, kMmaWarp = kCompute + 1;
   static constexpr int kBudget = 227 * 1024 - 4096;
-  static constexpr int kStages = (kBudget - 2 * kTileBytes) / kTileBytes > 6
-                                     ? 6
+  static constexpr int kStages = (kBudget - 2 * kTileBytes) / kTileBytes > USPB_DKDV_STAGES
+                                     ? USPB_DKDV_STAGES
                                      : (kBudget - 2 * kTileBytes) / kTileBytes;
   static constexpr int kSmemBytes = 1024 + 2 * kTileBytes + kStages * kTileBytes + 4096;
   // dq kernel: K tiles in a 3-slot ring (released after the tile's dQ MMAs),
   // V tiles in a 2-slot ring (released as soon as dP has been computed)
-  static constexpr int kKSlots = 3, kVSlots = 2;
+  static constexpr int kKSlots = USPB_DQ_KSLOTS, kVSlots = 2;
   static constexpr int kDqSmemBytes = 1024 + (2 + kKSlots + kVSlots) * kTileBytes + 512;
   static_assert(kDqSmemBytes <= 227 * 1024, "dq smem");
   static constexpr uint32_t kIdescSS = idesc_bf16_f32(128, 128, 0, 0);  // S / dP
@@ -426,10 +433,12 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
   uint64_t* bars = reinterpret_cast<uint64_t*>(sQD + NS * C::kTileBytes);
   uint64_t* kv_full = bars;          // K + V landed
   uint64_t* kv_empty = bars + 1;
-  uint64_t* s_full = bars + 2;       // S^T and dP^T in TMEM
-  uint64_t* chunk_ready = bars + 3;  // [4] P^T, dS^T chunk written (128 arrivals)
+  uint64_t* s_full = bars + 2;       // S^T in TMEM
+  uint64_t* p_ready = bars + 3;      // [4] P^T chunk written (128 arrivals)
   uint64_t* acc_full = bars + 7;     // unit's last dV/dK MMA done
-  uint64_t* qd_full = bars + 8;      // [NS]
+  uint64_t* dp_full = bars + 8;      // dP^T in TMEM
+  uint64_t* ds_ready = bars + 9;     // [4] dS^T chunk written (128 arrivals)
+  uint64_t* qd_full = bars + 13;     // [NS]
   uint64_t* qd_empty = qd_full + NS;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qd_empty + NS);
   int* unit_slot = reinterpret_cast<int*>(tmem_slot + 2);
@@ -443,7 +452,11 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
     mbar_init(kv_full, 1);
     mbar_init(kv_empty, 1);
     mbar_init(s_full, 1);
-    for (int c = 0; c < 4; ++c) mbar_init(&chunk_ready[c], 128);
+    mbar_init(dp_full, 1);
+    for (int c = 0; c < 4; ++c) {
+      mbar_init(&p_ready[c], 128);
+      mbar_init(&ds_ready[c], 128);
+    }
     mbar_init(acc_full, 1);
     mbar_init(u_full, 1);
     mbar_init(u_empty, C::kCompute + 1);
@@ -516,27 +529,26 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
         }
         if (i + 1 < total) fetch(i + 1, nl, nd, nq);
         bwd_bar_sync(1, 32 * C::kCompute);
+        // phase 1: P^T = exp(S^T - lse) (thread = key row), packed over the
+        // consumed S^T columns for the dV MMAs; fp32 P kept for phase 2
         mbar_wait(s_full, g & 1);
         tc_fence_after();
-#pragma unroll 1
+        uint32_t pp2[2][16];  // bf16 P^T pairs, reused by phase 2
+#pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
           const int c = 2 * hf + cc;
-          uint32_t s[32], dp[32];
-          tmem_ld32(lane_base + c * 32, s);
-          tmem_ld32(lane_base + 128 + c * 32, dp);
-          tmem_ld_wait(s);
-          tmem_ld_wait(dp);
-          uint32_t pp[16], pd[16];
+          uint32_t sv[32];
+          tmem_ld32(lane_base + c * 32, sv);
+          tmem_ld_wait(sv);
+          uint32_t* pp = pp2[cc];
 #pragma unroll
           for (int i4 = 0; i4 < 8; ++i4) {
             const uint32_t col = (c * 32 + 4 * i4) * 4;
             const float4 L4 = lds_f4(vb + col);
-            const float4 D4 = lds_f4(vb + 512 + col);
             const float lv[4] = {L4.x, L4.y, L4.z, L4.w};
-            const float dv[4] = {D4.x, D4.y, D4.z, D4.w};
             float pv[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) pv[e] = ex2(fmaf(__uint_as_float(s[4 * i4 + e]), sl2, -lv[e]));
+            for (int e = 0; e < 4; ++e) pv[e] = ex2(fmaf(__uint_as_float(sv[4 * i4 + e]), sl2, -lv[e]));
             if (entry < 0) {
               const float4 Q4 = lds_f4(vb + 1024 + col);
               const int qv[4] = {__float_as_int(Q4.x), __float_as_int(Q4.y), __float_as_int(Q4.z),
@@ -545,18 +557,42 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
               for (int e = 0; e < 4; ++e)
                 if (kpos > qv[e]) pv[e] = 0.f;
             }
-#pragma unroll
-            for (int e = 0; e < 4; e += 2) {
-              pp[2 * i4 + e / 2] = pack_bf16x2_pos(pv[e], pv[e + 1]);
-              pd[2 * i4 + e / 2] = pack_bf16x2_int(pv[e] * (__uint_as_float(dp[4 * i4 + e]) - dv[e]),
-                                                   pv[e + 1] * (__uint_as_float(dp[4 * i4 + e + 1]) - dv[e + 1]));
-            }
+            pp[2 * i4] = pack_bf16x2_pos(pv[0], pv[1]);
+            pp[2 * i4 + 1] = pack_bf16x2_pos(pv[2], pv[3]);
           }
           st16(lane_base + packed_col(c), pp);
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(&p_ready[c]);
+        }
+        // phase 2: dS^T = P^T (dP^T - delta), packed over the consumed dP^T
+        // columns for the dK MMAs (S^T(i+1) is computed meanwhile)
+        mbar_wait(dp_full, g & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          const int c = 2 * hf + cc;
+          uint32_t dp[32];
+          tmem_ld32(lane_base + 128 + c * 32, dp);
+          tmem_ld_wait(dp);
+          uint32_t pd[16];
+#pragma unroll
+          for (int i4 = 0; i4 < 8; ++i4) {
+            const float4 D4 = lds_f4(vb + 512 + (c * 32 + 4 * i4) * 4);
+            const float dv[4] = {D4.x, D4.y, D4.z, D4.w};
+#pragma unroll
+            for (int e = 0; e < 4; e += 2) {
+              // P^T as the dV MMA consumed it (bf16), widened
+              const uint32_t w = pp2[cc][2 * i4 + e / 2];
+              const float p0 = __uint_as_float(w << 16), p1 = __uint_as_float(w & 0xFFFF0000u);
+              pd[2 * i4 + e / 2] = pack_bf16x2_int(p0 * (__uint_as_float(dp[4 * i4 + e]) - dv[e]),
+                                                   p1 * (__uint_as_float(dp[4 * i4 + e + 1]) - dv[e + 1]));
+            }
+          }
           st16(lane_base + 128 + packed_col(c), pd);
           tmem_st_wait();
           tc_fence_before();
-          mbar_arrive(&chunk_ready[c]);
+          mbar_arrive(&ds_ready[c]);
         }
       }
       // epilogue: warp half 0 stores dv (+)= dV, half 1 dk (+)= dK / sqrt(hs)
@@ -634,48 +670,68 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
       ++kv_phase;
       tc_fence_after();
       const int total = group * n;
+      auto ss = [&](uint32_t d, uint64_t ad, uint32_t slot) {  // D = A * B^T, B K-major from slot
+        bwd_dispatch_slot<NS>(slot, [&](auto S) {
+          constexpr int sl = decltype(S)::value;
+          const uint64_t bd = qd_desc0 + static_cast<uint64_t>((sl * C::kTileBytes) >> 4);
+          if (elect_one()) {
+            if constexpr (HS == 128)
+              mma_qk_hs128(d, ad, bd, C::kIdescSS, 0u);
+            else
+              mma_qk_hs64(d, ad, bd, C::kIdescSS, 0u);
+          }
+          __syncwarp();
+        });
+      };
+      auto wait_qd = [&](uint32_t x) {
+        mbar_wait(&qd_full[x % NS], (x / NS) & 1);
+        tc_fence_after();
+      };
+      // S^T(0) = K Q(0)^T, dP^T(0) = V dO(0)^T
+      wait_qd(qd_it);
+      ss(0, k_desc, qd_it % NS);
+      bwd_commit(s_full);
+      wait_qd(qd_it + 1);
+      ss(128, v_desc, (qd_it + 1) % NS);
+      bwd_commit(dp_full);
       for (int i = 0; i < total; ++i, ++g) {
         const uint32_t qi = qd_it + 2 * i, di = qi + 1;
-        mbar_wait(&qd_full[qi % NS], (qi / NS) & 1);
-        mbar_wait(&qd_full[di % NS], (di / NS) & 1);
-        tc_fence_after();
-        bwd_dispatch_slot<NS>(qi % NS, [&](auto S) {  // S^T = K Q^T
-          constexpr int sl = decltype(S)::value;
-          const uint64_t bd = qd_desc0 + static_cast<uint64_t>((sl * C::kTileBytes) >> 4);
-          if (elect_one()) {
-            if constexpr (HS == 128)
-              mma_qk_hs128(0, k_desc, bd, C::kIdescSS, 0u);
-            else
-              mma_qk_hs64(0, k_desc, bd, C::kIdescSS, 0u);
-          }
-          __syncwarp();
-        });
-        bwd_dispatch_slot<NS>(di % NS, [&](auto S) {  // dP^T = V dO^T
-          constexpr int sl = decltype(S)::value;
-          const uint64_t bd = qd_desc0 + static_cast<uint64_t>((sl * C::kTileBytes) >> 4);
-          if (elect_one()) {
-            if constexpr (HS == 128)
-              mma_qk_hs128(128, v_desc, bd, C::kIdescSS, 0u);
-            else
-              mma_qk_hs64(128, v_desc, bd, C::kIdescSS, 0u);
-          }
-          __syncwarp();
-        });
-        bwd_commit(s_full);
-        // dV += P^T dO and dK += dS^T Q, chunk by chunk
         const uint64_t dbd = qdmn_desc0 + static_cast<uint64_t>((((di % NS) * C::kTileBytes)) >> 4);
         const uint64_t qbd = qdmn_desc0 + static_cast<uint64_t>((((qi % NS) * C::kTileBytes)) >> 4);
+        const uint32_t acc = i > 0 ? 1u : 0u;
+        // dV += P^T dO(i), chunk by chunk as P^T lands
 #pragma unroll
         for (int n4 = 0; n4 < 4; ++n4) {
           const int c = chunk_at(n4);
-          mbar_wait(&chunk_ready[c], g & 1);
+          mbar_wait(&p_ready[c], g & 1);
           tc_fence_after();
-          const uint32_t acc = (i > 0 || n4 > 0) ? 1u : 0u;
-          if (elect_one()) {
-            mma_ts_k2(256, packed_col(c), dbd + static_cast<uint64_t>(c * 256), C::kIdescTS, acc);
-            mma_ts_k2(256 + HS, 128 + packed_col(c), qbd + static_cast<uint64_t>(c * 256), C::kIdescTS, acc);
-          }
+          if (elect_one())
+            mma_ts_k2(256, packed_col(c), dbd + static_cast<uint64_t>(c * 256), C::kIdescTS, (acc | n4) ? 1u : 0u);
           __syncwarp();
+        }
+        // S^T(i+1) over the S^T region (its P^T is consumed by the dV MMAs
+        // issued above): overlaps this tile's dS^T work
+        if (i + 1 < total) {
+          wait_qd(qi + 2);
+          ss(0, k_desc, (qi + 2) % NS);
+          bwd_commit(s_full);
+        }
+        // dK += dS^T Q(i), chunk by chunk as dS^T lands
+#pragma unroll
+        for (int n4 = 0; n4 < 4; ++n4) {
+          const int c = chunk_at(n4);
+          mbar_wait(&ds_ready[c], g & 1);
+          tc_fence_after();
+          if (elect_one())
+            mma_ts_k2(256 + HS, 128 + packed_col(c), qbd + static_cast<uint64_t>(c * 256), C::kIdescTS,
+                      (acc | n4) ? 1u : 0u);
+          __syncwarp();
+        }
+        // dP^T(i+1) over the dP^T region (its dS^T is consumed by the dK MMAs)
+        if (i + 1 < total) {
+          wait_qd(di + 2);
+          ss(128, v_desc, (di + 2) % NS);
+          bwd_commit(dp_full);
         }
         bwd_commit(&qd_empty[qi % NS]);
         bwd_commit(&qd_empty[di % NS]);

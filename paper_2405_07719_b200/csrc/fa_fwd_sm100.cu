@@ -29,6 +29,9 @@
 #include "fa_fwd.hpp"
 #include "ptx_sm100.cuh"
 
+#ifndef USPB_FWD_SPLIT
+#define USPB_FWD_SPLIT 1  // softmax warps per TMEM lane quarter and q tile (2: measured equal per cycle)
+#endif
 #ifndef USPB_FWD_STAGES
 #define USPB_FWD_STAGES 4  // K/V pipeline depth: measured best at 4 (2 tiles of K+V) on B200
 #endif
@@ -36,34 +39,47 @@ namespace uspb200 {
 
 using namespace ptx;
 
-template <int NQ, int HS, int POLY>
+template <int NQ, int HS, int POLY, int SPL>
 struct FwdCfg {
-  static constexpr int kSoftmaxWarps = 4 * NQ;
+  // SPL softmax warps per TMEM lane quarter and q tile, each owning 128/SPL
+  // of the key columns: with SPL = 2 two warps of every SM sub-partition
+  // run a q tile's exponentials concurrently (one warp alone issues MUFU.EX2
+  // at ~1/12 per cycle; two keep the 1/8-per-cycle pipe busy).
+  static constexpr int kSplit = SPL;
+  static constexpr int kCols = 128 / SPL;  // key columns per softmax warp
+  static constexpr int kSoftmaxWarps = 4 * NQ * SPL;
   static constexpr int kTmaWarp = kSoftmaxWarps;
   static constexpr int kMmaWarp = kSoftmaxWarps + 1;
-  // NQ == 2: a full third warpgroup (TMA, MMA, 2 idle warps) so registers
+  // NQ == 2: a full extra warpgroup (TMA, MMA, 2 idle warps) so registers
   // can be moved to the softmax warpgroups with setmaxnreg.
   static constexpr bool kRegSplit = NQ == 2;
   // producer warpgroup: TMA warp, S-issue warp, PV-issue warp, 1 idle
   static constexpr int kPvWarp = kSoftmaxWarps + 2;
   static constexpr int kThreads = 32 * (kSoftmaxWarps + 4);
-  static constexpr int kSoftmaxRegs = 208;  // 8 x 208 + 4 x 88 = 384 x 168 (the launch allocation)
-  static constexpr int kProducerRegs = 88;
   // setmaxnreg only redistributes the registers allocated at launch
-  // (384 threads x 168 under __launch_bounds__(384, 1)); asking for more
-  // would block the .inc forever.
-  static_assert(!kRegSplit || 8 * 32 * kSoftmaxRegs + 4 * 32 * kProducerRegs <= 384 * 168,
+  // (kThreads x kLaunchRegs under __launch_bounds__(kThreads, 1)); asking for
+  // more would block the .inc forever.
+  static constexpr int kLaunchRegs = (65536 / kThreads) / 8 * 8;
+  static constexpr int kProducerRegs = SPL == 1 ? 88 : 64;
+  static constexpr int kSoftmaxRegs =
+      ((kLaunchRegs * kThreads - 128 * kProducerRegs) / (32 * kSoftmaxWarps)) / 8 * 8 > 240
+          ? 240
+          : ((kLaunchRegs * kThreads - 128 * kProducerRegs) / (32 * kSoftmaxWarps)) / 8 * 8;
+  static_assert(!kRegSplit || 32 * kSoftmaxWarps * kSoftmaxRegs + 128 * kProducerRegs <= kThreads * kLaunchRegs,
                 "register split exceeds the launch allocation");
   static constexpr int kSub = HS / 64;           // 128-byte (64 x bf16) column blocks
   static constexpr int kSubBytes = 128 * 128;    // one block: 128 rows x 128 B
   static constexpr int kQBytes = kTileM * HS * 2;
   static constexpr int kKVBytes = kTileN * HS * 2;
-  static constexpr int kBudget = 227 * 1024 - 2048;
+  // sibling-warp exchange (SPL == 2): row maxima [2 parity][NQ][SPL][128]
+  // and row sums / epilogue weights [2 parity][NQ][SPL][128]
+  static constexpr int kXchgBytes = SPL == 1 ? 0 : 2 * (2 * NQ * SPL * 128 * 4);
+  static constexpr int kBudget = 227 * 1024 - 2048 - kXchgBytes;
   static constexpr int kStagesFit = (kBudget - NQ * kQBytes) / kKVBytes;
   static constexpr int kStages = kStagesFit > USPB_FWD_STAGES ? USPB_FWD_STAGES : kStagesFit;
   static constexpr int kSchedDepth = 4;  // unit-ticket ring between producer and consumers
   static constexpr int kNumBars = 3 * NQ + 2 + NQ + 2 * kStages + 2 * kSchedDepth;
-  static constexpr int kSmemBytes = 1024 /*align slack*/ + NQ * kQBytes + kStages * kKVBytes +
+  static constexpr int kSmemBytes = 1024 /*align slack*/ + NQ * kQBytes + kStages * kKVBytes + kXchgBytes +
                                     kNumBars * 8 + 16 + 4 * kSchedDepth;
   // TMEM: ONE S buffer shared by the q tiles (time-multiplexed: the MMA
   // warp computes the next tile's S as soon as the previous S has been
@@ -74,6 +90,7 @@ struct FwdCfg {
   static constexpr uint32_t kColsUsed = kOCol + NQ * HS;
   static constexpr uint32_t kTmemCols = kColsUsed <= 128 ? 128 : (kColsUsed <= 256 ? 256 : 512);
   static_assert(HS == 64 || HS == 128, "head_size must be 64 or 128 on the tcgen05 path");
+  static_assert(SPL == 1 || SPL == 2, "one or two softmax warps per lane quarter");
   static_assert(kStages >= 2, "not enough shared memory for a K/V pipeline");
 };
 
@@ -132,17 +149,18 @@ __device__ __forceinline__ int next_unit_impl(uint64_t* full, uint64_t* empty, c
 #define next_unit(full, empty, slot, it, whole_warp) \
   next_unit_impl<C::kSchedDepth>(full, empty, slot, it, whole_warp)
 
-template <int NQ, int HS, int POLY>
-__global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY>::kThreads, 1)
+template <int NQ, int HS, int POLY, int SPL>
+__global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
     fa_fwd_sm100_kernel(const __grid_constant__ FwdParams p) {
-  using C = FwdCfg<NQ, HS, POLY>;
+  using C = FwdCfg<NQ, HS, POLY, SPL>;
   constexpr int NS = C::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sQ = smem;
   uint8_t* sKV = smem + NQ * C::kQBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + NS * C::kKVBytes);
+  const uint32_t xchg = smem_u32(sKV + NS * C::kKVBytes);  // sibling-warp exchange (SPL == 2)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + NS * C::kKVBytes + C::kXchgBytes);
   uint64_t* q_full = bars;              // [NQ]  TMA -> MMA
   uint64_t* q_empty = q_full + NQ;      // [1]   MMA -> TMA
   uint64_t* kv_full = q_empty + 1;      // [NS]  TMA -> MMA
@@ -163,10 +181,10 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY>::kThreads, 1)
     for (int t = 0; t < NQ; ++t) {
       mbar_init(&q_full[t], 1);
       mbar_init(&s_full[t], 1);
-      mbar_init(&p_ready[t], 128);
+      mbar_init(&p_ready[t], 128 * SPL);
       mbar_init(&pv_done[t], 1);
     }
-    mbar_init(s_free, 4);  // one elected lane of each warp of the group holding S
+    mbar_init(s_free, 4 * SPL);  // one lane of each warp of the group holding S
     mbar_init(q_empty, 1);
     for (int d = 0; d < C::kSchedDepth; ++d) {
       mbar_init(&sched_full[d], 1);
@@ -197,13 +215,26 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY>::kThreads, 1)
     // ------------------------------------------------------------ softmax
     if constexpr (C::kRegSplit)
       asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::kSoftmaxRegs));
-    const int t = warp >> 2;
-    const int quarter = warp & 3;
+    constexpr int KC = C::kCols;
+    const int t = warp / (4 * SPL);
+    const int quarter = warp & 3;             // TMEM lane quarter (warp id % 4)
+    const int half = (warp / 4) % SPL;        // which 128/SPL key columns
     const int row_in_tile = quarter * 32 + lane;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-    const uint32_t s_addr = lane_base + C::kSCol;
-    const uint32_t p_addr = lane_base + C::kPCol + t * 64;
-    const uint32_t o_addr = lane_base + C::kOCol + t * HS;
+    const uint32_t s_addr = lane_base + C::kSCol + half * KC;
+    const uint32_t p_addr = lane_base + C::kPCol + t * 64 + half * (KC / 2);
+    const uint32_t o_addr = lane_base + C::kOCol + t * HS + half * (HS / SPL);
+    // sibling exchange slots (SPL == 2): [parity][t][half][row] floats
+    const uint32_t bar_id = 1 + t * 4 + quarter;
+    auto xslot = [&](uint32_t region, uint32_t parity, int h) {
+      return xchg + region * (2 * NQ * SPL * 128 * 4) +
+             ((((parity * NQ + t) * SPL + h) * 128 + row_in_tile) << 2);
+    };
+    auto ld_sh = [](uint32_t a) {
+      float v;
+      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+      return v;
+    };
     const float sl2 = p.scale_log2;
     uint32_t s_phase = 0, pv_phase = 0;
     for (uint32_t it = 0;; ++it) {
@@ -220,25 +251,26 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY>::kThreads, 1)
       for (int j = 0; j < n; ++j) {
         const int entry = p.tile_list[beg + j];
         mbar_wait(&s_full[t], s_phase & 1);
-        const bool tr = (warp & 3) == 0 && lane == 0;
+        const bool tr = quarter == 0 && half == 0 && lane == 0;
         if (tr) trace_ev(p, 0 + 5 * t, s_phase);
+        const uint32_t par = s_phase & 1;
         ++s_phase;
         tc_fence_after();
-        uint32_t s[128];
+        uint32_t s[KC];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld32(s_addr + c * 32, s + c * 32);
+        for (int c = 0; c < KC / 32; ++c) tmem_ld32(s_addr + c * 32, s + c * 32);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld_wait(s + c * 32);
+        for (int c = 0; c < KC / 32; ++c) tmem_ld_wait(s + c * 32);
         // S is in registers: the shared S buffer may take the next S.
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(s_free);
-        if (tr) trace_ev(p, 1 + 5 * t, s_phase - 1, __uint_as_float(s[127]));
+        if (tr) trace_ev(p, 1 + 5 * t, s_phase - 1, __uint_as_float(s[KC - 1]));
         if (entry < 0) {  // partial tile: apply the position mask per element
           const int kt = entry & 0x7FFFFFFF;
-          const int4* kp4 = reinterpret_cast<const int4*>(p.k_pos + kt * kTileN);
+          const int4* kp4 = reinterpret_cast<const int4*>(p.k_pos + kt * kTileN + half * KC);
 #pragma unroll
-          for (int c = 0; c < 32; ++c) {
+          for (int c = 0; c < KC / 4; ++c) {
             const int4 kp = __ldg(kp4 + c);
             if (kp.x > qpos) s[4 * c + 0] = __float_as_uint(-INFINITY);
             if (kp.y > qpos) s[4 * c + 1] = __float_as_uint(-INFINITY);
@@ -249,13 +281,19 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY>::kThreads, 1)
         float mx0 = __uint_as_float(s[0]), mx1 = __uint_as_float(s[1]);
         float mx2 = __uint_as_float(s[2]), mx3 = __uint_as_float(s[3]);
 #pragma unroll
-        for (int i = 4; i < 128; i += 4) {
+        for (int i = 4; i < KC; i += 4) {
           mx0 = fmaxf(mx0, __uint_as_float(s[i + 0]));
           mx1 = fmaxf(mx1, __uint_as_float(s[i + 1]));
           mx2 = fmaxf(mx2, __uint_as_float(s[i + 2]));
           mx3 = fmaxf(mx3, __uint_as_float(s[i + 3]));
         }
-        const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+        float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+        if constexpr (SPL == 2) {
+          // the row max over both halves: both siblings end with the same value
+          sts_f32(xslot(0, par, half), mx);
+          asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+          mx = fmaxf(mx, ld_sh(xslot(0, par, half ^ 1)));
+        }
         if (tr) trace_ev(p, 2 + 5 * t, s_phase - 1, mx);
         const float m_new = fmaxf(m_run, mx * sl2);
         float alpha = 1.f;
@@ -276,7 +314,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY>::kThreads, 1)
         float2 acc2 = make_float2(0.f, 0.f);
         if (POLY > 0 && entry >= 0) {
 #pragma unroll
-          for (int i = 0; i < 64; ++i) {
+          for (int i = 0; i < KC / 2; ++i) {
             const float2 x = ffma2(make_float2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])),
                                    sc2, nb2);
             float2 e;
@@ -291,7 +329,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY>::kThreads, 1)
           }
         } else {
 #pragma unroll
-          for (int i = 0; i < 64; ++i) {
+          for (int i = 0; i < KC / 2; ++i) {
             const float2 x = ffma2(make_float2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])),
                                    sc2, nb2);
             float2 e;
@@ -303,18 +341,18 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY>::kThreads, 1)
         }
         const float sum0 = acc2.x, sum1 = acc2.y;
         if (tr) trace_ev(p, 3 + 5 * t, s_phase - 1, sum0 + sum1);
-        l_run = l_run * alpha + (sum0 + sum1);
+        l_run = l_run * alpha + (sum0 + sum1);  // this warp's columns only (SPL == 2)
         if (j > 0) {
           // PV_t(j-1) must be done before P_t is overwritten and O_t rescaled
           mbar_wait(&pv_done[t], pv_phase & 1);
           ++pv_phase;
           tc_fence_after();
         }
-        tmem_st32(p_addr, s);
-        tmem_st32(p_addr + 32, s + 32);
+#pragma unroll
+        for (int c = 0; c < KC / 64; ++c) tmem_st32(p_addr + c * 32, s + c * 32);
         if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
-          for (int c = 0; c < HS / 32; ++c) {
+          for (int c = 0; c < HS / SPL / 32; ++c) {
             uint32_t o[32];
             tmem_ld32(o_addr + c * 32, o);
             tmem_ld_wait(o);
@@ -337,12 +375,23 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY>::kThreads, 1)
       }
       const bool valid = q_row < p.q_len;
       const size_t row = (static_cast<size_t>(b) * p.q_len + q_row) * p.heads + h;
+      const int mode = p.mode;
+      const bool merge = mode == static_cast<int>(EpiMode::kMiddle) || mode == static_cast<int>(EpiMode::kLast);
+      // the running LSE of earlier ring steps (read before the sibling
+      // barrier below, after which half 0 may overwrite it)
+      const float acc_lse = (merge && valid) ? p.lse_acc[row] : -INFINITY;
+      if constexpr (SPL == 2) {
+        // the row sum over both halves, added in the same order by both
+        sts_f32(xslot(1, it & 1, half), l_run);
+        asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+        const float other = ld_sh(xslot(1, it & 1, half ^ 1));
+        l_run = half == 0 ? l_run + other : other + l_run;
+      }
       const float lse_t = l_run > 0.f ? m_use + log2f(l_run) : -INFINITY;  // log2 domain
       const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
       float w_run = 0.f, w_new = inv_l, lse_out = lse_t;
-      const int mode = p.mode;
-      if (mode == static_cast<int>(EpiMode::kMiddle) || mode == static_cast<int>(EpiMode::kLast)) {
-        const float a = valid ? p.lse_acc[row] : -INFINITY;
+      if (merge) {
+        const float a = acc_lse;
         const float mx = fmaxf(a, lse_t);
         if (mx == -INFINITY) {
           lse_out = -INFINITY;
@@ -357,8 +406,9 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY>::kThreads, 1)
       const bool write_bf16 =
           mode == static_cast<int>(EpiMode::kSingle) || mode == static_cast<int>(EpiMode::kLast);
       const bool read_acc = mode >= static_cast<int>(EpiMode::kMiddle);
+      const int col0 = half * (HS / SPL);  // this warp's O columns
 #pragma unroll 1
-      for (int c = 0; c < HS / 32; ++c) {
+      for (int c = 0; c < HS / SPL / 32; ++c) {
         float o[32];
         if (n > 0) {
           uint32_t r[32];
@@ -372,7 +422,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY>::kThreads, 1)
         }
         if (!valid) continue;
         if (read_acc) {
-          const float4* acc4 = reinterpret_cast<const float4*>(p.o_acc + row * HS + c * 32);
+          const float4* acc4 = reinterpret_cast<const float4*>(p.o_acc + row * HS + col0 + c * 32);
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const float4 a = acc4[i];
@@ -383,7 +433,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY>::kThreads, 1)
           }
         }
         if (write_bf16) {
-          uint4* dst = reinterpret_cast<uint4*>(static_cast<uint8_t*>(p.o) + (row * HS + c * 32) * 2);
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<uint8_t*>(p.o) + (row * HS + col0 + c * 32) * 2);
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             dst[i] = make_uint4(pack_bf16x2(o[8 * i + 0], o[8 * i + 1]),
@@ -392,13 +442,13 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY>::kThreads, 1)
                                 pack_bf16x2(o[8 * i + 6], o[8 * i + 7]));
           }
         } else {
-          float4* dst = reinterpret_cast<float4*>(p.o_acc + row * HS + c * 32);
+          float4* dst = reinterpret_cast<float4*>(p.o_acc + row * HS + col0 + c * 32);
 #pragma unroll
           for (int i = 0; i < 8; ++i)
             dst[i] = make_float4(o[4 * i + 0], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
         }
       }
-      if (valid) {
+      if (valid && half == 0) {
         if (write_bf16)
           p.lse[row] = lse_out * 0.69314718055994530942f;  // natural log (attention.cpp:260)
         else
@@ -585,10 +635,10 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY>::kThreads, 1)
 }
 
 // --------------------------------------------------------------- launchers
-template <int NQ, int HS, int POLY>
+template <int NQ, int HS, int POLY, int SPL>
 static cudaError_t launch_impl(const FwdParams& p, int grid, cudaStream_t stream) {
-  using C = FwdCfg<NQ, HS, POLY>;
-  auto kern = fa_fwd_sm100_kernel<NQ, HS, POLY>;
+  using C = FwdCfg<NQ, HS, POLY, SPL>;
+  auto kern = fa_fwd_sm100_kernel<NQ, HS, POLY, SPL>;
   static bool attr_set = false;  // per instantiation; set before first launch
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -600,34 +650,36 @@ static cudaError_t launch_impl(const FwdParams& p, int grid, cudaStream_t stream
   return cudaGetLastError();
 }
 
-// Fraction of softmax exponentials on the FMA-pipe polynomial: POLY/8.
-static int poly_setting() {
-  static int v = [] {
-    const char* e = getenv("USP_FA_POLY");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
+// Development knobs: USP_FA_POLY = POLY/8 of the exponentials on the FMA
+// pipe; USP_FA_SPLIT = softmax warps per lane quarter (1 or 2).
+static int env_setting(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
 }
 
 template <int NQ, int HS>
-static cudaError_t launch_poly(const FwdParams& p, int grid, cudaStream_t stream) {
-  switch (poly_setting()) {
-    case 0: return launch_impl<NQ, HS, 0>(p, grid, stream);
-    case 3: return launch_impl<NQ, HS, 3>(p, grid, stream);
-    case 4: return launch_impl<NQ, HS, 4>(p, grid, stream);
-    case 2: return launch_impl<NQ, HS, 2>(p, grid, stream);
-    default: return launch_impl<NQ, HS, 0>(p, grid, stream);
+static cudaError_t launch_variant(const FwdParams& p, int grid, cudaStream_t stream) {
+  static const int poly = env_setting("USP_FA_POLY", 0);
+  static const int split = env_setting("USP_FA_SPLIT", USPB_FWD_SPLIT);
+  if (split == 1) {
+    switch (poly) {
+      case 2: return launch_impl<NQ, HS, 2, 1>(p, grid, stream);
+      default: return launch_impl<NQ, HS, 0, 1>(p, grid, stream);
+    }
+  }
+  switch (poly) {
+    case 2: return launch_impl<NQ, HS, 2, 2>(p, grid, stream);
+    default: return launch_impl<NQ, HS, 0, 2>(p, grid, stream);
   }
 }
 
 cudaError_t launch_fa_fwd(const FwdParams& p, int nq, int hs, int grid, cudaStream_t stream) {
-  if (nq == 2 && hs == 128) return launch_poly<2, 128>(p, grid, stream);
-  if (nq == 1 && hs == 128) return launch_poly<1, 128>(p, grid, stream);
-  if (nq == 2 && hs == 64) return launch_poly<2, 64>(p, grid, stream);
-  if (nq == 1 && hs == 64) return launch_poly<1, 64>(p, grid, stream);
+  if (nq == 2 && hs == 128) return launch_variant<2, 128>(p, grid, stream);
+  if (nq == 1 && hs == 128) return launch_variant<1, 128>(p, grid, stream);
+  if (nq == 2 && hs == 64) return launch_variant<2, 64>(p, grid, stream);
+  if (nq == 1 && hs == 64) return launch_variant<1, 64>(p, grid, stream);
   return cudaErrorInvalidValue;
 }
 
-int fa_fwd_threads(int nq) { return nq == 2 ? 32 * 12 : 32 * 6; }
 
 }  // namespace uspb200
