@@ -66,7 +66,13 @@ struct BwdCfg {
   // 8 compute warps (two per TMEM lane quarter, each owning half of the
   // tile's columns), the TMA warp and the MMA warp
   static constexpr int kCompute = 8;
-  static constexpr int kThreads = 32 * (kCompute + 2);
+  // three full warpgroups (warps 10, 11 idle) so setmaxnreg can move
+  // registers to the compute warps: per SM sub-partition 2 x 208 + 1 x 88
+  // (384 threads x 168 at launch); without it 10 warps cap every thread at
+  // 168 registers and the compute warps spill
+  static constexpr int kThreads = 32 * (kCompute + 4);
+  static constexpr int kComputeRegs = 208, kProducerRegs = 88;
+  static_assert(kCompute * 32 * kComputeRegs + 128 * kProducerRegs <= kThreads * 168, "register split");
   static constexpr int kTmaWarp = kCompute, kMmaWarp = kCompute + 1;
   static constexpr int kBudget = 227 * 1024 - 4096;
   static constexpr int kStages = (kBudget - 2 * kTileBytes) / kTileBytes > USPB_DKDV_STAGES
@@ -207,7 +213,9 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
     return u;
   };
 
+  if (warp >= C::kCompute) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(C::kProducerRegs));
   if (warp < C::kCompute) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::kComputeRegs));
     // ---------------------------------------------------- compute warps
     const int q4 = warp & 3, hf = warp >> 2;
     const int row_in_tile = q4 * 32 + lane;
@@ -482,7 +490,9 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
     return u;
   };
 
+  if (warp >= C::kCompute) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(C::kProducerRegs));
   if (warp < C::kCompute) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::kComputeRegs));
     // ---------------------------------------------------- compute warps (thread = key row)
     const int q4 = warp & 3, hf = warp >> 2;
     const int key_in_tile = q4 * 32 + lane;
