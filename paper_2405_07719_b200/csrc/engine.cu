@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -368,13 +369,13 @@ class Engine {
   // ------------------------------------------------------------ host buffers
   // usp_attn_fwd_host: the same forward with Q/K/V/O/LSE in host memory; the
   // host<->device copies are part of the call. At U = R = 1 (bs 1, native
-  // head size) the sequence is cut into chunks of C rows: chunk c's Q/K/V
+  // head size) the sequence is cut into row chunks [r0, r1): chunk c's Q/K/V
   // rows go up on h2d_stream_, its attention launch (query rows of chunk c
-  // against keys [0, (c+1)C) when causal — positions are the identity at
+  // against keys [0, r1) when causal — positions are the identity at
   // U = R = 1 — or all keys otherwise) waits only for them, and its O/LSE
   // rows go down on d2h_stream_. PCIe traffic then overlaps the attention of
-  // the neighbouring chunks instead of adding to it. Other meshes copy the
-  // whole shard around fwd().
+  // the neighbouring chunks instead of adding to it (chunk_bounds() sizes the
+  // chunks so it does). Other meshes copy the whole shard around fwd().
   void fwd_host(const void* q, const void* k, const void* v, void* o, float* lse, cudaStream_t st) {
     USPB_CHECK(cudaSetDevice(cfg_.device));
     for (const void* ptr : {q, k, v, static_cast<const void*>(o), static_cast<const void*>(lse)})
@@ -389,12 +390,13 @@ class Engine {
       hlse_ = DevBuf(lb);
       USPB_CHECK(cudaStreamCreateWithFlags(&h2d_stream_, cudaStreamNonBlocking));
       USPB_CHECK(cudaStreamCreateWithFlags(&d2h_stream_, cudaStreamNonBlocking));
-      USPB_CHECK(cudaEventCreateWithFlags(&ev_entry_, cudaEventDisableTiming));
-      USPB_CHECK(cudaEventCreateWithFlags(&ev_drained_, cudaEventDisableTiming));
+      const unsigned fl = std::getenv("USP_HOST_TRACE") ? cudaEventDefault : cudaEventDisableTiming;
+      USPB_CHECK(cudaEventCreateWithFlags(&ev_entry_, fl));
+      USPB_CHECK(cudaEventCreateWithFlags(&ev_drained_, fl));
     }
     const bool reshape = U_ > 1 || hs_ != hsk_;
-    const int64_t C = host_chunk_rows();
-    if (U_ > 1 || R_ > 1 || B_ > 1 || reshape || C >= Tr_) {
+    const std::vector<int64_t> bounds = chunk_bounds();
+    if (U_ > 1 || R_ > 1 || B_ > 1 || reshape || bounds.size() <= 2) {
       USPB_CHECK(cudaMemcpyAsync(hq_.p, q, qb, cudaMemcpyHostToDevice, st));
       USPB_CHECK(cudaMemcpyAsync(hk_.p, k, kvb, cudaMemcpyHostToDevice, st));
       USPB_CHECK(cudaMemcpyAsync(hv_.p, v, kvb, cudaMemcpyHostToDevice, st));
@@ -403,7 +405,7 @@ class Engine {
       USPB_CHECK(cudaMemcpyAsync(lse, hlse_.p, lb, cudaMemcpyDeviceToHost, st));
       return;
     }
-    ensure_chunk_plans(C);
+    ensure_chunk_plans(bounds);
     launches_ = 0;
     ledger_.clear();
     for (int tsr = 0; tsr < 4; ++tsr) record_a2a(tsr, tsr == 0 || tsr == 3 ? q_part_ : kv_part_);
@@ -422,7 +424,7 @@ class Engine {
       up(hv_, v, 0, Tr_, kvrow);
     }
     for (int c = 0; c < n; ++c) {
-      const int64_t r0 = c * C, r1 = std::min<int64_t>(Tr_, r0 + C);
+      const int64_t r0 = bounds[c], r1 = bounds[c + 1];
       if (shape_.causal) {
         up(hk_, k, r0, r1, kvrow);
         up(hv_, v, r0, r1, kvrow);
@@ -445,45 +447,92 @@ class Engine {
     USPB_CHECK(cudaStreamWaitEvent(st, ev_drained_, 0));
     have_fwd_ = true;
     fwd_ledger_size_ = ledger_.size();
+    static const bool trace = std::getenv("USP_HOST_TRACE") != nullptr;  // development timeline
+    if (trace) {
+      USPB_CHECK(cudaStreamSynchronize(st));
+      auto at = [&](cudaEvent_t e) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev_entry_, e);
+        return ms;
+      };
+      for (int c = 0; c < n; ++c)
+        std::fprintf(stderr, "chunk %2d rows [%7lld,%7lld): inputs ready %8.3f ms, attention done %8.3f ms\n", c,
+                     static_cast<long long>(bounds[c]), static_cast<long long>(bounds[c + 1]), at(ev_chunk_in_[c]),
+                     at(ev_chunk_out_[c]));
+      std::fprintf(stderr, "drained %8.3f ms\n", at(ev_drained_));
+    }
   }
 
-  // Rows per pipelined chunk: 8 chunks (USP_HOST_CHUNKS overrides), whole
-  // 128-row tiles, at least 4096 rows.
-  int64_t host_chunk_rows() const {
-    static const int want = [] {
+  // Chunk boundaries (whole 128-row tiles). Causal: row p's attention grows
+  // with p but its upload does not, so early chunks are compute-light and the
+  // pipeline would wait on PCIe. The chunks therefore grow with the work that
+  // hides them: each next chunk is as large as the previous chunk's attention
+  // can cover at ~50 GB/s H2D and ~1.2 PFLOP/s (clamped to [1K rows, L/8]),
+  // and the last 8K rows form their own chunk so the final, exposed O
+  // download is short (measured timeline: tools/host_trace.py). Non-causal:
+  // 8 equal chunks. USP_HOST_CHUNKS=n forces n equal chunks; sequences of
+  // 8K rows or fewer are a single chunk (plain copies around fwd()).
+  std::vector<int64_t> chunk_bounds() const {
+    static const int forced = [] {
       const char* e = std::getenv("USP_HOST_CHUNKS");
-      return e ? std::max(1, std::atoi(e)) : 8;
+      return e ? std::max(1, std::atoi(e)) : 0;
     }();
-    int64_t c = (Tr_ + want - 1) / want;
-    c = (c + kTileM - 1) / kTileM * kTileM;
-    return std::max<int64_t>(c, 4096);
+    auto tiles = [](int64_t r) { return (r + kTileM - 1) / kTileM * kTileM; };
+    std::vector<int64_t> b{0};
+    if (Tr_ <= 8192) {
+      b.push_back(Tr_);
+      return b;
+    }
+    if (forced || !shape_.causal) {
+      const int n = forced ? forced : 8;
+      const int64_t c = std::max<int64_t>(tiles((Tr_ + n - 1) / n), 4096);
+      for (int64_t r = c; r < Tr_; r += c) b.push_back(r);
+      b.push_back(Tr_);
+      return b;
+    }
+    const double up_s_per_row = double((H_ + 2 * KV_) * hs_ * 2) / 50e9;
+    const double att_s_per_pair = 4.0 * hl_ * hs_ / 1.2e15;
+    const int64_t big = std::max<int64_t>(tiles(Tr_ / 8), 1024);
+    const int64_t tail = Tr_ > 4 * 8192 ? 8192 : 0;
+    int64_t prev = 0, r = 1024;
+    while (r < Tr_ - tail) {
+      b.push_back(r);
+      const double covered = att_s_per_pair * 0.5 * (double(r) * r - double(prev) * prev);
+      const int64_t next = std::clamp<int64_t>(tiles(int64_t(covered / up_s_per_row)) / kTileM * kTileM, 1024, big);
+      prev = r;
+      r += next;
+    }
+    if (tail && b.back() != Tr_ - tail) b.push_back(Tr_ - tail);
+    b.push_back(Tr_);
+    return b;
   }
 
-  void ensure_chunk_plans(int64_t C) {
-    if (!chunk_steps_.empty() && chunk_rows_ == C) return;
+  void ensure_chunk_plans(const std::vector<int64_t>& bounds) {
+    if (!chunk_steps_.empty() && chunk_bounds_ == bounds) return;
     chunk_steps_.clear();
     for (auto e : ev_chunk_in_) cudaEventDestroy(e);
     for (auto e : ev_chunk_out_) cudaEventDestroy(e);
     ev_chunk_in_.clear();
     ev_chunk_out_.clear();
-    chunk_rows_ = C;
+    chunk_bounds_ = bounds;
     const auto pos = head_positions(shape_, cfg_.rank);
     for (size_t i = 0; i < pos.size(); ++i)
       if (pos[i] != int64_t(i)) throw Error(ErrorCode::kInternal, "chunked forward needs identity positions");
     const int group = hl_ / kvl_;
-    for (int64_t r0 = 0; r0 < Tr_; r0 += C) {
-      const int64_t r1 = std::min<int64_t>(Tr_, r0 + C);
+    for (size_t c = 0; c + 1 < bounds.size(); ++c) {
+      const int64_t r0 = bounds[c], r1 = bounds[c + 1];
       const std::vector<int64_t> qp(pos.begin() + r0, pos.begin() + r1);
       const std::vector<int64_t> kp(pos.begin(), pos.begin() + (shape_.causal ? r1 : Tr_));
       DevStep d;
       upload_plan(d, plan_step(qp, kp, shape_.causal, B_, hl_ / nq_, true, std::max(1, group / nq_)));
       d.mode = EpiMode::kSingle;
       chunk_steps_.push_back(std::move(d));
-      cudaEvent_t a, b;
-      USPB_CHECK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
-      USPB_CHECK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+      cudaEvent_t a, e;
+      const unsigned fl = std::getenv("USP_HOST_TRACE") ? cudaEventDefault : cudaEventDisableTiming;
+      USPB_CHECK(cudaEventCreateWithFlags(&a, fl));
+      USPB_CHECK(cudaEventCreateWithFlags(&e, fl));
       ev_chunk_in_.push_back(a);
-      ev_chunk_out_.push_back(b);
+      ev_chunk_out_.push_back(e);
     }
   }
 
@@ -959,7 +1008,7 @@ class Engine {
   // usp_attn_fwd_host staging and its chunk pipeline
   DevBuf hq_, hk_, hv_, ho_, hlse_;
   std::vector<DevStep> chunk_steps_;
-  int64_t chunk_rows_ = 0;
+  std::vector<int64_t> chunk_bounds_;
   cudaStream_t h2d_stream_ = nullptr, d2h_stream_ = nullptr;
   cudaEvent_t ev_entry_ = nullptr, ev_drained_ = nullptr;
   std::vector<cudaEvent_t> ev_chunk_in_, ev_chunk_out_;
