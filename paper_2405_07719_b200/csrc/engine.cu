@@ -155,7 +155,8 @@ class Engine {
     hs_ = shape_.head_size;
     hsk_ = shape_.kernel_head_size();
     const int group = hl_ / kvl_;
-    nq_ = (group % 2 == 0) ? 2 : 1;
+    tiling_ = fwd_tiling(hl_, kvl_);
+    nq_ = (tiling_.pair_rows || group % 2 == 0) ? 2 : 1;
 
     USPB_CHECK(cudaSetDevice(c.device));
     USPB_CHECK(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, c.device));
@@ -208,8 +209,8 @@ class Engine {
       st.mode = R_ == 1 ? EpiMode::kSingle
                         : (t == 0 ? EpiMode::kFirst : (t == R_ - 1 ? EpiMode::kLast : EpiMode::kMiddle));
       const bool include_empty = st.mode != EpiMode::kMiddle;
-      st.host = plan_step(my_pos, k_pos, shape_.causal, B_, hl_ / nq_, include_empty,
-                          std::max(1, group / nq_));
+      st.host = plan_step(my_pos, k_pos, shape_.causal, B_, tiling_.head_units, include_empty,
+                          tiling_.units_per_kv, tiling_.rows_per_unit);
       st.q_pos = upload(st.host.q_pos);
       st.k_pos = upload(st.host.k_pos);
       st.tile_off = upload(st.host.tile_off);
@@ -518,13 +519,13 @@ class Engine {
     const auto pos = head_positions(shape_, cfg_.rank);
     for (size_t i = 0; i < pos.size(); ++i)
       if (pos[i] != int64_t(i)) throw Error(ErrorCode::kInternal, "chunked forward needs identity positions");
-    const int group = hl_ / kvl_;
     for (size_t c = 0; c + 1 < bounds.size(); ++c) {
       const int64_t r0 = bounds[c], r1 = bounds[c + 1];
       const std::vector<int64_t> qp(pos.begin() + r0, pos.begin() + r1);
       const std::vector<int64_t> kp(pos.begin(), pos.begin() + (shape_.causal ? r1 : Tr_));
       DevStep d;
-      upload_plan(d, plan_step(qp, kp, shape_.causal, B_, hl_ / nq_, true, std::max(1, group / nq_)));
+      upload_plan(d, plan_step(qp, kp, shape_.causal, B_, tiling_.head_units, true, tiling_.units_per_kv,
+                               tiling_.rows_per_unit));
       d.mode = EpiMode::kSingle;
       chunk_steps_.push_back(std::move(d));
       cudaEvent_t a, e;
@@ -923,6 +924,7 @@ class Engine {
     p.heads = hl_;
     p.kv_heads = kvl_;
     p.mode = static_cast<int>(s.mode);
+    p.pair_rows = tiling_.pair_rows ? 1 : 0;
     p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(double(hs_)));
     static const int kv_hint = [] {
       const char* e = std::getenv("USP_KV_HINT");
@@ -996,6 +998,7 @@ class Engine {
   std::shared_ptr<Groups> groups_;
   UspShape shape_;
   int U_ = 1, R_ = 1, u_ = 0, r_ = 0, H_ = 0, KV_ = 0, hl_ = 0, kvl_ = 0, hs_ = 0, hsk_ = 0, nq_ = 1;
+  FwdTiling tiling_{};
   int64_t B_ = 1, T_ = 0, Tr_ = 0;
   int num_sms_ = 148;
   size_t q_part_ = 0, kv_part_ = 0, kv_bytes_ = 0;
@@ -1136,11 +1139,12 @@ usp_status usp_schedule(const usp_config* cfg, int32_t step, usp_step_info* out)
     const int u = s.mesh.ulysses_coord(cfg->rank), r = s.mesh.ring_coord(cfg->rank);
     const int R = s.mesh.ring;
     const int src = ring_source(r, step, R);
-    const int hl = s.local_heads(), kvl = s.local_kv_heads();
-    const int nq = ((hl / kvl) % 2 == 0) ? 2 : 1;
+    const int kvl = s.local_kv_heads();
+    const FwdTiling tl = fwd_tiling(s.local_heads(), kvl);
     const auto st = plan_step(head_positions(s, cfg->rank),
                               head_positions(s, s.mesh.rank_of(u, src)), s.causal, s.batch,
-                              hl / nq, R == 1 || step == 0 || step == R - 1);
+                              tl.head_units, R == 1 || step == 0 || step == R - 1, tl.units_per_kv,
+                              tl.rows_per_unit);
     out->step = step;
     out->src_ring_coord = src;
     out->send_to_rank = s.mesh.rank_of(u, (r + 1) % R);

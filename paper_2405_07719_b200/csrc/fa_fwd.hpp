@@ -38,7 +38,8 @@ struct FwdParams {
   float* o_acc;       // fp32 running O (batch, q_len, heads, hs) [kFirst..kLast]
   float* lse_acc;     // fp32 running LSE, log2 domain           [kFirst..kLast]
 
-  const uint32_t* units;     // packed work units: q_tile | hp << 16 | b << 24
+  const uint32_t* units;     // packed work units: q_tile | hp << 16 | b << 24 (pair_rows:
+                             // tile pair | head << 16 | b << 24)
   const int32_t* tile_off;   // CSR row offsets per q tile (n_q_tiles + 1)
   const int32_t* tile_list;  // k tile index | partial << 31
   const int32_t* q_pos;      // effective query positions, padded to 128
@@ -48,6 +49,8 @@ struct FwdParams {
   int num_units;
   int batch, q_len, k_len, heads, kv_heads;
   int mode;          // EpiMode
+  int pair_rows;     // 1: a unit is two adjacent 128-row tiles of one head
+                     //    (q_tile field = tile pair); 0: two heads of a pair
   float scale_log2;  // log2(e) / sqrt(head_size)
   int kv_hint;       // L2 policy for K/V tile loads: 0 normal, 1 evict_last
   // Development tracing (nullptr in production): clock64 stamps of CTA 0's

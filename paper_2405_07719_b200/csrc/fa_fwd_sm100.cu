@@ -242,10 +242,10 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
       if (u >= p.num_units) break;
       const uint32_t unit = p.units[u];
       const int qt = unit & 0xFFFF, hp = (unit >> 16) & 0xFF, b = unit >> 24;
-      const int h = hp * NQ + t;
+      const int h = p.pair_rows ? hp : hp * NQ + t;
       const int beg = p.tile_off[qt];
       const int n = p.tile_off[qt + 1] - beg;
-      const int q_row = qt * kTileM + row_in_tile;
+      const int q_row = (p.pair_rows ? qt * NQ + t : qt) * kTileM + row_in_tile;
       const int qpos = p.q_pos[q_row];
       float m_run = -INFINITY, l_run = 0.f, m_use = 0.f;
       for (int j = 0; j < n; ++j) {
@@ -482,12 +482,13 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
         ++q_it;
         for (int t = 0; t < NQ; ++t) {
           mbar_arrive_expect_tx(&q_full[t], C::kQBytes);
+          const int qh = p.pair_rows ? hp : hp * NQ + t;
+          const int qr = (p.pair_rows ? qt * NQ + t : qt) * kTileM;
 #pragma unroll
           for (int sb = 0; sb < C::kSub; ++sb)
-            tma_load_4d(sQ + t * C::kQBytes + sb * C::kSubBytes, &p.tm_q, &q_full[t], sb * 64,
-                        hp * NQ + t, qt * kTileM, b);
+            tma_load_4d(sQ + t * C::kQBytes + sb * C::kSubBytes, &p.tm_q, &q_full[t], sb * 64, qh, qr, b);
         }
-        const int kvh = (hp * NQ) / group;
+        const int kvh = (p.pair_rows ? hp : hp * NQ) / group;
         for (int j = 0; j < n; ++j) {
           const int kt = p.tile_list[beg + j] & 0x7FFFFFFF;
 #pragma unroll

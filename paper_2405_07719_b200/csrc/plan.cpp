@@ -225,10 +225,22 @@ int64_t visible_pairs(const std::vector<int64_t>& q_pos, const std::vector<int64
   return pairs;
 }
 
+FwdTiling fwd_tiling(int hl, int kvl) {
+  static const bool rows_ok = [] {
+    const char* e = std::getenv("USP_FA_PAIR_ROWS");
+    return !e || std::atoi(e) != 0;
+  }();
+  const int group = hl / kvl;
+  if (group % 2 == 0) return {false, hl / 2, group / 2, kTileM};
+  if (rows_ok) return {true, hl, group, 2 * kTileM};
+  return {false, hl, group, kTileM};  // one q tile per CTA (development fallback)
+}
+
 StepPlan plan_step(const std::vector<int64_t>& q_pos, const std::vector<int64_t>& k_pos,
                    bool causal, int64_t batch, int head_pairs, bool include_empty,
-                   int pairs_per_kv) {
+                   int pairs_per_kv, int rows_per_unit) {
   StepPlan p;
+  const int kTileM = rows_per_unit;  // query rows per unit (shadows the 128-row tile)
   p.q_len = static_cast<int>(q_pos.size());
   p.k_len = static_cast<int>(k_pos.size());
   p.n_q_tiles = (p.q_len + kTileM - 1) / kTileM;

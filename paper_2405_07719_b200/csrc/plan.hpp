@@ -89,9 +89,24 @@ struct StepPlan {
 // pairs_per_kv = head pairs sharing one kv head (GQA group / NQ); the unit
 // order keeps CTAs that run concurrently on the same kv head (L2 reuse of
 // the streamed K/V tiles) — see plan.cpp.
+// rows_per_unit: query rows per work unit (128, or 256 when the kernel runs
+// two adjacent 128-row tiles of one head; the tile list is then the union of
+// both tiles' visible key tiles, classified over all 256 rows).
 StepPlan plan_step(const std::vector<int64_t>& q_pos, const std::vector<int64_t>& k_pos,
                    bool causal, int64_t batch, int head_pairs, bool include_empty,
-                   int pairs_per_kv = 1);
+                   int pairs_per_kv = 1, int rows_per_unit = 128);
+
+// How the forward kernel fills its two q tiles per CTA: two q heads of one
+// GQA group over the same rows when the local group is even (K/V tiles and
+// masks shared), otherwise two adjacent 128-row tiles of ONE head (MHA and
+// odd groups; K/V tiles shared, key-tile list = union, per-element masks).
+struct FwdTiling {
+  bool pair_rows;    // two row tiles of one head (else two heads)
+  int head_units;    // head slots per unit list entry (head pairs or heads)
+  int units_per_kv;  // head slots sharing one kv head
+  int rows_per_unit; // 128 or 256
+};
+FwdTiling fwd_tiling(int local_heads, int local_kv_heads);
 
 // The same block transposed for the dK/dV kernel: CSR over KEY tiles
 // (tile_list = q tile | partial << 31, same partial flags), units
