@@ -791,20 +791,18 @@ __global__ void cast_rows_kernel(const float* src, const float* src2, uint16_t* 
   }
 }
 
-template <class K>
-cudaError_t set_smem(K kern, int bytes) {
-  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-}
 
 }  // namespace
 
 cudaError_t launch_bwd_dq(const BwdParams& p, int hs, int grid, cudaStream_t stream) {
   if (hs == 128) {
-    static cudaError_t once = set_smem(fa_bwd_dq_kernel<128>, BwdCfg<128>::kDqSmemBytes);
+    static std::atomic<uint64_t> done{0};
+    const cudaError_t once = ensure_smem_attr(fa_bwd_dq_kernel<128>, BwdCfg<128>::kDqSmemBytes, done);
     if (once != cudaSuccess) return once;
     fa_bwd_dq_kernel<128><<<grid, BwdCfg<128>::kThreads, BwdCfg<128>::kDqSmemBytes, stream>>>(p);
   } else if (hs == 64) {
-    static cudaError_t once = set_smem(fa_bwd_dq_kernel<64>, BwdCfg<64>::kDqSmemBytes);
+    static std::atomic<uint64_t> done{0};
+    const cudaError_t once = ensure_smem_attr(fa_bwd_dq_kernel<64>, BwdCfg<64>::kDqSmemBytes, done);
     if (once != cudaSuccess) return once;
     fa_bwd_dq_kernel<64><<<grid, BwdCfg<64>::kThreads, BwdCfg<64>::kDqSmemBytes, stream>>>(p);
   } else {
@@ -815,11 +813,13 @@ cudaError_t launch_bwd_dq(const BwdParams& p, int hs, int grid, cudaStream_t str
 
 cudaError_t launch_bwd_dkdv(const BwdParams& p, int hs, int grid, cudaStream_t stream) {
   if (hs == 128) {
-    static cudaError_t once = set_smem(fa_bwd_dkdv_kernel<128>, BwdCfg<128>::kSmemBytes);
+    static std::atomic<uint64_t> done{0};
+    const cudaError_t once = ensure_smem_attr(fa_bwd_dkdv_kernel<128>, BwdCfg<128>::kSmemBytes, done);
     if (once != cudaSuccess) return once;
     fa_bwd_dkdv_kernel<128><<<grid, BwdCfg<128>::kThreads, BwdCfg<128>::kSmemBytes, stream>>>(p);
   } else if (hs == 64) {
-    static cudaError_t once = set_smem(fa_bwd_dkdv_kernel<64>, BwdCfg<64>::kSmemBytes);
+    static std::atomic<uint64_t> done{0};
+    const cudaError_t once = ensure_smem_attr(fa_bwd_dkdv_kernel<64>, BwdCfg<64>::kSmemBytes, done);
     if (once != cudaSuccess) return once;
     fa_bwd_dkdv_kernel<64><<<grid, BwdCfg<64>::kThreads, BwdCfg<64>::kSmemBytes, stream>>>(p);
   } else {

@@ -12,6 +12,9 @@
 #pragma once
 
 #include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
 #include <cstdint>
 
 namespace uspb200 {
@@ -58,5 +61,19 @@ struct FwdParams {
   unsigned long long* trace;
   int debug_flags;  // development: bit 0 = skip the softmax math (pipeline-only timing)
 };
+
+// cudaFuncSetAttribute is per device: opt a kernel in to its dynamic shared
+// memory once on every device it is launched on (`done`: one bit per device).
+template <class K>
+inline cudaError_t ensure_smem_attr(K kern, int bytes, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = uint64_t(1) << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_release);
+  return e;
+}
 
 }  // namespace uspb200

@@ -640,13 +640,9 @@ template <int NQ, int HS, int POLY, int SPL>
 static cudaError_t launch_impl(const FwdParams& p, int grid, cudaStream_t stream) {
   using C = FwdCfg<NQ, HS, POLY, SPL>;
   auto kern = fa_fwd_sm100_kernel<NQ, HS, POLY, SPL>;
-  static bool attr_set = false;  // per instantiation; set before first launch
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};  // per instantiation and device
+  const cudaError_t e = ensure_smem_attr(kern, C::kSmemBytes, attr_done);
+  if (e != cudaSuccess) return e;
   kern<<<grid, C::kThreads, C::kSmemBytes, stream>>>(p);
   return cudaGetLastError();
 }
