@@ -22,6 +22,7 @@
 #ifndef USP_ATTN_H
 #define USP_ATTN_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #if defined(__GNUC__)
@@ -131,6 +132,17 @@ USP_API usp_status usp_comm_create_nccl(const uint8_t unique_id[128], int32_t wo
  * the ranks' buffers (the analogue of simcomm::World::run, world.hpp:217-236).
  * One handle is shared by all ranks of the world; ranks may share a device. */
 USP_API usp_status usp_comm_create_local(int32_t world_size, usp_comm** out);
+/* Peer-memory transport, one process per GPU, no NCCL: receive buffers are
+ * exported with CUDA IPC and written directly by the senders (copy engines
+ * over NVLink / NVSwitch, so no SMs are taken from the attention kernel);
+ * cross-process ordering by GPU stream memory operations on IPC-shared
+ * signals. `allgather` is a host all-gather over the world (called
+ * collectively at create and when a new buffer is first exchanged):
+ * recv[world_size * bytes] <- every rank's send[bytes], rank order; it must
+ * stay callable for the comm's lifetime. Returns 0 on success. */
+typedef int (*usp_allgather_fn)(const void* send, void* recv, size_t bytes, void* ctx);
+USP_API usp_status usp_comm_create_p2p(int32_t world_size, int32_t rank, int32_t device,
+                                       usp_allgather_fn allgather, void* ctx, usp_comm** out);
 USP_API void usp_comm_destroy(usp_comm* comm);
 
 /* ---- engine -------------------------------------------------------------- */

@@ -80,7 +80,7 @@ EXPORTS = [
     "usp_comm_create_nccl", "usp_comm_create_local", "usp_comm_destroy", "usp_engine_create",
     "usp_attn_fwd", "usp_engine_last_launches", "usp_engine_destroy", "usp_engine_enable_timing",
     "usp_engine_kernel_times", "usp_local_world_fwd", "usp_attn_bwd", "usp_local_world_bwd",
-    "usp_backward_ledger", "usp_attn_fwd_host",
+    "usp_backward_ledger", "usp_attn_fwd_host", "usp_comm_create_p2p",
     "usp_last_error", "usp_version",
 ]
 # Every symbol include/usp_sim.h declares (the reference's uspsim.h ABI).
@@ -88,6 +88,9 @@ SIM_EXPORTS = [
     "uspsim_run", "uspsim_report_json", "uspsim_report_text", "uspsim_report_ledger_csv",
     "uspsim_report_exit_code", "uspsim_report_free", "uspsim_last_error", "uspsim_version",
 ]
+
+# int (*)(const void* send, void* recv, size_t bytes, void* ctx)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
 
 _lib = None
 _lock = threading.Lock()
@@ -115,6 +118,7 @@ def _declare(lib):
         "usp_nccl_unique_id": (st, [ctypes.c_char_p]),
         "usp_comm_create_nccl": (st, [ctypes.c_char_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P(vp)]),
         "usp_comm_create_local": (st, [ctypes.c_int32, P(vp)]),
+        "usp_comm_create_p2p": (st, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ALLGATHER_FN, vp, P(vp)]),
         "usp_comm_destroy": (None, [vp]),
         "usp_engine_create": (st, [P(UspConfig), vp, P(vp)]),
         "usp_attn_fwd": (st, [vp, vp, vp, vp, vp, vp, vp]),

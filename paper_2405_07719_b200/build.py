@@ -19,7 +19,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libusp_b200.so")
 OBJ = os.path.join(HERE, "build")
 SOURCES = ["fa_fwd_sm100.cu", "fa_bwd_sm100.cu", "reshard.cu", "engine.cu", "plan.cpp", "transport.cpp",
-           "simulate.cu", "check_fp64.cu"]
+           "simulate.cu", "check_fp64.cu", "transport_p2p.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -1248,6 +1248,17 @@ usp_status usp_comm_create_local(int32_t world_size, usp_comm** out) {
   });
 }
 
+usp_status usp_comm_create_p2p(int32_t world_size, int32_t rank, int32_t device, usp_allgather_fn allgather,
+                               void* ctx, usp_comm** out) {
+  if (!out) return USP_INVALID_INPUT;
+  *out = nullptr;
+  return guarded([&] {
+    auto c = std::make_unique<usp_comm>();
+    c->impl = make_p2p_transport(world_size, rank, device, allgather, ctx);
+    *out = c.release();
+  });
+}
+
 void usp_comm_destroy(usp_comm* comm) { delete comm; }
 
 usp_status usp_engine_create(const usp_config* cfg, usp_comm* comm, usp_engine** out) {

@@ -52,6 +52,12 @@ class Transport {
 };
 
 std::unique_ptr<Transport> make_local_transport(int world_size);
+// Host all-gather used to bootstrap the peer-memory transport: every rank
+// contributes `bytes` at `send`; `recv` receives world_size * bytes in rank
+// order. Returns 0 on success.
+using AllGatherFn = int (*)(const void* send, void* recv, size_t bytes, void* ctx);
+std::unique_ptr<Transport> make_p2p_transport(int world_size, int rank, int device, AllGatherFn allgather,
+                                              void* ctx);
 std::unique_ptr<Transport> make_nccl_transport(const unsigned char unique_id[128],
                                                int world_size, int rank, int device);
 void nccl_unique_id(unsigned char out[128]);

@@ -225,6 +225,50 @@ class Comm:
         dist.broadcast(t, src=0, group=group)
         return cls.nccl(bytes(t.cpu().tolist()), world, rank, device)
 
+    @classmethod
+    def p2p(cls, world_size: int, rank: int, device: int, allgather) -> "Comm":
+        """Peer-memory transport (usp_comm_create_p2p): CUDA IPC buffers written
+        directly by the senders with copy engines, no NCCL. ``allgather(bytes)
+        -> list[bytes]`` is a host all-gather over the world in rank order; it
+        is called collectively at creation and when a buffer is first used."""
+        from ._lib import ALLGATHER_FN
+
+        def _cb(send, recv, nbytes, _ctx):
+            try:
+                parts = allgather(ctypes.string_at(send, nbytes))
+                if len(parts) != world_size or any(len(x) != nbytes for x in parts):
+                    return 1
+                ctypes.memmove(recv, b"".join(parts), nbytes * world_size)
+                return 0
+            except Exception:  # pragma: no cover - reported as a failed collective
+                return 1
+
+        cb = ALLGATHER_FN(_cb)
+        h = ctypes.c_void_p()
+        check(lib().usp_comm_create_p2p(world_size, rank, device, cb, None, ctypes.byref(h)))
+        c = cls(h.value, "p2p", world_size)
+        c._keep = cb  # the library calls it for the comm's whole lifetime
+        return c
+
+    @classmethod
+    def p2p_from_torch_distributed(cls, device: int, group=None) -> "Comm":
+        """The peer-memory transport bootstrapped over a torch.distributed
+        group (a gloo group is created for the host all-gather when the
+        given one is not CPU-capable)."""
+        import torch
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        host_group = group if dist.get_backend(group) == "gloo" else dist.new_group(backend="gloo")
+
+        def allgather(blob: bytes):
+            t = torch.frombuffer(bytearray(blob), dtype=torch.uint8)
+            out = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(out, t, group=host_group)
+            return [bytes(x.numpy().tobytes()) for x in out]
+
+        return cls.p2p(world, rank, device, allgather)
+
     def close(self) -> None:
         if self._h:
             lib().usp_comm_destroy(self._h)

@@ -1,0 +1,91 @@
+"""The peer-memory transport (usp_comm_create_p2p) across PROCESSES.
+
+One process per rank, as on a multi-GPU node, but all on cuda:0 (this build
+has one GPU): CUDA IPC works between processes on one device, so the whole
+multi-process path runs for real — handle exchange over a gloo host
+all-gather, receive buffers written by the other processes with copy
+engines, cross-process ordering by stream memory operations — for the
+forward and the backward on U x R meshes. Each rank checks its own shard
+against the CPU oracle (forward) and all ranks' gradients are checked on
+rank 0 (backward)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, U, R, port, L, hc, kv, hs, causal, errq):
+    try:
+        import torch.distributed as dist
+
+        from oracle.oracle import Oracle, oracle_reference_attention_grad
+        from paper_2405_07719_b200 import Comm, ProcessMesh, UspAttention, UspForward
+        from tests.usp_harness import UspCase, errors, make_globals_with_dout, to_bf16, widen
+
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        dev = torch.device("cuda", 0)
+        torch.cuda.set_device(dev)
+        comm = Comm.p2p_from_torch_distributed(0)
+        eng = UspAttention(ProcessMesh(U, R), rank=rank, seq_len=L, heads=hc, kv_heads=kv, head_size=hs,
+                           causal=causal, device=0, comm=comm)
+        c = UspCase(seq=L, hc=hc, kv_hc=kv, hs=hs, ulysses=U, ring=R, causal=causal, seed=11)
+        q, k, v, do = make_globals_with_dout(c)
+        tq, tk, tv, tdo = (to_bf16(x, dev) for x in (q, k, v, do))
+        pos = torch.tensor(eng.positions(), dtype=torch.long, device=dev)
+        qs, ks, vs, dos = (t[:, pos].contiguous() for t in (tq, tk, tv, tdo))
+        for _ in range(2):  # the second call reuses the registered buffers and bumps the epochs
+            fwd = eng.forward(qs, ks, vs)
+            grads = eng.backward(fwd, dos)
+        torch.cuda.synchronize()
+        qd, kd, vd, dod = widen(tq), widen(tk), widen(tv), widen(tdo)
+        ref = Oracle.reference_attention(qd, kd, vd, causal)
+        p = pos.cpu().numpy()
+        eo = errors(widen(fwd.out), ref[:, p])
+        assert eo["max_abs"] <= 1e-2 and eo["rel_l2"] <= 1e-2, (rank, eo)
+        # gradients: gather every shard on all ranks, compare with the oracle
+        gq, gk, gv = oracle_reference_attention_grad(qd, kd, vd, dod, causal)
+        for got, want in ((grads.dq, gq), (grads.dk, gk), (grads.dv, gv)):
+            e = errors(widen(got), want[:, p])
+            assert e["rel_l2"] <= 2e-2, (rank, e)
+        assert eng.last_launches() >= 1
+        eng.close()
+        dist.barrier()
+        comm.close()
+        dist.destroy_process_group()
+    except BaseException as e:  # noqa: BLE001
+        errq.put(f"rank {rank}: {e!r}")
+        raise
+
+
+@pytest.mark.parametrize("U,R", [(2, 2), (1, 4), (4, 1)])
+def test_p2p_transport_multi_process(cuda, U, R):
+    ctx = mp.get_context("spawn")
+    errq = ctx.Queue()
+    world = U * R
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, U, R, port, 512, 8, 4 if U <= 4 else 8, 128, True, errq))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    alive = [p for p in procs if p.is_alive()]
+    for p in alive:
+        p.kill()
+    errs = []
+    while not errq.empty():
+        errs.append(errq.get())
+    assert not alive, "p2p ranks hung"
+    assert not errs and all(p.exitcode == 0 for p in procs), errs
