@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--head-size", type=int, default=128)
     ap.add_argument("--ulysses", type=int, default=1, help="Ulysses degree U (R = N / U)")
     ap.add_argument("--non-causal", action="store_true")
+    ap.add_argument("--transport", choices=["nccl", "p2p"], default="nccl",
+                    help="N>1 exchange: NCCL all-to-all + send/recv (north star), or the peer-memory "
+                         "transport (CUDA IPC + copy engines, no SMs reserved)")
     ap.add_argument("--cpu-sample-len", type=int, default=4096)
     ap.add_argument("--skip-cpu-baseline", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
@@ -70,6 +73,7 @@ def peaks():
 
 def workload_config(a, n, U, R):
     return {
+        **({"transport": a.transport} if n > 1 else {}),
         "workload": f"usp_attn_fwd llama3-8b layer L={a.seq_len} {'causal zigzag' if not a.non_causal else 'full'}",
         "seq_len": a.seq_len, "batch": 1, "heads": a.heads, "kv_heads": a.kv_heads, "head_size": a.head_size,
         "causal": not a.non_causal, "ulysses": U, "ring": R, "parallelism": f"u{U}r{R}",
@@ -226,17 +230,31 @@ def run_ours(a):
     n = a.gpus
     if world != n:
         raise SystemExit(f"--gpus {n} but WORLD_SIZE={world}")
+    # Development only: USP_BENCH_SAME_DEVICE=1 puts every rank on cuda:0
+    # (gloo for the host plumbing, the p2p transport for the data) so the
+    # multi-process path of this script can be exercised on a one-GPU box;
+    # its numbers measure N processes sharing one GPU, not scaling.
+    same_dev = os.environ.get("USP_BENCH_SAME_DEVICE") == "1"
+    if same_dev:
+        local = 0
+        a.transport = "p2p"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     distributed = world > 1
     if distributed:
-        dist.init_process_group("nccl", device_id=dev)
+        if same_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     U = a.ulysses
     if n % U:
         raise SystemExit("ulysses degree must divide the GPU count")
     R = n // U
     mesh = ProcessMesh(U, R)
-    comm = Comm.from_torch_distributed(local) if distributed else None
+    comm = None
+    if distributed:
+        comm = (Comm.p2p_from_torch_distributed(local) if a.transport == "p2p"
+                else Comm.from_torch_distributed(local))
     causal = not a.non_causal
     eng = UspAttention(mesh, rank=rank, seq_len=a.seq_len, heads=a.heads, kv_heads=a.kv_heads,
                        head_size=a.head_size, causal=causal, device=local, comm=comm)
@@ -254,7 +272,7 @@ def run_ours(a):
     def max_over_ranks(x: float) -> float:
         if not distributed:
             return x
-        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        t = torch.tensor([x], device="cpu" if same_dev else dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
