@@ -27,7 +27,8 @@
  *     event keeps the reference's (group, step) numbering and bytes as moved
  *     (bf16, fp32 for the circulating dK/dV partials);
  *   * optional param "device" (CUDA ordinal, default 0) hosts all ranks;
- *   * "cost", "plan" and "balance" (analytic, host-only, outside the
+ *   * "balance" is served (host arithmetic over the zigzag layout);
+ *     "cost" and "plan" (analytic, host-only, outside the
  *     accelerated path) return an invalid-input report naming the
  *     reference library.
  */

@@ -558,6 +558,62 @@ Report cmd_simulate(const Value& params) {
   return r;
 }
 
+// cmd_balance (commands.cpp:414-462): the zigzag vs contiguous causal load of
+// each ring rank — host arithmetic over the layout the engine itself uses
+// (plan.cpp zigzag_partition / even_partition / causal_pair_counts).
+Report cmd_balance(const Value& params) {
+  const int64_t seq_len = params.value("seqlen", int64_t(16));
+  const int ring = params.value("ring", 4);
+  const auto zz = zigzag_partition(seq_len, ring);
+  const auto ev = even_partition(seq_len, ring);
+  const auto zc = causal_pair_counts(zz, ring, seq_len);
+  const auto ec = causal_pair_counts(ev, ring, seq_len);
+  const int64_t per = ring > 0 ? seq_len / ring : 0;
+  auto arr = [](const std::vector<int64_t>& v, size_t b, size_t e) {
+    Value a = Value::array();
+    for (size_t i = b; i < e; ++i) a.push_back(v[i]);
+    return a;
+  };
+  const double skew = double(ec.back()) / double(ec.front());
+  Report r;
+  r.doc = envelope("balance", params);
+  Value results = Value::object();
+  results["seqlen"] = seq_len;
+  results["ring"] = ring;
+  results["zigzag_counts"] = arr(zc, 0, zc.size());
+  results["even_counts"] = arr(ec, 0, ec.size());
+  results["even_skew"] = skew;
+  std::ostringstream text;
+  text << "balance: L=" << seq_len << " ring=" << ring << "\n";
+  if (seq_len <= 64) {
+    Value lists = Value::array();
+    for (int p = 0; p < ring; ++p) {
+      lists.push_back(arr(zz, size_t(p * per), size_t((p + 1) * per)));
+      text << "  ring rank " << p << " tokens [";
+      for (int64_t i = 0; i < per; ++i) text << (i ? "," : "") << zz[size_t(p * per + i)];
+      text << "]\n";
+    }
+    results["zigzag_assignment"] = lists;
+  }
+  auto print_counts = [&](const char* name, const std::vector<int64_t>& counts) {
+    text << "  " << name << " causal pair counts:";
+    for (int64_t c : counts) text << " " << c;
+    text << "\n";
+  };
+  print_counts("zigzag", zc);
+  print_counts("even  ", ec);
+  char buf[64];
+  std::snprintf(buf, sizeof(buf), "%g", skew);  // std::ostream's default double format
+  text << "  even skew last/first = " << buf << "\n";
+  r.exit_code = 0;
+  r.status = "ok";
+  r.doc["status"] = r.status;
+  r.doc["exit_code"] = r.exit_code;
+  r.doc["results"] = results;
+  r.text = text.str();
+  return r;
+}
+
 // run_command (commands.cpp:464-491)
 Report run_command(const Value& request) {
   std::string command;
@@ -570,7 +626,8 @@ Report run_command(const Value& request) {
   }
   try {
     if (command == "simulate") return cmd_simulate(params);
-    if (command == "cost" || command == "plan" || command == "balance")
+    if (command == "balance") return cmd_balance(params);
+    if (command == "cost" || command == "plan")
       return invalid_report(command, params,
                             "command \"" + command +
                                 "\" is analytic (host-only) and not served by the B200 engine; use the "

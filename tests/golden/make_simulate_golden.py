@@ -34,6 +34,16 @@ INVALID = [
                                        "y": 1e16, "z": 123.456, "w": -0.0, "big": 18446744073709551615,
                                        "neg": -7, "s": "a\"b\\c\né", "arr": [1, 2.5, None, True]}},
 ]
+# the balance command (zigzag vs contiguous causal load), host-only
+BALANCE = [
+    {"command": "balance", "params": {}},
+    {"command": "balance", "params": {"seqlen": 64, "ring": 4}},
+    {"command": "balance", "params": {"seqlen": 131072, "ring": 8}},
+    {"command": "balance", "params": {"seqlen": 48, "ring": 3}},
+    {"command": "balance", "params": {"seqlen": 20, "ring": 4}},
+    {"command": "balance", "params": {"seqlen": 16, "ring": 0}},
+    {"command": "balance", "params": {"seqlen": 12, "ring": 1}},
+]
 # runnable simulations (the B200 side runs them in bf16; compared on structure + ledger)
 SIMULATE = [
     {"command": "simulate", "params": {"seqlen": 64, "heads": 8, "kv_heads": 2, "head_size": 16, "ulysses": 2,
@@ -70,6 +80,7 @@ def main():
         return out
 
     golden = {"invalid": [run(r) for r in INVALID] + [run("xx"), run("{\"command\": }")],
+              "balance": [run(r) for r in BALANCE],
               "simulate": [run(r) for r in SIMULATE]}
     with open(os.path.join(HERE, "simulate_golden.json"), "w") as f:
         json.dump(golden, f, indent=1)

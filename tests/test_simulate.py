@@ -63,7 +63,7 @@ def test_bf16_is_the_only_precision():
 
 
 def test_analytic_commands_are_rejected_with_a_pointer():
-    for cmd in ("cost", "plan", "balance"):
+    for cmd in ("cost", "plan"):
         r = sim.run({"command": cmd, "params": {}})
         assert r.status == 2 and "not served by the B200 engine" in r.doc["results"]["error"]
 
@@ -161,3 +161,13 @@ def test_simulate_tolerance_failure_is_exit_1(cuda):
                                                    "causal": True, "check": True, "tolerance": 1e-9}})
     assert r.status == sim.USPSIM_TOLERANCE_EXCEEDED and r.exit_code == 1
     assert r.doc["status"] == "tolerance_exceeded" and "FAIL" in r.text
+
+
+@pytest.mark.parametrize("case", _golden()["balance"], ids=lambda c: c["request"][:60])
+def test_balance_reports_identical_to_reference(case):
+    """The `balance` command (commands.cpp:414-462): zigzag vs contiguous
+    causal pair counts per ring rank, byte-identical to the reference."""
+    ours = sim.run(case["request"])
+    assert ours.status == case["status"]
+    assert ours.json == case["json"]
+    assert ours.text == case["text"]
