@@ -321,6 +321,17 @@ class Engine {
       if (t == 0) return vh;
       return kv_ring_[(t - 1) & 1].as<uint8_t>() + kv_bytes_;
     };
+    // Direct O: over a peer-memory transport the last step's
+    // epilogue stores each O row straight into the owning Ulysses member's
+    // receive buffer, so the O all-to-all overlaps the attention tile by tile.
+    static const bool direct_ok = [] {
+      const char* e = std::getenv("USP_DIRECT_O");
+      return !e || std::atoi(e) != 0;
+    }();
+    const bool direct_o = direct_ok && U_ > 1 && B_ == 1 && U_ <= 16 && tr_ && tr_->peer_memory();
+    void* o_peer[16] = {};
+    if (direct_o)
+      for (int m = 0; m < U_; ++m) o_peer[m] = tr_->ulysses_peer_ptr(*groups_, o_recv_.p, m, U_ * q_part_);
     for (int t = 0; t < R_; ++t) {
       if (t + 1 < R_) {
         USPB_CHECK(cudaEventRecord(ev_pre_[t], st));  // buf(t) ready, buf(t+1) free
@@ -333,11 +344,17 @@ class Engine {
         USPB_CHECK(cudaEventRecord(ev_recv_[t], comm_stream_));
       }
       if (t > 0) USPB_CHECK(cudaStreamWaitEvent(st, ev_recv_[t - 1], 0));
-      launch_step(t, tm_q, kbuf(t), vbuf(t), o_heads, lse, st);
+      const bool last = t == R_ - 1;
+      if (direct_o && last) tr_->ulysses_ready(*groups_, st);  // every member's o_recv_ is free
+      launch_step(t, tm_q, kbuf(t), vbuf(t), o_heads, lse, st, direct_o && last ? o_peer : nullptr);
     }
 
     // -- 3. Ulysses out: [peer][b][T][H/U] -> (b, T, H, hs)
-    if (U_ > 1) {
+    if (direct_o) {
+      tr_->ulysses_done(*groups_, st);  // every member's rows for me have landed
+      record_a2a(3, q_part_);
+      unpack_heads(o_recv_.p, o, st);
+    } else if (U_ > 1) {
       uint8_t* osend = o_h_.as<uint8_t>();
       if (B_ > 1) {
         split_seq(o_h_.p, o_send_.p, st);
@@ -893,14 +910,15 @@ class Engine {
   }
 
   void launch_step(int t, const CUtensorMap& tm_q, const void* kb, const void* vb, void* o_heads,
-                   float* lse, cudaStream_t st) {
-    launch_plan(steps_[t], tm_q, kb, vb, o_heads, lse, Tr_, Tr_, st);
+                   float* lse, cudaStream_t st, void* const* o_peer = nullptr) {
+    launch_plan(steps_[t], tm_q, kb, vb, o_heads, lse, Tr_, Tr_, st, o_peer);
   }
 
   // One attention launch over plan s: q_len query rows (tm_q, o, lse start
   // at the plan's first row) against the first k_len rows of K/V.
   void launch_plan(const DevStep& s, const CUtensorMap& tm_q, const void* kb, const void* vb,
-                   void* o_heads, float* lse, int64_t q_len, int64_t k_len, cudaStream_t st) {
+                   void* o_heads, float* lse, int64_t q_len, int64_t k_len, cudaStream_t st,
+                   void* const* o_peer = nullptr) {
     if (s.host.units.empty()) return;
     FwdParams p;
     std::memset(&p, 0, sizeof(p));
@@ -925,6 +943,11 @@ class Engine {
     p.kv_heads = kvl_;
     p.mode = static_cast<int>(s.mode);
     p.pair_rows = tiling_.pair_rows ? 1 : 0;
+    if (o_peer) {
+      for (int m = 0; m < U_; ++m) p.o_peer[m] = o_peer[m];
+      p.o_part_rows = static_cast<int>(T_);
+      p.o_me = u_;
+    }
     p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(double(hs_)));
     static const int kv_hint = [] {
       const char* e = std::getenv("USP_KV_HINT");

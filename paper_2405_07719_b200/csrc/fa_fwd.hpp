@@ -52,6 +52,13 @@ struct FwdParams {
   int num_units;
   int batch, q_len, k_len, heads, kv_heads;
   int mode;          // EpiMode
+  // Direct O (Ulysses out fused into the epilogue): when o_peer[0] != null,
+  // bf16 O row r of this rank's head-sharded block goes to Ulysses member
+  // p = r / o_part_rows, straight into that member's receive buffer at
+  // [o_me][r - p*o_part_rows][head][hs] (peer memory over NVLink).
+  void* o_peer[16];
+  int o_part_rows;   // T: rows per Ulysses part
+  int o_me;          // this rank's index in its Ulysses group
   int pair_rows;     // 1: a unit is two adjacent 128-row tiles of one head
                      //    (q_tile field = tile pair); 0: two heads of a pair
   float scale_log2;  // log2(e) / sqrt(head_size)

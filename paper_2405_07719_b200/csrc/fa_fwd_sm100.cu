@@ -433,13 +433,23 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
           }
         }
         if (write_bf16) {
+          uint4 w[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            w[i] = make_uint4(pack_bf16x2(o[8 * i + 0], o[8 * i + 1]), pack_bf16x2(o[8 * i + 2], o[8 * i + 3]),
+                              pack_bf16x2(o[8 * i + 4], o[8 * i + 5]), pack_bf16x2(o[8 * i + 6], o[8 * i + 7]));
           uint4* dst = reinterpret_cast<uint4*>(static_cast<uint8_t*>(p.o) + (row * HS + col0 + c * 32) * 2);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            dst[i] = make_uint4(pack_bf16x2(o[8 * i + 0], o[8 * i + 1]),
-                                pack_bf16x2(o[8 * i + 2], o[8 * i + 3]),
-                                pack_bf16x2(o[8 * i + 4], o[8 * i + 5]),
-                                pack_bf16x2(o[8 * i + 6], o[8 * i + 7]));
+          for (int i = 0; i < 4; ++i) dst[i] = w[i];  // head-sharded O (kept for the backward)
+          if (p.o_peer[0] != nullptr) {
+            // direct O: the same row straight into the owning Ulysses
+            // member's receive buffer (peer memory), replacing the O all-to-all
+            const int part = q_row / p.o_part_rows;
+            const size_t prow = static_cast<size_t>(p.o_me) * p.o_part_rows + (q_row - part * p.o_part_rows);
+            uint4* rdst = reinterpret_cast<uint4*>(static_cast<uint8_t*>(p.o_peer[part]) +
+                                                   ((prow * p.heads + h) * HS + col0 + c * 32) * 2);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) rdst[i] = w[i];
           }
         } else {
           float4* dst = reinterpret_cast<float4*>(p.o_acc + row * HS + col0 + c * 32);

@@ -49,6 +49,17 @@ class Transport {
   // NCCL kernels occupy SMs (the attention grid leaves room for them);
   // the local transport uses copy engines.
   virtual int reserved_sms() const = 0;
+
+  // Peer memory (optional): the address, valid on this rank's device, of
+  // Ulysses member m's copy of the symmetric buffer holding `local`
+  // (collective on first use of a buffer), and a two-phase handshake that
+  // brackets direct stores into peers' buffers: ulysses_ready() = every
+  // member's receive buffer is free, ulysses_done() = every member's stores
+  // into mine have landed. Stream-ordered.
+  virtual bool peer_memory() const { return false; }
+  virtual void* ulysses_peer_ptr(const Groups&, const void*, int, size_t) { return nullptr; }
+  virtual void ulysses_ready(const Groups&, cudaStream_t) {}
+  virtual void ulysses_done(const Groups&, cudaStream_t) {}
 };
 
 std::unique_ptr<Transport> make_local_transport(int world_size);

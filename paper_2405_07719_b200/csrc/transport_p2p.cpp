@@ -166,6 +166,25 @@ class P2PTransport final : public Transport {
       if (peer != rank_) wait(stream, 1, 0, peer, e);  // every peer's data for me landed
   }
 
+  bool peer_memory() const override { return true; }
+  void* ulysses_peer_ptr(const Groups& g, const void* local, int member, size_t bytes) override {
+    return remote(local, g.ulysses.at(member), bytes);
+  }
+  void ulysses_ready(const Groups& g, cudaStream_t stream) override {
+    const uint64_t e = ++epoch_[0];
+    for (int peer : g.ulysses)
+      if (peer != rank_) signal(stream, peer, 0, 0, e);
+    for (int peer : g.ulysses)
+      if (peer != rank_) wait(stream, 0, 0, peer, e);
+  }
+  void ulysses_done(const Groups& g, cudaStream_t stream) override {
+    const uint64_t e = epoch_[0];
+    for (int peer : g.ulysses)
+      if (peer != rank_) signal(stream, peer, 1, 0, e);
+    for (int peer : g.ulysses)
+      if (peer != rank_) wait(stream, 1, 0, peer, e);
+  }
+
   void ring_shift(const Groups& g, const std::vector<const void*>& send, const std::vector<void*>& recv,
                   const std::vector<size_t>& bytes, cudaStream_t stream) override {
     const int n = static_cast<int>(g.ring.size());
