@@ -263,7 +263,38 @@ class Engine {
     const void* kh = k;
     const void* vh = v;
     uint8_t* kv0 = kv0_.as<uint8_t>();
-    if (U_ > 1) {
+    static const bool direct_ok = [] {
+      const char* e = std::getenv("USP_DIRECT_A2A");
+      return !e || std::atoi(e) != 0;
+    }();
+    // Direct exchange over a peer-memory transport at bs = 1:
+    // the pack kernels store Q/K/V parts straight into the owning members'
+    // head-sharded buffers (no staging, no copy), and the last attention
+    // step stores O rows straight into the owners' receive buffers.
+    const bool direct = direct_ok && U_ > 1 && B_ == 1 && U_ <= 16 && tr_ && tr_->peer_memory();
+    if (direct) {
+      // -- 1. Ulysses in, fused with the pack: part m of my Q/K/V rows ->
+      //    member m's rows [u*T, (u+1)*T) of its head-sharded Q / K / V
+      void* pq[16];
+      void* pkv[16];
+      for (int m = 0; m < U_; ++m) {
+        pq[m] = tr_->ulysses_peer_ptr(*groups_, q_h_.p, m, U_ * q_part_);
+        pkv[m] = tr_->ulysses_peer_ptr(*groups_, kv0_.p, m, 2 * kv_bytes_);
+      }
+      tr_->ulysses_ready(*groups_, st);  // every member's Q/K/V buffers are free
+      for (int m = 0; m < U_; ++m) {
+        pack_part(q, static_cast<uint8_t*>(pq[m]) + u_ * q_part_, H_, hl_, m, st);
+        pack_part(k, static_cast<uint8_t*>(pkv[m]) + u_ * kv_part_, KV_, kvl_, m, st);
+        pack_part(v, static_cast<uint8_t*>(pkv[m]) + kv_bytes_ + u_ * kv_part_, KV_, kvl_, m, st);
+      }
+      tr_->ulysses_done(*groups_, st);  // every member's parts for me have landed
+      record_a2a(0, q_part_);
+      record_a2a(1, kv_part_);
+      record_a2a(2, kv_part_);
+      qh = q_h_.p;
+      kh = kv0;
+      vh = kv0 + kv_bytes_;
+    } else if (U_ > 1) {
       // -- 1. Ulysses in: pack (b,T,H,hs) -> [peer][b][T][H/U][hsk], one exchange
       uint8_t* sq = send_.as<uint8_t>();
       uint8_t* sk = sq + U_ * q_part_;
@@ -324,11 +355,7 @@ class Engine {
     // Direct O: over a peer-memory transport the last step's
     // epilogue stores each O row straight into the owning Ulysses member's
     // receive buffer, so the O all-to-all overlaps the attention tile by tile.
-    static const bool direct_ok = [] {
-      const char* e = std::getenv("USP_DIRECT_O");
-      return !e || std::atoi(e) != 0;
-    }();
-    const bool direct_o = direct_ok && U_ > 1 && B_ == 1 && U_ <= 16 && tr_ && tr_->peer_memory();
+    const bool direct_o = direct;
     void* o_peer[16] = {};
     if (direct_o)
       for (int m = 0; m < U_; ++m) o_peer[m] = tr_->ulysses_peer_ptr(*groups_, o_recv_.p, m, U_ * q_part_);
@@ -727,6 +754,21 @@ class Engine {
     rp.src_stride[3] = 1;
     rp.dst_stride[0] = B_ * T_ * local;
     rp.dst_stride[1] = T_ * local;
+    rp.dst_stride[2] = local;
+    rp.dst_stride[3] = 1;
+    rp.hs_src = hs_;
+    rp.hs_dst = hsk_;
+    permute(rp, st);
+  }
+  // bs == 1: Ulysses part m of (T, heads, hs) -> dst (T, local, hsk) rows
+  void pack_part(const void* src, void* dst, int heads, int local, int m, cudaStream_t st) {
+    RowPermute rp;
+    rp.src = static_cast<const uint8_t*>(src) + size_t(m) * local * hs_ * 2;
+    rp.dst = dst;
+    rp.dims[2] = T_;
+    rp.dims[3] = local;
+    rp.src_stride[2] = heads;
+    rp.src_stride[3] = 1;
     rp.dst_stride[2] = local;
     rp.dst_stride[3] = 1;
     rp.hs_src = hs_;

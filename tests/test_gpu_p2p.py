@@ -47,7 +47,14 @@ def _worker(rank, world, U, R, port, L, hc, kv, hs, causal, errq):
         qs, ks, vs, dos = (t[:, pos].contiguous() for t in (tq, tk, tv, tdo))
         for _ in range(2):  # the second call reuses the registered buffers and bumps the epochs
             fwd = eng.forward(qs, ks, vs)
+            fwd_launches = eng.last_launches()
             grads = eng.backward(fwd, dos)
+        if U > 1:
+            # direct exchange (default): one pack launch per member and tensor
+            # straight into the peers' buffers, the O all-to-all folded into the
+            # attention epilogue; otherwise 3 staging packs + an exchange
+            direct = os.environ.get("USP_DIRECT_A2A", "1") != "0"
+            assert fwd_launches == (3 * U if direct else 3) + R + 1, (fwd_launches, direct)
         torch.cuda.synchronize()
         qd, kd, vd, dod = widen(tq), widen(tk), widen(tv), widen(tdo)
         ref = Oracle.reference_attention(qd, kd, vd, causal)
