@@ -229,6 +229,7 @@ class Engine {
     for (auto e : ev_chunk_in_) cudaEventDestroy(e);
     for (auto e : ev_chunk_out_) cudaEventDestroy(e);
     if (ev_entry_) cudaEventDestroy(ev_entry_);
+    if (ev_kv_) cudaEventDestroy(ev_kv_);
     if (ev_drained_) cudaEventDestroy(ev_drained_);
     if (h2d_stream_) cudaStreamDestroy(h2d_stream_);
     if (d2h_stream_) cudaStreamDestroy(d2h_stream_);
@@ -440,6 +441,10 @@ class Engine {
       USPB_CHECK(cudaEventCreateWithFlags(&ev_drained_, fl));
     }
     const bool reshape = U_ > 1 || hs_ != hsk_;
+    if (U_ == 1 && R_ > 1 && B_ == 1 && !reshape && Tr_ >= 4 * kTileM) {
+      fwd_host_ring(q, k, v, o, lse, st);
+      return;
+    }
     const std::vector<int64_t> bounds = chunk_bounds();
     if (U_ > 1 || R_ > 1 || B_ > 1 || reshape || bounds.size() <= 2) {
       USPB_CHECK(cudaMemcpyAsync(hq_.p, q, qb, cudaMemcpyHostToDevice, st));
@@ -505,6 +510,111 @@ class Engine {
                      static_cast<long long>(bounds[c]), static_cast<long long>(bounds[c + 1]), at(ev_chunk_in_[c]),
                      at(ev_chunk_out_[c]));
       std::fprintf(stderr, "drained %8.3f ms\n", at(ev_drained_));
+    }
+  }
+
+  // usp_attn_fwd_host on a pure ring (U = 1, R > 1, bs 1): K and V go up
+  // first, so the ring's first K/V shift starts while Q is still uploading;
+  // Q follows in row chunks, each chunk's step-0 attention (own K/V block)
+  // launched as soon as it has landed; the last ring step runs per row chunk
+  // too, each chunk's O/LSE rows downloaded while the next chunk computes.
+  // Every launch walks the same key tiles in the same order as fwd(), so
+  // the results are bitwise those of the device-resident forward.
+  void fwd_host_ring(const void* q, const void* k, const void* v, void* o, float* lse, cudaStream_t st) {
+    ensure_ring_chunk_plans();
+    launches_ = 0;
+    ledger_.clear();
+    have_fwd_ = false;
+    for (int tsr = 0; tsr < 3; ++tsr) record_a2a(tsr, tsr == 0 ? q_part_ : kv_part_);
+    const size_t qrow = size_t(H_) * hs_ * 2, kvrow = size_t(KV_) * hs_ * 2, lrow = size_t(hl_) * 4;
+    const int n = static_cast<int>(ring_bounds_.size()) - 1;
+    USPB_CHECK(cudaEventRecord(ev_entry_, st));
+    USPB_CHECK(cudaStreamWaitEvent(h2d_stream_, ev_entry_, 0));
+    USPB_CHECK(cudaStreamWaitEvent(d2h_stream_, ev_entry_, 0));
+    USPB_CHECK(cudaMemcpyAsync(hk_.p, k, Tr_ * kvrow, cudaMemcpyHostToDevice, h2d_stream_));
+    USPB_CHECK(cudaMemcpyAsync(hv_.p, v, Tr_ * kvrow, cudaMemcpyHostToDevice, h2d_stream_));
+    USPB_CHECK(cudaEventRecord(ev_kv_, h2d_stream_));
+    USPB_CHECK(cudaStreamWaitEvent(st, ev_kv_, 0));
+    auto kbuf = [&](int t) -> const void* { return t == 0 ? hk_.p : kv_ring_[(t - 1) & 1].p; };
+    auto vbuf = [&](int t) -> const void* {
+      return t == 0 ? hv_.p : static_cast<const void*>(kv_ring_[(t - 1) & 1].as<uint8_t>() + kv_bytes_);
+    };
+    const CUtensorMap tm_q = make_tmap(hq_.p, hsk_, hl_, Tr_, B_);
+    for (int t = 0; t < R_; ++t) {
+      if (t + 1 < R_) {
+        USPB_CHECK(cudaEventRecord(ev_pre_[t], st));
+        USPB_CHECK(cudaStreamWaitEvent(comm_stream_, ev_pre_[t], 0));
+        record_shift(1);
+        record_shift(2);
+        tr_->ring_shift(*groups_, {kbuf(t), vbuf(t)},
+                        {const_cast<void*>(kbuf(t + 1)), const_cast<void*>(vbuf(t + 1))},
+                        {kv_bytes_, kv_bytes_}, comm_stream_);
+        USPB_CHECK(cudaEventRecord(ev_recv_[t], comm_stream_));
+      }
+      if (t > 0) USPB_CHECK(cudaStreamWaitEvent(st, ev_recv_[t - 1], 0));
+      if (t != 0 && t != R_ - 1) {
+        launch_step(t, tm_q, kbuf(t), vbuf(t), ho_.p, hlse_.as<float>(), st);
+        continue;
+      }
+      for (int c = 0; c < n; ++c) {
+        const int64_t r0 = ring_bounds_[c], r1 = ring_bounds_[c + 1];
+        if (t == 0) {
+          USPB_CHECK(cudaMemcpyAsync(hq_.as<uint8_t>() + r0 * qrow, static_cast<const uint8_t*>(q) + r0 * qrow,
+                                     (r1 - r0) * qrow, cudaMemcpyHostToDevice, h2d_stream_));
+          USPB_CHECK(cudaEventRecord(ev_chunk_in_[c], h2d_stream_));
+          USPB_CHECK(cudaStreamWaitEvent(st, ev_chunk_in_[c], 0));
+        }
+        const CUtensorMap tmc = make_tmap(hq_.as<uint8_t>() + r0 * qrow, hsk_, hl_, r1 - r0, B_);
+        launch_plan(t == 0 ? ring_first_[c] : ring_last_[c], tmc, kbuf(t), vbuf(t), ho_.as<uint8_t>() + r0 * qrow,
+                    hlse_.as<float>() + r0 * hl_, r1 - r0, Tr_, st, nullptr, r0);
+        if (t == R_ - 1) {
+          USPB_CHECK(cudaEventRecord(ev_chunk_out_[c], st));
+          USPB_CHECK(cudaStreamWaitEvent(d2h_stream_, ev_chunk_out_[c], 0));
+          USPB_CHECK(cudaMemcpyAsync(static_cast<uint8_t*>(o) + r0 * qrow, ho_.as<uint8_t>() + r0 * qrow,
+                                     (r1 - r0) * qrow, cudaMemcpyDeviceToHost, d2h_stream_));
+          USPB_CHECK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(lse) + r0 * lrow, hlse_.as<uint8_t>() + r0 * lrow,
+                                     (r1 - r0) * lrow, cudaMemcpyDeviceToHost, d2h_stream_));
+        }
+      }
+    }
+    record_a2a(3, q_part_);
+    USPB_CHECK(cudaEventRecord(ev_drained_, d2h_stream_));
+    USPB_CHECK(cudaStreamWaitEvent(st, ev_drained_, 0));
+    have_fwd_ = true;
+    fwd_ledger_size_ = ledger_.size();
+  }
+
+  // Row chunks of the pure-ring host path (4 chunks of whole tiles) and the
+  // step-0 (kFirst) / last-step (kLast) plans restricted to each.
+  void ensure_ring_chunk_plans() {
+    if (!ring_first_.empty()) return;
+    const int64_t c = std::max<int64_t>((Tr_ / 4 + kTileM - 1) / kTileM * kTileM, kTileM);
+    ring_bounds_ = {0};
+    for (int64_t r = c; r < Tr_; r += c) ring_bounds_.push_back(r);
+    ring_bounds_.push_back(Tr_);
+    const auto my_pos = head_positions(shape_, cfg_.rank);
+    const auto k_first = head_positions(shape_, shape_.mesh.rank_of(u_, ring_source(r_, 0, R_)));
+    const auto k_last = head_positions(shape_, shape_.mesh.rank_of(u_, ring_source(r_, R_ - 1, R_)));
+    for (size_t i = 0; i + 1 < ring_bounds_.size(); ++i) {
+      const std::vector<int64_t> qp(my_pos.begin() + ring_bounds_[i], my_pos.begin() + ring_bounds_[i + 1]);
+      DevStep f, l;
+      upload_plan(f, plan_step(qp, k_first, shape_.causal, B_, tiling_.head_units, true, tiling_.units_per_kv,
+                               tiling_.rows_per_unit));
+      f.mode = EpiMode::kFirst;
+      upload_plan(l, plan_step(qp, k_last, shape_.causal, B_, tiling_.head_units, true, tiling_.units_per_kv,
+                               tiling_.rows_per_unit));
+      l.mode = EpiMode::kLast;
+      ring_first_.push_back(std::move(f));
+      ring_last_.push_back(std::move(l));
+    }
+    const unsigned fl = std::getenv("USP_HOST_TRACE") ? cudaEventDefault : cudaEventDisableTiming;
+    USPB_CHECK(cudaEventCreateWithFlags(&ev_kv_, fl));
+    while (ev_chunk_in_.size() < ring_first_.size()) {
+      cudaEvent_t a, e;
+      USPB_CHECK(cudaEventCreateWithFlags(&a, fl));
+      USPB_CHECK(cudaEventCreateWithFlags(&e, fl));
+      ev_chunk_in_.push_back(a);
+      ev_chunk_out_.push_back(e);
     }
   }
 
@@ -960,7 +1070,7 @@ class Engine {
   // at the plan's first row) against the first k_len rows of K/V.
   void launch_plan(const DevStep& s, const CUtensorMap& tm_q, const void* kb, const void* vb,
                    void* o_heads, float* lse, int64_t q_len, int64_t k_len, cudaStream_t st,
-                   void* const* o_peer = nullptr) {
+                   void* const* o_peer = nullptr, int64_t row0 = 0) {
     if (s.host.units.empty()) return;
     FwdParams p;
     std::memset(&p, 0, sizeof(p));
@@ -969,8 +1079,8 @@ class Engine {
     p.tm_v = make_tmap(vb, hsk_, kvl_, k_len, B_);
     p.o = o_heads;
     p.lse = lse;
-    p.o_acc = o_acc_.as<float>();
-    p.lse_acc = lse_acc_.as<float>();
+    p.o_acc = o_acc_.p ? o_acc_.as<float>() + row0 * hl_ * hsk_ : nullptr;  // bs 1 when row0 > 0
+    p.lse_acc = lse_acc_.p ? lse_acc_.as<float>() + row0 * hl_ : nullptr;
     p.units = s.units.as<uint32_t>();
     p.tile_off = s.tile_off.as<int32_t>();
     p.tile_list = s.tile_list.as<int32_t>();
@@ -1076,6 +1186,9 @@ class Engine {
   // usp_attn_fwd_host staging and its chunk pipeline
   DevBuf hq_, hk_, hv_, ho_, hlse_;
   std::vector<DevStep> chunk_steps_;
+  std::vector<DevStep> ring_first_, ring_last_;  // pure-ring host path
+  std::vector<int64_t> ring_bounds_;
+  cudaEvent_t ev_kv_ = nullptr;
   std::vector<int64_t> chunk_bounds_;
   cudaStream_t h2d_stream_ = nullptr, d2h_stream_ = nullptr;
   cudaEvent_t ev_entry_ = nullptr, ev_drained_ = nullptr;

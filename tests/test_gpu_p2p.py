@@ -49,6 +49,15 @@ def _worker(rank, world, U, R, port, L, hc, kv, hs, causal, errq):
             fwd = eng.forward(qs, ks, vs)
             fwd_launches = eng.last_launches()
             grads = eng.backward(fwd, dos)
+        # the host-buffer entry (usp_attn_fwd_host; pipelined on a pure ring)
+        # must reproduce the device-resident forward bit for bit
+        pin = lambda t: t.cpu().pin_memory()  # noqa: E731
+        oh = torch.empty(fwd.out.shape, dtype=torch.bfloat16).pin_memory()
+        lh = torch.empty(fwd.logsumexp.shape, dtype=torch.float32).pin_memory()
+        eng.forward_host(pin(qs), pin(ks), pin(vs), oh, lh)
+        torch.cuda.synchronize()
+        assert torch.equal(oh.view(torch.int16), fwd.out.cpu().view(torch.int16)), rank
+        assert torch.equal(lh.view(torch.int32), fwd.logsumexp.cpu().view(torch.int32)), rank
         if U > 1:
             # direct exchange (default): one pack launch per member and tensor
             # straight into the peers' buffers, the O all-to-all folded into the
@@ -82,7 +91,7 @@ def test_p2p_transport_multi_process(cuda, U, R):
     errq = ctx.Queue()
     world = U * R
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, U, R, port, 512, 8, 4 if U <= 4 else 8, 128, True, errq))
+    procs = [ctx.Process(target=_worker, args=(r, world, U, R, port, 2048, 8, 4 if U <= 4 else 8, 128, True, errq))
              for r in range(world)]
     for p in procs:
         p.start()
