@@ -155,8 +155,9 @@ class Engine {
     hs_ = shape_.head_size;
     hsk_ = shape_.kernel_head_size();
     const int group = hl_ / kvl_;
-    tiling_ = fwd_tiling(hl_, kvl_);
+    tiling_ = fwd_tiling(hl_, kvl_, hsk_);
     nq_ = (tiling_.pair_rows || group % 2 == 0) ? 2 : 1;
+    cluster_ = tiling_.cluster;  // 2-CTA clusters sharing K/V tiles by TMA multicast
 
     USPB_CHECK(cudaSetDevice(c.device));
     USPB_CHECK(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, c.device));
@@ -1095,6 +1096,7 @@ class Engine {
     p.kv_heads = kvl_;
     p.mode = static_cast<int>(s.mode);
     p.pair_rows = tiling_.pair_rows ? 1 : 0;
+    p.cluster = cluster_ ? 1 : 0;
     if (o_peer) {
       for (int m = 0; m < U_; ++m) p.o_peer[m] = o_peer[m];
       p.o_part_rows = static_cast<int>(T_);
@@ -1119,7 +1121,8 @@ class Engine {
     }
     const int reserve = (R_ > 1 && tr_) ? tr_->reserved_sms() : 0;
     const int slots = std::max(1, num_sms_ - reserve);
-    const int grid = std::min(p.num_units, slots);
+    // cluster mode: two CTAs (one per SM of a TPC) per unit, an even grid
+    const int grid = cluster_ ? std::max(2, std::min(2 * p.num_units, slots) & ~1) : std::min(p.num_units, slots);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (timing_) {
       e0 = timing_event(2 * timed_.size());
@@ -1174,6 +1177,7 @@ class Engine {
   UspShape shape_;
   int U_ = 1, R_ = 1, u_ = 0, r_ = 0, H_ = 0, KV_ = 0, hl_ = 0, kvl_ = 0, hs_ = 0, hsk_ = 0, nq_ = 1;
   FwdTiling tiling_{};
+  bool cluster_ = false;
   int64_t B_ = 1, T_ = 0, Tr_ = 0;
   int num_sms_ = 148;
   size_t q_part_ = 0, kv_part_ = 0, kv_bytes_ = 0;
@@ -1318,7 +1322,7 @@ usp_status usp_schedule(const usp_config* cfg, int32_t step, usp_step_info* out)
     const int R = s.mesh.ring;
     const int src = ring_source(r, step, R);
     const int kvl = s.local_kv_heads();
-    const FwdTiling tl = fwd_tiling(s.local_heads(), kvl);
+    const FwdTiling tl = fwd_tiling(s.local_heads(), kvl, s.kernel_head_size());
     const auto st = plan_step(head_positions(s, cfg->rank),
                               head_positions(s, s.mesh.rank_of(u, src)), s.causal, s.batch,
                               tl.head_units, R == 1 || step == 0 || step == R - 1, tl.units_per_kv,

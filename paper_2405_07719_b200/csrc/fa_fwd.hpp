@@ -59,6 +59,7 @@ struct FwdParams {
   void* o_peer[16];
   int o_part_rows;   // T: rows per Ulysses part
   int o_me;          // this rank's index in its Ulysses group
+  int cluster;       // 1: 2-CTA clusters, unit hp field = head quad (fa_fwd_sm100.cu MC)
   int pair_rows;     // 1: a unit is two adjacent 128-row tiles of one head
                      //    (q_tile field = tile pair); 0: two heads of a pair
   float scale_log2;  // log2(e) / sqrt(head_size)

@@ -132,27 +132,37 @@ __device__ __forceinline__ void dispatch_slot(uint32_t slot, F&& f) {
 // it % depth, reads the unit index, and one lane per warp releases the slot.
 // whole_warp: all 32 lanes run this (softmax warps); otherwise a single
 // lane (the MMA issuer) does.
-template <int kDepth>
+// MC (2-CTA cluster): the tickets are written by the leader CTA into both
+// CTAs' slots and every consumer releases the LEADER's slot.
+template <int kDepth, int MC>
 __device__ __forceinline__ int next_unit_impl(uint64_t* full, uint64_t* empty, const int* slot,
                                               uint32_t it, bool whole_warp) {
   const uint32_t d = it % kDepth;
-  mbar_wait(&full[d], (it / kDepth) & 1);
+  if constexpr (MC)
+    mbar_wait_cluster(&full[d], (it / kDepth) & 1);
+  else
+    mbar_wait(&full[d], (it / kDepth) & 1);
   const int u = *reinterpret_cast<const volatile int*>(&slot[d]);
-  if (whole_warp) {
-    __syncwarp();
-    if (lane_id() == 0) mbar_arrive(&empty[d]);
-  } else {
-    mbar_arrive(&empty[d]);
+  if (whole_warp) __syncwarp();
+  if (!whole_warp || lane_id() == 0) {
+    if constexpr (MC)
+      mbar_arrive_cluster(mapa_shared(smem_u32(&empty[d]), 0));
+    else
+      mbar_arrive(&empty[d]);
   }
   return u;
 }
 #define next_unit(full, empty, slot, it, whole_warp) \
-  next_unit_impl<C::kSchedDepth>(full, empty, slot, it, whole_warp)
+  next_unit_impl<C::kSchedDepth, MC>(full, empty, slot, it, whole_warp)
 
-template <int NQ, int HS, int POLY, int SPL>
+// MC = 1: a 2-CTA cluster runs the two head pairs of a 4-head GQA group over
+// the same rows (unit = q tile x head quad); each CTA loads half of every
+// K/V tile and multicasts it to both, so L2->SMEM traffic per FLOP halves.
+template <int NQ, int HS, int POLY, int SPL, int MC>
 __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
     fa_fwd_sm100_kernel(const __grid_constant__ FwdParams p) {
   using C = FwdCfg<NQ, HS, POLY, SPL>;
+  static_assert(!MC || (NQ == 2 && HS == 128), "cluster mode: two head pairs, 128-column tiles");
   constexpr int NS = C::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -176,6 +186,9 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t crank = MC ? cluster_ctarank() : 0u;
+  // the head pair a unit's hp field names for this CTA
+  auto unit_hp = [&](uint32_t unit) { return MC ? int((unit >> 16) & 0xFF) * 2 + int(crank) : int((unit >> 16) & 0xFF); };
 
   if (threadIdx.x == 0) {
     for (int t = 0; t < NQ; ++t) {
@@ -188,11 +201,12 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
     mbar_init(q_empty, 1);
     for (int d = 0; d < C::kSchedDepth; ++d) {
       mbar_init(&sched_full[d], 1);
-      mbar_init(&sched_empty[d], 2 + C::kSoftmaxWarps);  // S warp, PV warp, softmax warps
+      // S warp, PV warp, softmax warps (of both CTAs + the peer's TMA warp with MC)
+      mbar_init(&sched_empty[d], MC ? 2 * (2 + C::kSoftmaxWarps) + 1 : 2 + C::kSoftmaxWarps);
     }
     for (int s = 0; s < NS; ++s) {
       mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
+      mbar_init(&kv_empty[s], MC ? 2 : 1);  // MC: both CTAs' MMAs have read the slot
     }
     fence_barrier_init();
   }
@@ -241,7 +255,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
       const int u = next_unit(sched_full, sched_empty, sched_slot, it, true);
       if (u >= p.num_units) break;
       const uint32_t unit = p.units[u];
-      const int qt = unit & 0xFFFF, hp = (unit >> 16) & 0xFF, b = unit >> 24;
+      const int qt = unit & 0xFFFF, hp = unit_hp(unit), b = unit >> 24;
       const int h = p.pair_rows ? hp : hp * NQ + t;
       const int beg = p.tile_off[qt];
       const int n = p.tile_off[qt + 1] - beg;
@@ -477,14 +491,25 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
       for (uint32_t it = 0;; ++it) {
         // Claim the next unit (dynamic, longest-first) and hand it to the
         // consumer roles through the ticket ring.
-        const int u = atomicAdd(&p.sched[0], 1);
         const uint32_t d = it % C::kSchedDepth;
-        mbar_wait(&sched_empty[d], ((it / C::kSchedDepth) & 1) ^ 1);
-        sched_slot[d] = u;
-        mbar_arrive(&sched_full[d]);
+        int u;
+        if (!MC || crank == 0) {
+          u = atomicAdd(&p.sched[0], 1);
+          mbar_wait(&sched_empty[d], ((it / C::kSchedDepth) & 1) ^ 1);
+          sched_slot[d] = u;
+          if constexpr (MC) {  // the same ticket to the peer CTA
+            st_cluster_u32(mapa_shared(smem_u32(&sched_slot[d]), 1), static_cast<uint32_t>(u));
+            mbar_arrive_cluster(mapa_shared(smem_u32(&sched_full[d]), 1));
+          }
+          mbar_arrive(&sched_full[d]);
+        } else {  // MC peer: take the leader's ticket like a consumer
+          mbar_wait_cluster(&sched_full[d], (it / C::kSchedDepth) & 1);
+          u = *reinterpret_cast<const volatile int*>(&sched_slot[d]);
+          mbar_arrive_cluster(mapa_shared(smem_u32(&sched_empty[d]), 0));
+        }
         if (u >= p.num_units) break;
         const uint32_t unit = p.units[u];
-        const int qt = unit & 0xFFFF, hp = (unit >> 16) & 0xFF, b = unit >> 24;
+        const int qt = unit & 0xFFFF, hp = unit_hp(unit), b = unit >> 24;
         const int beg = p.tile_off[qt];
         const int n = p.tile_off[qt + 1] - beg;
         if (n == 0) continue;
@@ -508,14 +533,19 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
             ++kv_it;
             mbar_arrive_expect_tx(&kv_full[slot], C::kKVBytes);
             const CUtensorMap* tm = which == 0 ? &p.tm_k : &p.tm_v;
+            if constexpr (MC) {  // my half of the tile, to both CTAs
+              tma_load_4d_mc(sKV + slot * C::kKVBytes + crank * C::kSubBytes, tm, &kv_full[slot], int(crank) * 64,
+                             kvh, kt * kTileN, b, uint16_t(0x3));
+            } else {
 #pragma unroll
-            for (int sb = 0; sb < C::kSub; ++sb) {
-              if (hint)
-                tma_load_4d_hint(sKV + slot * C::kKVBytes + sb * C::kSubBytes, tm, &kv_full[slot],
-                                 sb * 64, kvh, kt * kTileN, b, keep);
-              else
-                tma_load_4d(sKV + slot * C::kKVBytes + sb * C::kSubBytes, tm, &kv_full[slot],
-                            sb * 64, kvh, kt * kTileN, b);
+              for (int sb = 0; sb < C::kSub; ++sb) {
+                if (hint)
+                  tma_load_4d_hint(sKV + slot * C::kKVBytes + sb * C::kSubBytes, tm, &kv_full[slot],
+                                   sb * 64, kvh, kt * kTileN, b, keep);
+                else
+                  tma_load_4d(sKV + slot * C::kKVBytes + sb * C::kSubBytes, tm, &kv_full[slot],
+                              sb * 64, kvh, kt * kTileN, b);
+              }
             }
           }
         }
@@ -605,7 +635,12 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
               if (lane == 0) trace_ev(p, 11 + 2 * t, j);
               ++s_count;
             }
-            commit_one(&kv_empty[ki % NS]);
+            if constexpr (MC) {
+              if (elect_one()) mma_commit_mc(&kv_empty[ki % NS], uint16_t(0x3));
+              __syncwarp();
+            } else {
+              commit_one(&kv_empty[ki % NS]);
+            }
             if (j == n - 1) commit_one(q_empty);
           }
         } else {
@@ -622,7 +657,12 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
               issue_pv(t, vi % NS, j > 0);
               commit_one(&pv_done[t]);
             }
-            commit_one(&kv_empty[vi % NS]);
+            if constexpr (MC) {
+              if (elect_one()) mma_commit_mc(&kv_empty[vi % NS], uint16_t(0x3));
+              __syncwarp();
+            } else {
+              commit_one(&kv_empty[vi % NS]);
+            }
           }
         }
         kv_it += 2 * n;
@@ -631,9 +671,9 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
   }
 
   }  // producer warpgroup
-  if (warp == C::kTmaWarp && lane == 0) {
-    // The last CTA to finish claiming resets the tickets for the next launch.
-    if (atomicAdd(&p.sched[1], 1) == static_cast<int>(gridDim.x) - 1) {
+  if (warp == C::kTmaWarp && lane == 0 && crank == 0) {
+    // The last claimer to finish resets the tickets for the next launch.
+    if (atomicAdd(&p.sched[1], 1) == static_cast<int>(gridDim.x) / (MC ? 2 : 1) - 1) {
       p.sched[0] = 0;
       p.sched[1] = 0;
       __threadfence();
@@ -641,18 +681,34 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (MC) cluster_sync();  // no remote ticket / barrier traffic may target an exited CTA
   tc_fence_after();
   if (warp == C::kMmaWarp) tmem_dealloc(tmem, C::kTmemCols);
 }
 
 // --------------------------------------------------------------- launchers
-template <int NQ, int HS, int POLY, int SPL>
+template <int NQ, int HS, int POLY, int SPL, int MC = 0>
 static cudaError_t launch_impl(const FwdParams& p, int grid, cudaStream_t stream) {
   using C = FwdCfg<NQ, HS, POLY, SPL>;
-  auto kern = fa_fwd_sm100_kernel<NQ, HS, POLY, SPL>;
+  auto kern = fa_fwd_sm100_kernel<NQ, HS, POLY, SPL, MC>;
   static std::atomic<uint64_t> attr_done{0};  // per instantiation and device
   const cudaError_t e = ensure_smem_attr(kern, C::kSmemBytes, attr_done);
   if (e != cudaSuccess) return e;
+  if constexpr (MC) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid & ~1), 1, 1);
+    cfg.blockDim = dim3(C::kThreads, 1, 1);
+    cfg.dynamicSmemBytes = C::kSmemBytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, p);
+  }
   kern<<<grid, C::kThreads, C::kSmemBytes, stream>>>(p);
   return cudaGetLastError();
 }
@@ -681,6 +737,10 @@ static cudaError_t launch_variant(const FwdParams& p, int grid, cudaStream_t str
 }
 
 cudaError_t launch_fa_fwd(const FwdParams& p, int nq, int hs, int grid, cudaStream_t stream) {
+  if (p.cluster) {
+    if (nq != 2 || hs != 128 || p.pair_rows) return cudaErrorInvalidValue;
+    return launch_impl<2, 128, 0, 1, 1>(p, grid, stream);
+  }
   if (nq == 2 && hs == 128) return launch_variant<2, 128>(p, grid, stream);
   if (nq == 1 && hs == 128) return launch_variant<1, 128>(p, grid, stream);
   if (nq == 2 && hs == 64) return launch_variant<2, 64>(p, grid, stream);

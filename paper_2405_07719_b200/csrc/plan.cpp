@@ -225,15 +225,20 @@ int64_t visible_pairs(const std::vector<int64_t>& q_pos, const std::vector<int64
   return pairs;
 }
 
-FwdTiling fwd_tiling(int hl, int kvl) {
+FwdTiling fwd_tiling(int hl, int kvl, int hsk) {
   static const bool rows_ok = [] {
     const char* e = std::getenv("USP_FA_PAIR_ROWS");
     return !e || std::atoi(e) != 0;
   }();
+  static const bool cluster_ok = [] {
+    const char* e = std::getenv("USP_FA_CLUSTER");
+    return !e || std::atoi(e) != 0;
+  }();
   const int group = hl / kvl;
-  if (group % 2 == 0) return {false, hl / 2, group / 2, kTileM};
-  if (rows_ok) return {true, hl, group, 2 * kTileM};
-  return {false, hl, group, kTileM};  // one q tile per CTA (development fallback)
+  if (group % 4 == 0 && hsk == 128 && cluster_ok) return {false, hl / 4, group / 4, kTileM, true};
+  if (group % 2 == 0) return {false, hl / 2, group / 2, kTileM, false};
+  if (rows_ok) return {true, hl, group, 2 * kTileM, false};
+  return {false, hl, group, kTileM, false};  // one q tile per CTA (development fallback)
 }
 
 StepPlan plan_step(const std::vector<int64_t>& q_pos, const std::vector<int64_t>& k_pos,

@@ -100,13 +100,17 @@ StepPlan plan_step(const std::vector<int64_t>& q_pos, const std::vector<int64_t>
 // GQA group over the same rows when the local group is even (K/V tiles and
 // masks shared), otherwise two adjacent 128-row tiles of ONE head (MHA and
 // odd groups; K/V tiles shared, key-tile list = union, per-element masks).
+// With a 4-head (or larger multiple) local group at head size 128, a 2-CTA
+// cluster runs both head pairs of a head quad and shares each K/V tile by
+// TMA multicast (unit = q tile x head quad).
 struct FwdTiling {
   bool pair_rows;    // two row tiles of one head (else two heads)
-  int head_units;    // head slots per unit list entry (head pairs or heads)
+  int head_units;    // head slots per unit list entry (head pairs, quads or heads)
   int units_per_kv;  // head slots sharing one kv head
   int rows_per_unit; // 128 or 256
+  bool cluster;      // 2-CTA clusters over head quads
 };
-FwdTiling fwd_tiling(int local_heads, int local_kv_heads);
+FwdTiling fwd_tiling(int local_heads, int local_kv_heads, int kernel_head_size);
 
 // The same block transposed for the dK/dV kernel: CSR over KEY tiles
 // (tile_list = q tile | partial << 31, same partial flags), units
