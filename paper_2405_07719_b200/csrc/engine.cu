@@ -71,14 +71,14 @@ static EncodeTiledFn encode_fn() {
 // (hs, heads, seq, batch) bf16 tensor; box = one 128-row x 64-column block
 // of one head, 128-byte swizzled to match the UMMA SW128 descriptors.
 static CUtensorMap make_tmap(const void* base, int64_t hs, int64_t heads, int64_t seq,
-                             int64_t batch) {
+                             int64_t batch, uint32_t box_rows = kTileM) {
   CUtensorMap m;
   const cuuint64_t dims[4] = {static_cast<cuuint64_t>(hs), static_cast<cuuint64_t>(heads),
                               static_cast<cuuint64_t>(seq), static_cast<cuuint64_t>(batch)};
   const cuuint64_t strides[3] = {static_cast<cuuint64_t>(hs * 2),
                                  static_cast<cuuint64_t>(heads * hs * 2),
                                  static_cast<cuuint64_t>(seq * heads * hs * 2)};
-  const cuuint32_t box[4] = {64, 1, static_cast<cuuint32_t>(kTileM), 1};
+  const cuuint32_t box[4] = {64, 1, box_rows, 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base),
                                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -158,6 +158,11 @@ class Engine {
     tiling_ = fwd_tiling(hl_, kvl_, hsk_);
     nq_ = (tiling_.pair_rows || group % 2 == 0) ? 2 : 1;
     cluster_ = tiling_.cluster;  // 2-CTA clusters sharing K/V tiles by TMA multicast
+    static const int cluster_mode = [] {  // 2: cta_group::2 MMAs on the same clusters (experimental)
+      const char* e = std::getenv("USP_FA_CLUSTER");
+      return e ? std::atoi(e) : 1;
+    }();
+    cluster_mode_ = cluster_ ? (cluster_mode == 2 ? 2 : 1) : 0;
 
     USPB_CHECK(cudaSetDevice(c.device));
     USPB_CHECK(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, c.device));
@@ -1096,7 +1101,8 @@ class Engine {
     p.kv_heads = kvl_;
     p.mode = static_cast<int>(s.mode);
     p.pair_rows = tiling_.pair_rows ? 1 : 0;
-    p.cluster = cluster_ ? 1 : 0;
+    p.cluster = cluster_mode_;
+    if (cluster_mode_ == 2) p.tm_k64 = make_tmap(kb, hsk_, kvl_, k_len, B_, 64);
     if (o_peer) {
       for (int m = 0; m < U_; ++m) p.o_peer[m] = o_peer[m];
       p.o_part_rows = static_cast<int>(T_);
@@ -1178,6 +1184,7 @@ class Engine {
   int U_ = 1, R_ = 1, u_ = 0, r_ = 0, H_ = 0, KV_ = 0, hl_ = 0, kvl_ = 0, hs_ = 0, hsk_ = 0, nq_ = 1;
   FwdTiling tiling_{};
   bool cluster_ = false;
+  int cluster_mode_ = 0;
   int64_t B_ = 1, T_ = 0, Tr_ = 0;
   int num_sms_ = 148;
   size_t q_part_ = 0, kv_part_ = 0, kv_bytes_ = 0;

@@ -35,6 +35,7 @@ struct FwdParams {
   CUtensorMap tm_q;  // (hs, heads, q_len, batch) bf16, box (64, 1, 128, 1), SW128
   CUtensorMap tm_k;  // (hs, kv_heads, k_len, batch)
   CUtensorMap tm_v;
+  CUtensorMap tm_k64;  // K with 64-row boxes (2SM cluster mode: each CTA loads 64 keys)
 
   void* o;            // bf16 (batch, q_len, heads, hs)  [kSingle, kLast]
   float* lse;         // fp32 (batch, q_len, heads), natural log [kSingle, kLast]
@@ -59,7 +60,7 @@ struct FwdParams {
   void* o_peer[16];
   int o_part_rows;   // T: rows per Ulysses part
   int o_me;          // this rank's index in its Ulysses group
-  int cluster;       // 1: 2-CTA clusters, unit hp field = head quad (fa_fwd_sm100.cu MC)
+  int cluster;       // 1/2: 2-CTA clusters (TMA multicast / cta_group::2 MMAs), unit hp = head quad
   int pair_rows;     // 1: a unit is two adjacent 128-row tiles of one head
                      //    (q_tile field = tile pair); 0: two heads of a pair
   float scale_log2;  // log2(e) / sqrt(head_size)

@@ -163,6 +163,10 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
     fa_fwd_sm100_kernel(const __grid_constant__ FwdParams p) {
   using C = FwdCfg<NQ, HS, POLY, SPL>;
   static_assert(!MC || (NQ == 2 && HS == 128), "cluster mode: two head pairs, 128-column tiles");
+  // MC == 2: cta_group::2 MMAs (M = 256 over the pair): the leader CTA issues
+  // every MMA; each CTA holds its own Q tiles, one 64-key half of every K
+  // tile and one 64-column half of every V tile.
+  constexpr bool k2 = MC == 2;
   constexpr int NS = C::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -194,10 +198,10 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
     for (int t = 0; t < NQ; ++t) {
       mbar_init(&q_full[t], 1);
       mbar_init(&s_full[t], 1);
-      mbar_init(&p_ready[t], 128 * SPL);
+      mbar_init(&p_ready[t], k2 ? 2 * 4 * SPL : 128 * SPL);  // 2SM: one lane per warp of both CTAs
       mbar_init(&pv_done[t], 1);
     }
-    mbar_init(s_free, 4 * SPL);  // one lane of each warp of the group holding S
+    mbar_init(s_free, (k2 ? 2 : 1) * 4 * SPL);  // one lane of each warp holding S (both CTAs with 2SM)
     mbar_init(q_empty, 1);
     for (int d = 0; d < C::kSchedDepth; ++d) {
       mbar_init(&sched_full[d], 1);
@@ -206,11 +210,16 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
     }
     for (int s = 0; s < NS; ++s) {
       mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], MC ? 2 : 1);  // MC: both CTAs' MMAs have read the slot
+      mbar_init(&kv_empty[s], MC == 1 ? 2 : 1);  // MC 1: both CTAs' MMAs have read the slot
     }
     fence_barrier_init();
   }
-  if (warp == C::kMmaWarp) tmem_alloc(tmem_slot, C::kTmemCols);
+  if (warp == C::kMmaWarp) {
+    if constexpr (k2)
+      tmem_alloc_2sm(tmem_slot, C::kTmemCols);
+    else
+      tmem_alloc(tmem_slot, C::kTmemCols);
+  }
   if (warp == C::kTmaWarp && lane == 0) {
     tma_prefetch_desc(&p.tm_q);
     tma_prefetch_desc(&p.tm_k);
@@ -218,6 +227,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (MC > 0) cluster_sync();  // the peer's barriers are initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   // One CTA per SM (shared memory) owns all of TMEM, so the allocation
@@ -264,7 +274,10 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
       float m_run = -INFINITY, l_run = 0.f, m_use = 0.f;
       for (int j = 0; j < n; ++j) {
         const int entry = p.tile_list[beg + j];
-        mbar_wait(&s_full[t], s_phase & 1);
+        if constexpr (k2)
+          mbar_wait_cluster(&s_full[t], s_phase & 1);
+        else
+          mbar_wait(&s_full[t], s_phase & 1);
         const bool tr = quarter == 0 && half == 0 && lane == 0;
         if (tr) trace_ev(p, 0 + 5 * t, s_phase);
         const uint32_t par = s_phase & 1;
@@ -278,7 +291,12 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
         // S is in registers: the shared S buffer may take the next S.
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(s_free);
+        if (lane == 0) {
+          if constexpr (k2)
+            mbar_arrive_cluster(mapa_shared(smem_u32(s_free), 0));
+          else
+            mbar_arrive(s_free);
+        }
         if (tr) trace_ev(p, 1 + 5 * t, s_phase - 1, __uint_as_float(s[KC - 1]));
         if (entry < 0) {  // partial tile: apply the position mask per element
           const int kt = entry & 0x7FFFFFFF;
@@ -358,7 +376,10 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
         l_run = l_run * alpha + (sum0 + sum1);  // this warp's columns only (SPL == 2)
         if (j > 0) {
           // PV_t(j-1) must be done before P_t is overwritten and O_t rescaled
-          mbar_wait(&pv_done[t], pv_phase & 1);
+          if constexpr (k2)
+            mbar_wait_cluster(&pv_done[t], pv_phase & 1);
+          else
+            mbar_wait(&pv_done[t], pv_phase & 1);
           ++pv_phase;
           tc_fence_after();
         }
@@ -377,13 +398,21 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
         }
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(&p_ready[t]);
+        if constexpr (k2) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&p_ready[t]), 0));
+        } else {
+          mbar_arrive(&p_ready[t]);
+        }
         if (tr) trace_ev(p, 4 + 5 * t, s_phase - 1);
       }
 
       // ------------------------------------------------------------ epilogue
       if (n > 0) {  // the unit's last PV_t
-        mbar_wait(&pv_done[t], pv_phase & 1);
+        if constexpr (k2)
+          mbar_wait_cluster(&pv_done[t], pv_phase & 1);
+        else
+          mbar_wait(&pv_done[t], pv_phase & 1);
         ++pv_phase;
         tc_fence_after();
       }
@@ -516,12 +545,20 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
         mbar_wait(q_empty, (q_it & 1) ^ 1);
         ++q_it;
         for (int t = 0; t < NQ; ++t) {
-          mbar_arrive_expect_tx(&q_full[t], C::kQBytes);
           const int qh = p.pair_rows ? hp : hp * NQ + t;
           const int qr = (p.pair_rows ? qt * NQ + t : qt) * kTileM;
+          if constexpr (k2) {  // both CTAs' Q tiles complete on the leader's barrier
+            if (crank == 0) mbar_arrive_expect_tx(&q_full[t], 2 * C::kQBytes);
+            const uint32_t bar = mapa_shared(smem_u32(&q_full[t]), 0);
 #pragma unroll
-          for (int sb = 0; sb < C::kSub; ++sb)
-            tma_load_4d(sQ + t * C::kQBytes + sb * C::kSubBytes, &p.tm_q, &q_full[t], sb * 64, qh, qr, b);
+            for (int sb = 0; sb < C::kSub; ++sb)
+              tma_load_4d_2sm(sQ + t * C::kQBytes + sb * C::kSubBytes, &p.tm_q, bar, sb * 64, qh, qr, b);
+          } else {
+            mbar_arrive_expect_tx(&q_full[t], C::kQBytes);
+#pragma unroll
+            for (int sb = 0; sb < C::kSub; ++sb)
+              tma_load_4d(sQ + t * C::kQBytes + sb * C::kSubBytes, &p.tm_q, &q_full[t], sb * 64, qh, qr, b);
+          }
         }
         const int kvh = (p.pair_rows ? hp : hp * NQ) / group;
         for (int j = 0; j < n; ++j) {
@@ -531,8 +568,22 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
             const uint32_t slot = kv_it % NS;
             mbar_wait(&kv_empty[slot], ((kv_it / NS) & 1) ^ 1);
             ++kv_it;
-            mbar_arrive_expect_tx(&kv_full[slot], C::kKVBytes);
             const CUtensorMap* tm = which == 0 ? &p.tm_k : &p.tm_v;
+            if constexpr (k2) {
+              // my half (K: 64 key rows; V: 64 columns), completing on the leader's barrier
+              if (crank == 0) mbar_arrive_expect_tx(&kv_full[slot], C::kKVBytes);
+              const uint32_t bar = mapa_shared(smem_u32(&kv_full[slot]), 0);
+              if (which == 0) {
+#pragma unroll
+                for (int sb = 0; sb < C::kSub; ++sb)
+                  tma_load_4d_2sm(sKV + slot * C::kKVBytes + sb * (C::kSubBytes / 2), &p.tm_k64, bar, sb * 64, kvh,
+                                  kt * kTileN + 64 * int(crank), b);
+              } else {
+                tma_load_4d_2sm(sKV + slot * C::kKVBytes, &p.tm_v, bar, 64 * int(crank), kvh, kt * kTileN, b);
+              }
+              continue;
+            }
+            mbar_arrive_expect_tx(&kv_full[slot], C::kKVBytes);
             if constexpr (MC) {  // my half of the tile, to both CTAs
               tma_load_4d_mc(sKV + slot * C::kKVBytes + crank * C::kSubBytes, tm, &kv_full[slot], int(crank) * 64,
                              kvh, kt * kTileN, b, uint16_t(0x3));
@@ -561,16 +612,28 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
     // issues, and its commits track only its own MMAs.
     const bool s_role = warp == C::kMmaWarp;
     {
-      constexpr uint32_t kIdescQK = idesc_bf16_f32(128, 128, 0, 0);
-      constexpr uint32_t kIdescPV = idesc_bf16_f32(128, HS, 0, 1);
+      constexpr uint32_t kIdescQK = idesc_bf16_f32(k2 ? 256 : 128, 128, 0, 0);
+      constexpr uint32_t kIdescPV = idesc_bf16_f32(k2 ? 256 : 128, HS, 0, 1);
       const uint32_t sq = smem_u32(sQ), skv = smem_u32(sKV);
       uint32_t kv_it = 0, q_phase = 0, f_phase = 0;
       uint32_t p_phase[NQ];
 #pragma unroll
       for (int t = 0; t < NQ; ++t) p_phase[t] = 0;
       auto wait_full = [&](uint32_t idx) {
-        mbar_wait(&kv_full[idx % NS], (idx / NS) & 1);
+        if constexpr (k2)
+          mbar_wait_cluster(&kv_full[idx % NS], (idx / NS) & 1);
+        else
+          mbar_wait(&kv_full[idx % NS], (idx / NS) & 1);
         tc_fence_after();
+      };
+      // commit to this CTA's barrier, or (2SM) to the same barrier of both CTAs
+      auto commit = [&](uint64_t* bar) {
+        if constexpr (k2) {
+          if (elect_one()) mma2_commit_mc(bar, uint16_t(0x3));
+          __syncwarp();
+        } else {
+          commit_one(bar);
+        }
       };
       // Descriptor bases (16-byte units in the low bits); the batched
       // chains add the per-k-step offsets in PTX. Every MMA operand is a
@@ -585,7 +648,9 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
           const uint64_t ad = q_desc0 + static_cast<uint64_t>((t * C::kQBytes) >> 4);
           const uint64_t bd = kv_desc0 + static_cast<uint64_t>((sl * C::kKVBytes) >> 4);
           if (elect_one()) {
-            if constexpr (HS == 128)
+            if constexpr (k2)
+              mma2_qk_hs128(C::kSCol, ad, bd, kIdescQK, 0u);
+            else if constexpr (HS == 128)
               mma_qk_hs128(C::kSCol, ad, bd, kIdescQK, 0u);
             else
               mma_qk_hs64(C::kSCol, ad, bd, kIdescQK, 0u);
@@ -598,7 +663,9 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
           constexpr int sl = decltype(S)::value;
           const uint64_t bd = v_desc0 + static_cast<uint64_t>((sl * C::kKVBytes) >> 4);
           if (elect_one()) {
-            if (acc)
+            if constexpr (k2)
+              mma2_pv_chain(C::kOCol + t * HS, C::kPCol + t * 64, bd, kIdescPV, acc ? 1u : 0u);
+            else if (acc)
               mma_pv_chain(C::kOCol + t * HS, C::kPCol + t * 64, bd, kIdescPV, 1u);
             else
               mma_pv_chain(C::kOCol + t * HS, C::kPCol + t * 64, bd, kIdescPV, 0u);
@@ -611,6 +678,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
       for (uint32_t it = 0;; ++it) {
         const int u = next_unit(sched_full, sched_empty, sched_slot, it, true);
         if (u >= p.num_units) break;
+        if (k2 && crank != 0) continue;  // 2SM: the leader issues every MMA of the pair
         const int qt = p.units[u] & 0xFFFF;
         const int n = p.tile_off[qt + 1] - p.tile_off[qt];
         if (n == 0) continue;
@@ -618,7 +686,12 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
           // S_t(j) in (j, t) order; each needs the shared S buffer (the
           // previous S loaded into registers by its softmax) and K_j.
 #pragma unroll
-          for (int t = 0; t < NQ; ++t) mbar_wait(&q_full[t], q_phase & 1);
+          for (int t = 0; t < NQ; ++t) {
+            if constexpr (k2)
+              mbar_wait_cluster(&q_full[t], q_phase & 1);
+            else
+              mbar_wait(&q_full[t], q_phase & 1);
+          }
           ++q_phase;
           for (int j = 0; j < n; ++j) {
             const uint32_t ki = kv_it + 2 * j;
@@ -626,22 +699,25 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
 #pragma unroll
             for (int t = 0; t < NQ; ++t) {
               if (s_count > 0) {
-                mbar_wait(s_free, f_phase & 1);
+                if constexpr (k2)
+                  mbar_wait_cluster(s_free, f_phase & 1);
+                else
+                  mbar_wait(s_free, f_phase & 1);
                 ++f_phase;
               }
               tc_fence_after();
               issue_qk(t, ki % NS);
-              commit_one(&s_full[t]);
+              commit(&s_full[t]);
               if (lane == 0) trace_ev(p, 11 + 2 * t, j);
               ++s_count;
             }
-            if constexpr (MC) {
+            if constexpr (MC == 1) {
               if (elect_one()) mma_commit_mc(&kv_empty[ki % NS], uint16_t(0x3));
               __syncwarp();
             } else {
-              commit_one(&kv_empty[ki % NS]);
+              commit(&kv_empty[ki % NS]);
             }
-            if (j == n - 1) commit_one(q_empty);
+            if (j == n - 1) commit(q_empty);
           }
         } else {
           // PV_t(j) in (j, t) order; each needs P_t(j) and V_j.
@@ -650,18 +726,21 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
             wait_full(vi);
 #pragma unroll
             for (int t = 0; t < NQ; ++t) {
-              mbar_wait(&p_ready[t], p_phase[t] & 1);
+              if constexpr (k2)
+                mbar_wait_cluster(&p_ready[t], p_phase[t] & 1);
+              else
+                mbar_wait(&p_ready[t], p_phase[t] & 1);
               if (lane == 0) trace_ev(p, 10 + 2 * t, p_phase[t]);
               ++p_phase[t];
               tc_fence_after();
               issue_pv(t, vi % NS, j > 0);
-              commit_one(&pv_done[t]);
+              commit(&pv_done[t]);
             }
-            if constexpr (MC) {
+            if constexpr (MC == 1) {
               if (elect_one()) mma_commit_mc(&kv_empty[vi % NS], uint16_t(0x3));
               __syncwarp();
             } else {
-              commit_one(&kv_empty[vi % NS]);
+              commit(&kv_empty[vi % NS]);
             }
           }
         }
@@ -683,7 +762,12 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
   __syncthreads();
   if constexpr (MC) cluster_sync();  // no remote ticket / barrier traffic may target an exited CTA
   tc_fence_after();
-  if (warp == C::kMmaWarp) tmem_dealloc(tmem, C::kTmemCols);
+  if (warp == C::kMmaWarp) {
+    if constexpr (k2)
+      tmem_dealloc_2sm(tmem, C::kTmemCols);
+    else
+      tmem_dealloc(tmem, C::kTmemCols);
+  }
 }
 
 // --------------------------------------------------------------- launchers
@@ -694,7 +778,7 @@ static cudaError_t launch_impl(const FwdParams& p, int grid, cudaStream_t stream
   static std::atomic<uint64_t> attr_done{0};  // per instantiation and device
   const cudaError_t e = ensure_smem_attr(kern, C::kSmemBytes, attr_done);
   if (e != cudaSuccess) return e;
-  if constexpr (MC) {
+  if constexpr (MC > 0) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(grid & ~1), 1, 1);
     cfg.blockDim = dim3(C::kThreads, 1, 1);
@@ -739,6 +823,7 @@ static cudaError_t launch_variant(const FwdParams& p, int grid, cudaStream_t str
 cudaError_t launch_fa_fwd(const FwdParams& p, int nq, int hs, int grid, cudaStream_t stream) {
   if (p.cluster) {
     if (nq != 2 || hs != 128 || p.pair_rows) return cudaErrorInvalidValue;
+    if (p.cluster == 2) return launch_impl<2, 128, 0, 1, 2>(p, grid, stream);
     return launch_impl<2, 128, 0, 1, 1>(p, grid, stream);
   }
   if (nq == 2 && hs == 128) return launch_variant<2, 128>(p, grid, stream);

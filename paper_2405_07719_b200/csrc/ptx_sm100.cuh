@@ -161,6 +161,16 @@ __device__ __forceinline__ void tma_load_4d_mc(void* dst, const void* tmap, uint
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "h"(mask)
       : "memory");
 }
+// A CTA pair's load: data into this CTA's shared memory, completion signalled
+// on the barrier at `mbar_cluster` (a shared::cluster address, the leader's).
+__device__ __forceinline__ void tma_load_4d_2sm(void* dst, const void* tmap, uint32_t mbar_cluster, int c0, int c1,
+                                                int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(mbar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_4d_hint(void* dst, const void* tmap, uint64_t* bar, int c0,
                                                  int c1, int c2, int c3, uint64_t policy) {
   asm volatile(
@@ -189,6 +199,16 @@ __device__ __forceinline__ void tmem_alloc(uint32_t* dst, uint32_t ncols) {
                "r"(ncols)
                : "memory");
   asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+// cta_group::2: the same warp of both CTAs of a pair allocates; the two
+// allocations are at the same TMEM address.
+__device__ __forceinline__ void tmem_alloc_2sm(uint32_t* dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)), "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_2sm(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
 }
 __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
@@ -268,6 +288,69 @@ __device__ __forceinline__ void mma_qk_hs64(uint32_t d_tmem, uint64_t a_desc, ui
       ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// cta_group::2 (M = 256 over a CTA pair): S = Q K^T with each CTA's own
+// 128 Q rows (A, 16 KB column blocks) and ITS HALF of the K tile (B: 64 key
+// rows, 8 KB column blocks); issued by the leader CTA only.
+__device__ __forceinline__ void mma2_qk_hs128(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p0, p1;\n\t.reg .b64 ra, rb;\n\t"
+      "setp.ne.b32 p0, %4, 0;\n\t"
+      "setp.eq.u32 p1, 1, 1;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p0;\n\t"
+      "add.s64 ra, %1, 2;\n\tadd.s64 rb, %2, 2;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 4;\n\tadd.s64 rb, %2, 4;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 6;\n\tadd.s64 rb, %2, 6;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 1024;\n\tadd.s64 rb, %2, 512;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 1026;\n\tadd.s64 rb, %2, 514;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 1028;\n\tadd.s64 rb, %2, 516;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 1030;\n\tadd.s64 rb, %2, 518;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "}"
+      ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// O += P V over a CTA pair: P from each CTA's TMEM, V's 64-column half of
+// each CTA (B, N split across the pair); leader only.
+__device__ __forceinline__ void mma2_pv_chain(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p0, p1;\n\t.reg .b64 rb;\n\t.reg .b32 ta;\n\t"
+      "setp.ne.b32 p0, %4, 0;\n\t"
+      "setp.eq.u32 p1, 1, 1;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p0;\n\t"
+      "add.u32 ta, %1, 8;\n\tadd.s64 rb, %2, 128;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [ta], rb, %3, p1;\n\t"
+      "add.u32 ta, %1, 16;\n\tadd.s64 rb, %2, 256;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [ta], rb, %3, p1;\n\t"
+      "add.u32 ta, %1, 24;\n\tadd.s64 rb, %2, 384;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [ta], rb, %3, p1;\n\t"
+      "add.u32 ta, %1, 32;\n\tadd.s64 rb, %2, 512;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [ta], rb, %3, p1;\n\t"
+      "add.u32 ta, %1, 40;\n\tadd.s64 rb, %2, 640;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [ta], rb, %3, p1;\n\t"
+      "add.u32 ta, %1, 48;\n\tadd.s64 rb, %2, 768;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [ta], rb, %3, p1;\n\t"
+      "add.u32 ta, %1, 56;\n\tadd.s64 rb, %2, 896;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [ta], rb, %3, p1;\n\t"
+      "}"
+      ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
 // O[128 x N] (+)= P[128 x 128] V[128 x N]: P (bf16) from TMEM, 8 columns per
 // 16-key step; V MN-major, 16 rows (2 KB) per step.
 __device__ __forceinline__ void mma_pv_chain(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
