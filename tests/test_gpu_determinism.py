@@ -1,0 +1,43 @@
+"""Repeated runs are bit-identical (no races in the persistent kernels'
+dynamic unit tickets, the 2-CTA cluster ticket hand-off, the backward's
+chunk hand-offs or the ring's double buffers): every unit's arithmetic is
+independent of which CTA claims it. Longer runs: tools/stress.py."""
+import pytest
+import torch
+
+from paper_2405_07719_b200 import ProcessMesh, UspAttention
+from tests.usp_harness import UspCase, run_usp_gpu_fwd_bwd
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("L,hc,kv,hs", [(2048, 32, 8, 128), (2048, 8, 8, 64), (1500, 12, 4, 128)])
+def test_single_rank_bitwise_repeatable(cuda, L, hc, kv, hs):
+    eng = UspAttention(ProcessMesh(1, 1), rank=0, seq_len=L, heads=hc, kv_heads=kv, head_size=hs, causal=True)
+    g = torch.Generator(device=cuda).manual_seed(L)
+    q = torch.randn(eng.q_shape(), device=cuda, dtype=torch.bfloat16, generator=g)
+    k = torch.randn(eng.kv_shape(), device=cuda, dtype=torch.bfloat16, generator=g)
+    v = torch.randn(eng.kv_shape(), device=cuda, dtype=torch.bfloat16, generator=g)
+    do = torch.randn(eng.q_shape(), device=cuda, dtype=torch.bfloat16, generator=g)
+    f0 = eng.forward(q, k, v)
+    o0, l0 = f0.out.clone(), f0.logsumexp.clone()
+    g0 = eng.backward(f0, do)
+    ref = [g0.dq.clone(), g0.dk.clone(), g0.dv.clone()]
+    for _ in range(40):
+        f = eng.forward(q, k, v)
+        gr = eng.backward(f, do)
+        assert torch.equal(f.out, o0) and torch.equal(f.logsumexp, l0)
+        assert all(torch.equal(a, b) for a, b in zip((gr.dq, gr.dk, gr.dv), ref))
+
+
+def test_mesh_bitwise_repeatable(cuda):
+    c = UspCase(seq=2048, hc=32, kv_hc=8, hs=128, ulysses=2, ring=4, causal=True)
+    g = torch.Generator(device=cuda).manual_seed(5)
+    q = torch.randn(1, c.seq, c.hc, c.hs, device=cuda, dtype=torch.bfloat16, generator=g)
+    k = torch.randn(1, c.seq, c.kv_hc, c.hs, device=cuda, dtype=torch.bfloat16, generator=g)
+    v = torch.randn(1, c.seq, c.kv_hc, c.hs, device=cuda, dtype=torch.bfloat16, generator=g)
+    do = torch.randn(1, c.seq, c.hc, c.hs, device=cuda, dtype=torch.bfloat16, generator=g)
+    ref = [x.clone() for x in run_usp_gpu_fwd_bwd(c, q, k, v, do, cuda)[:4]]
+    for _ in range(10):
+        got = run_usp_gpu_fwd_bwd(c, q, k, v, do, cuda)[:4]
+        assert all(torch.equal(a, b) for a, b in zip(got, ref))
