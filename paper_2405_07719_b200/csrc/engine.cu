@@ -155,7 +155,9 @@ class Engine {
     hs_ = shape_.head_size;
     hsk_ = shape_.kernel_head_size();
     const int group = hl_ / kvl_;
-    tiling_ = fwd_tiling(hl_, kvl_, hsk_);
+    USPB_CHECK(cudaSetDevice(c.device));
+    USPB_CHECK(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, c.device));
+    tiling_ = fwd_tiling(hl_, kvl_, hsk_, Tr_, B_, num_sms_);
     nq_ = (tiling_.pair_rows || group % 2 == 0) ? 2 : 1;
     cluster_ = tiling_.cluster;  // 2-CTA clusters sharing K/V tiles by TMA multicast
     static const int cluster_mode = [] {  // 2: cta_group::2 MMAs on the same clusters (experimental)
@@ -164,8 +166,6 @@ class Engine {
     }();
     cluster_mode_ = cluster_ ? (cluster_mode == 2 ? 2 : 1) : 0;
 
-    USPB_CHECK(cudaSetDevice(c.device));
-    USPB_CHECK(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, c.device));
     if (tr_) groups_ = tr_->make_groups(c.rank, shape_.mesh.ulysses_group(c.rank),
                                         shape_.mesh.ring_group(c.rank));
 
@@ -1329,7 +1329,7 @@ usp_status usp_schedule(const usp_config* cfg, int32_t step, usp_step_info* out)
     const int R = s.mesh.ring;
     const int src = ring_source(r, step, R);
     const int kvl = s.local_kv_heads();
-    const FwdTiling tl = fwd_tiling(s.local_heads(), kvl, s.kernel_head_size());
+    const FwdTiling tl = fwd_tiling(s.local_heads(), kvl, s.kernel_head_size(), s.tokens_per_ring_rank(), s.batch);
     const auto st = plan_step(head_positions(s, cfg->rank),
                               head_positions(s, s.mesh.rank_of(u, src)), s.causal, s.batch,
                               tl.head_units, R == 1 || step == 0 || step == R - 1, tl.units_per_kv,

@@ -225,7 +225,7 @@ int64_t visible_pairs(const std::vector<int64_t>& q_pos, const std::vector<int64
   return pairs;
 }
 
-FwdTiling fwd_tiling(int hl, int kvl, int hsk) {
+FwdTiling fwd_tiling(int hl, int kvl, int hsk, int64_t q_rows, int64_t batch, int sms) {
   static const bool rows_ok = [] {
     const char* e = std::getenv("USP_FA_PAIR_ROWS");
     return !e || std::atoi(e) != 0;
@@ -237,7 +237,8 @@ FwdTiling fwd_tiling(int hl, int kvl, int hsk) {
   const int group = hl / kvl;
   if (group % 4 == 0 && hsk == 128 && cluster_ok) return {false, hl / 4, group / 4, kTileM, true};
   if (group % 2 == 0) return {false, hl / 2, group / 2, kTileM, false};
-  if (rows_ok) return {true, hl, group, 2 * kTileM, false};
+  const int64_t pair_units = (q_rows + 2 * kTileM - 1) / (2 * kTileM) * hl * batch;
+  if (rows_ok && pair_units >= sms) return {true, hl, group, 2 * kTileM, false};
   return {false, hl, group, kTileM, false};  // one q tile per CTA (development fallback)
 }
 

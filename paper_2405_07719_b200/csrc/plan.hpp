@@ -110,7 +110,10 @@ struct FwdTiling {
   int rows_per_unit; // 128 or 256
   bool cluster;      // 2-CTA clusters over head quads
 };
-FwdTiling fwd_tiling(int local_heads, int local_kv_heads, int kernel_head_size);
+// q_rows / batch / sms: a short sequence keeps 128-row units when pairing
+// rows would leave fewer units than SMs (measured faster below ~4K rows).
+FwdTiling fwd_tiling(int local_heads, int local_kv_heads, int kernel_head_size, int64_t q_rows = 1 << 30,
+                     int64_t batch = 1, int sms = 148);
 
 // The same block transposed for the dK/dV kernel: CSR over KEY tiles
 // (tile_list = q tile | partial << 31, same partial flags), units
