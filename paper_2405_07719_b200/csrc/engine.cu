@@ -740,7 +740,8 @@ class Engine {
     }
     record_a2a(4, q_part_);
     // delta = rowsum(dO * O) (output_dot_rows, attention.cpp:266-280)
-    USPB_CHECK(launch_bwd_delta(oh, doh, delta_.as<float>(), B_ * Tr_ * hl_, hsk_, st));
+    USPB_CHECK(launch_bwd_delta(oh, doh, delta_.as<float>(), B_, Tr_, hl_, hsk_, lse,
+                                bwd_steps_[0].dkdv.q_pos.as<int32_t>(), qvec_.as<float>(), st));
     ++launches_;
 
     // -- 2. ring backward
@@ -990,6 +991,7 @@ class Engine {
     const size_t kv_heads = size_t(B_) * Tr_ * kvl_ * hsk_;
     if (reshape) do_h_ = DevBuf(q_heads * 2);
     delta_ = DevBuf(size_t(B_) * Tr_ * hl_ * sizeof(float));
+    qvec_ = DevBuf(size_t(B_) * hl_ * ((Tr_ + kTileM - 1) / kTileM) * 384 * sizeof(float));
     dq_acc_ = DevBuf(q_heads * sizeof(float));
     own_dkv_ = DevBuf(2 * kv_heads * sizeof(float));
     if (R_ > 1) {
@@ -1032,6 +1034,8 @@ class Engine {
     p.tm_v = make_tmap(vb, hsk_, kvl_, Tr_, B_);
     p.lse = lse;
     p.delta = delta_.as<float>();
+    p.qvec = qvec_.as<float>();
+    p.n_q_tiles = static_cast<int>((Tr_ + kTileM - 1) / kTileM);
     p.dq = dq;
     p.dk = dk;
     p.dv = dv;
@@ -1191,7 +1195,7 @@ class Engine {
   DevBuf q_h_, kv0_, o_h_, send_, recv_, o_send_, o_recv_, o_acc_, lse_acc_;
   DevBuf kv_ring_[2];
   // backward (allocated by the first usp_attn_bwd)
-  DevBuf do_h_, delta_, dq_acc_, own_dkv_, grad_h_, grad_recv_;
+  DevBuf do_h_, delta_, qvec_, dq_acc_, own_dkv_, grad_h_, grad_recv_;
   DevBuf acc_dkv_[2];
   std::vector<BwdStep> bwd_steps_;
   // usp_attn_fwd_host staging and its chunk pipeline

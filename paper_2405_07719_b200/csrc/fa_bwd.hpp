@@ -29,6 +29,12 @@ struct BwdParams {
   const int32_t* q_pos;      // effective positions (see StepPlan), padded to 128
   const int32_t* k_pos;
   int* sched;                // unit tickets, zero between launches
+  // dK/dV kernel: per (batch, q head, 128-row q tile) the 3 x 128 floats
+  // {lse * log2(e) (INF on padding rows), delta, q position} laid out
+  // contiguously ([b][h][q tile][3][128], filled by launch_bwd_delta) so the
+  // TMA warp bulk-copies them next to the Q tile
+  const float* qvec;
+  int n_q_tiles;  // q tiles per (batch, head) in qvec
 
   int num_units;
   int batch, q_len, k_len, heads, kv_heads;
@@ -40,7 +46,11 @@ struct BwdParams {
 cudaError_t launch_bwd_dq(const BwdParams& p, int hs, int grid, cudaStream_t stream);
 cudaError_t launch_bwd_dkdv(const BwdParams& p, int hs, int grid, cudaStream_t stream);
 // delta[row] = sum_s o[row][s] * dout[row][s]  (output_dot_rows, attention.cpp:266-280)
-cudaError_t launch_bwd_delta(const void* o, const void* dout, float* delta, int64_t rows, int hs,
+// over rows (b, t, h) of a (batch, q_len, heads, hs) tensor; with qvec also
+// the dK/dV kernel's per-q-tile vectors (see BwdParams::qvec) from lse and
+// the effective q positions (padded to whole tiles).
+cudaError_t launch_bwd_delta(const void* o, const void* dout, float* delta, int64_t batch, int64_t q_len,
+                             int heads, int hs, const float* lse, const int32_t* q_pos, float* qvec,
                              cudaStream_t stream);
 // dst = bf16(src [+ src2]), rows of hs_src -> hs_dst (drops padding);
 // the sum is (src + src2) in that order (ring_attention.cpp:145-150).

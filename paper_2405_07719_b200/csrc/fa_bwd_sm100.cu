@@ -78,7 +78,8 @@ struct BwdCfg {
   static constexpr int kStages = (kBudget - 2 * kTileBytes) / kTileBytes > USPB_DKDV_STAGES
                                      ? USPB_DKDV_STAGES
                                      : (kBudget - 2 * kTileBytes) / kTileBytes;
-  static constexpr int kSmemBytes = 1024 + 2 * kTileBytes + kStages * kTileBytes + 4096;
+  static constexpr int kVecBytes = 3 * 128 * 4;  // lse2 | delta | q position of one q tile
+  static constexpr int kSmemBytes = 1024 + 2 * kTileBytes + kStages * kTileBytes + 2048 + kStages * kVecBytes;
   // dq kernel: K tiles in a 3-slot ring (released after the tile's dQ MMAs),
   // V tiles in a 2-slot ring (released as soon as dP has been computed)
   static constexpr int kKSlots = USPB_DQ_KSLOTS, kVSlots = 2;
@@ -452,8 +453,10 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
   int* unit_slot = reinterpret_cast<int*>(tmem_slot + 2);
   uint64_t* u_full = reinterpret_cast<uint64_t*>(unit_slot + 2);
   uint64_t* u_empty = u_full + 1;
-  // [2 parity][lse2 128 | delta 128 | qpos 128], addressed in the shared window
-  const uint32_t vec_s = (smem_u32(u_empty + 1) + 15u) & ~15u;  // 16-byte aligned for ld.shared.v4
+  // [NS slots][lse2 128 | delta 128 | qpos 128]: the vector of the q tile whose
+  // Q sits in ring slot s, bulk-copied by the TMA warp with that Q tile
+  uint8_t* vec = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(u_empty + 1) + 15u) & ~uintptr_t(15));
+  const uint32_t vec_s = smem_u32(vec);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -512,33 +515,13 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
       // loads are issued one q tile ahead, so the L2 latency hides behind
       // the previous tile's MMAs and elementwise work.
       const int total = group * n;
-      auto fetch = [&](int i, float& fl, float& fd, int& fq) {
-        const int h = kvh * group + i / n;
-        const int qt = p.tile_list[beg + i % n] & 0x7FFFFFFF;
-        const int qr = qt * 128 + key_in_tile;
-        const bool ok = qr < p.q_len;
-        const size_t r = (static_cast<size_t>(b) * p.q_len + (ok ? qr : 0)) * p.heads + h;
-        if (hf == 0) {
-          fl = ok ? p.lse[r] * 1.4426950408889634f : INFINITY;  // padding rows: p = 0
-          fd = ok ? p.delta[r] : 0.f;
-        } else {
-          fq = p.q_pos[qr];
-        }
-      };
-      float nl = 0.f, nd = 0.f;
-      int nq = 0;
-      if (total > 0) fetch(0, nl, nd, nq);
       for (int i = 0; i < total; ++i, ++g) {
         const int entry = p.tile_list[beg + i % n];
-        const uint32_t vb = vec_s + (g & 1) * (384 * 4);
-        if (hf == 0) {
-          sts_f32(vb + key_in_tile * 4, nl);
-          sts_f32(vb + (128 + key_in_tile) * 4, nd);
-        } else {
-          sts_f32(vb + (256 + key_in_tile) * 4, __int_as_float(nq));
-        }
-        if (i + 1 < total) fetch(i + 1, nl, nd, nq);
-        bwd_bar_sync(1, 32 * C::kCompute);
+        // this q tile's lse2 / delta / positions came with its Q tile (ring
+        // slot 2g % NS; the slot is not refilled before this tile's dK MMAs)
+        const uint32_t qslot = (2 * g) % NS;
+        mbar_wait(&qd_full[qslot], ((2 * g) / NS) & 1);
+        const uint32_t vb = vec_s + qslot * C::kVecBytes;
         // phase 1: P^T = exp(S^T - lse) (thread = key row), packed over the
         // consumed S^T columns for the dV MMAs; fp32 P kept for phase 2
         mbar_wait(s_full, g & 1);
@@ -648,7 +631,11 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
               const uint32_t slot = qd_it % NS;
               mbar_wait(&qd_empty[slot], ((qd_it / NS) & 1) ^ 1);
               ++qd_it;
-              mbar_arrive_expect_tx(&qd_full[slot], C::kTileBytes);
+              mbar_arrive_expect_tx(&qd_full[slot], C::kTileBytes + (which == 0 ? C::kVecBytes : 0));
+              if (which == 0)
+                bulk_g2s(vec + slot * C::kVecBytes,
+                         p.qvec + ((static_cast<size_t>(b) * p.heads + h) * p.n_q_tiles + qt) * 384, C::kVecBytes,
+                         &qd_full[slot]);
               const CUtensorMap* tm = which == 0 ? &p.tm_q : &p.tm_do;
               for (int sb = 0; sb < C::kSub; ++sb)
                 tma_load_4d(sQD + slot * C::kTileBytes + sb * C::kSubBytes, tm, &qd_full[slot], sb * 64, h,
@@ -758,23 +745,39 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
 }
 
 // ============================================================ small kernels
-__global__ void delta_kernel(const uint16_t* o, const uint16_t* dout, float* delta,
-                             int64_t rows, int hs) {
-  // one warp per row: 16-byte loads, fp32 dot, shuffle reduction
+__global__ void delta_kernel(const uint16_t* o, const uint16_t* dout, float* delta, int64_t batch, int64_t q_len,
+                             int heads, int hs, int64_t n_qt, const float* lse, const int32_t* q_pos, float* qvec) {
+  // one warp per row (b, t, h) over the padded rows t < n_qt * 128: 16-byte
+  // loads, fp32 dot, shuffle reduction
   const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x & 31;
-  if (row >= rows) return;
-  const uint16_t* a = o + row * hs;
-  const uint16_t* bq = dout + row * hs;
+  const int64_t t_pad = n_qt * 128;
+  if (row >= batch * t_pad * heads) return;
+  const int h = static_cast<int>(row % heads);
+  const int64_t t = (row / heads) % t_pad, b = row / (heads * t_pad);
+  const bool valid = t < q_len;
   float acc = 0.f;
-  for (int e = lane * 2; e < hs; e += 64) {
-    const uint32_t x = *reinterpret_cast<const uint32_t*>(a + e);
-    const uint32_t y = *reinterpret_cast<const uint32_t*>(bq + e);
-    acc = fmaf(__uint_as_float(x << 16), __uint_as_float(y << 16), acc);
-    acc = fmaf(__uint_as_float(x & 0xFFFF0000u), __uint_as_float(y & 0xFFFF0000u), acc);
+  const int64_t r = (b * q_len + (valid ? t : 0)) * heads + h;
+  if (valid) {
+    const uint16_t* a = o + r * hs;
+    const uint16_t* bq = dout + r * hs;
+    for (int e = lane * 2; e < hs; e += 64) {
+      const uint32_t x = *reinterpret_cast<const uint32_t*>(a + e);
+      const uint32_t y = *reinterpret_cast<const uint32_t*>(bq + e);
+      acc = fmaf(__uint_as_float(x << 16), __uint_as_float(y << 16), acc);
+      acc = fmaf(__uint_as_float(x & 0xFFFF0000u), __uint_as_float(y & 0xFFFF0000u), acc);
+    }
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
   }
-  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if (lane == 0) delta[row] = acc;
+  if (lane == 0) {
+    if (valid) delta[r] = acc;
+    if (qvec) {
+      float* v = qvec + ((b * heads + h) * n_qt + t / 128) * 384 + (t % 128);
+      v[0] = valid ? lse[r] * 1.4426950408889634f : INFINITY;  // padding rows: p = 0
+      v[128] = valid ? acc : 0.f;
+      v[256] = __int_as_float(q_pos[t]);
+    }
+  }
 }
 
 __global__ void cast_rows_kernel(const float* src, const float* src2, uint16_t* dst, int64_t rows, int hs_src,
@@ -828,13 +831,16 @@ cudaError_t launch_bwd_dkdv(const BwdParams& p, int hs, int grid, cudaStream_t s
   return cudaGetLastError();
 }
 
-cudaError_t launch_bwd_delta(const void* o, const void* dout, float* delta, int64_t rows, int hs,
+cudaError_t launch_bwd_delta(const void* o, const void* dout, float* delta, int64_t batch, int64_t q_len,
+                             int heads, int hs, const float* lse, const int32_t* q_pos, float* qvec,
                              cudaStream_t stream) {
+  const int64_t n_qt = (q_len + 127) / 128;
+  const int64_t rows = batch * n_qt * 128 * heads;
   if (rows == 0) return cudaSuccess;
   const int64_t threads = rows * 32;
   const int grid = static_cast<int>((threads + 255) / 256);
-  delta_kernel<<<grid, 256, 0, stream>>>(static_cast<const uint16_t*>(o),
-                                         static_cast<const uint16_t*>(dout), delta, rows, hs);
+  delta_kernel<<<grid, 256, 0, stream>>>(static_cast<const uint16_t*>(o), static_cast<const uint16_t*>(dout), delta,
+                                         batch, q_len, heads, hs, n_qt, lse, q_pos, qvec);
   return cudaGetLastError();
 }
 

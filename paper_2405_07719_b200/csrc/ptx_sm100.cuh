@@ -151,6 +151,13 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const void* tmap, uint64_
       "r"(c3)
       : "memory");
 }
+// Plain bulk copy global -> shared (16-byte multiple), completion on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 // The same load multicast to every CTA of the cluster in `mask`: data and
 // complete_tx land at the same shared-memory offsets in each of them.
 __device__ __forceinline__ void tma_load_4d_mc(void* dst, const void* tmap, uint64_t* bar, int c0, int c1, int c2,
