@@ -1008,6 +1008,11 @@ class Engine {
       grad_recv_ = DevBuf(U_ * (q_part_ + 2 * kv_part_));
     }
     const int group = hl_ / kvl_;
+    static const bool bwd_cluster_env = [] {
+      const char* e = std::getenv("USP_BWD_CLUSTER");
+      return !e || std::atoi(e) != 0;
+    }();
+    bwd_cluster_ = bwd_cluster_env && hsk_ == 128 && group % 2 == 0;
     const auto my_pos = head_positions(shape_, cfg_.rank);
     for (int t = 0; t < R_; ++t) {
       const int src = ring_source(r_, t, R_);
@@ -1017,7 +1022,10 @@ class Engine {
       StepPlan fq = plan_step(my_pos, k_pos, shape_.causal, B_, hl_, t == 0, group);
       // dK/dV: t = 0 (own) and t = 1 (new partial) write every key row
       upload_plan(bs.dkdv, transpose_plan(fq, B_, kvl_, t <= 1));
-      upload_plan(bs.dq, std::move(fq));
+      if (bwd_cluster_)  // dQ over head pairs (2-CTA clusters sharing K/V by multicast)
+        upload_plan(bs.dq, plan_step(my_pos, k_pos, shape_.causal, B_, hl_ / 2, t == 0, group / 2));
+      else
+        upload_plan(bs.dq, std::move(fq));
       bwd_steps_.push_back(std::move(bs));
     }
   }
@@ -1054,9 +1062,10 @@ class Engine {
     p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(double(hs_)));
     p.inv_scale = static_cast<float>(1.0 / std::sqrt(double(hs_)));
     p.accumulate = accumulate ? 1 : 0;
+    p.cluster = (is_dq && bwd_cluster_) ? 1 : 0;
     const int reserve = (R_ > 1 && tr_) ? tr_->reserved_sms() : 0;
     const int slots = std::max(1, num_sms_ - reserve);
-    const int grid = std::min(p.num_units, slots);
+    const int grid = p.cluster ? std::max(2, std::min(2 * p.num_units, slots) & ~1) : std::min(p.num_units, slots);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (timing_) {
       e0 = timing_event(2 * timed_.size());
@@ -1188,6 +1197,7 @@ class Engine {
   int U_ = 1, R_ = 1, u_ = 0, r_ = 0, H_ = 0, KV_ = 0, hl_ = 0, kvl_ = 0, hs_ = 0, hsk_ = 0, nq_ = 1;
   FwdTiling tiling_{};
   bool cluster_ = false;
+  bool bwd_cluster_ = false;
   int cluster_mode_ = 0;
   int64_t B_ = 1, T_ = 0, Tr_ = 0;
   int num_sms_ = 148;

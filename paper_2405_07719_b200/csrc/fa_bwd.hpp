@@ -35,6 +35,7 @@ struct BwdParams {
   // TMA warp bulk-copies them next to the Q tile
   const float* qvec;
   int n_q_tiles;  // q tiles per (batch, head) in qvec
+  int cluster;    // dq kernel: 1 = 2-CTA clusters over head pairs (unit head field = pair)
 
   int num_units;
   int batch, q_len, k_len, heads, kv_heads;

@@ -145,9 +145,13 @@ __device__ __forceinline__ void store_rows(uint32_t lane_base, uint32_t col, boo
 // of the S buffer it came from (packed_col). S(j+1) goes to the other S buffer
 // while tile j's elementwise work runs; dQ k-steps are issued per 32-key
 // chunk as soon as that chunk's dS is in TMEM.
-template <int HS>
+// MC = 1: a 2-CTA cluster runs the two q heads of a head pair (same kv
+// head) over the same q tile; each CTA loads one 64-column half of every
+// K / V tile and multicasts it to both (unit hp field = head pair).
+template <int HS, int MC>
 __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(const __grid_constant__ BwdParams p) {
   using C = BwdCfg<HS>;
+  static_assert(!MC || HS == 128, "cluster mode needs two 64-column halves");
   constexpr int NK = C::kKSlots, NV = C::kVSlots;
   constexpr uint32_t kDP = 128, kDQ = 256, kS1 = 384;
   extern __shared__ uint8_t smem_raw[];
@@ -187,30 +191,44 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
     for (int c = 0; c < 8; ++c) mbar_init(&chunk_ready[c], 128);
     mbar_init(dq_full, 1);
     mbar_init(u_full, 1);
-    mbar_init(u_empty, C::kCompute + 1);
+    // compute warps + MMA warp (of both CTAs, + the peer's TMA warp, with MC)
+    mbar_init(u_empty, MC ? 2 * (C::kCompute + 1) + 1 : C::kCompute + 1);
     for (int s = 0; s < NK; ++s) {
       mbar_init(&k_full[s], 1);
-      mbar_init(&k_empty[s], 1);
+      mbar_init(&k_empty[s], MC ? 2 : 1);
     }
     for (int s = 0; s < NV; ++s) {
       mbar_init(&v_full[s], 1);
-      mbar_init(&v_empty[s], 1);
+      mbar_init(&v_empty[s], MC ? 2 : 1);
     }
     fence_barrier_init();
   }
   if (warp == C::kMmaWarp) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
+  if constexpr (MC) cluster_sync();  // the peer's barriers exist before any remote arrive
   tc_fence_after();
+  const uint32_t crank = MC ? cluster_ctarank() : 0u;
+  auto unit_head = [&](uint32_t unit) {
+    return MC ? int((unit >> 16) & 0xFF) * 2 + int(crank) : int((unit >> 16) & 0xFF);
+  };
   const uint32_t tmem = *tmem_slot;
   if (tmem != 0) __trap();
   const int group = p.heads / p.kv_heads;
 
   auto get_unit = [&](uint32_t it) {
-    mbar_wait(u_full, it & 1);
+    if constexpr (MC)
+      mbar_wait_cluster(u_full, it & 1);
+    else
+      mbar_wait(u_full, it & 1);
     const int u = *reinterpret_cast<volatile int*>(unit_slot);
     __syncwarp();
-    if (lane == 0) mbar_arrive(u_empty);
+    if (lane == 0) {
+      if constexpr (MC)
+        mbar_arrive_cluster(mapa_shared(smem_u32(u_empty), 0));  // the leader's slot
+      else
+        mbar_arrive(u_empty);
+    }
     return u;
   };
 
@@ -227,7 +245,7 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
       const int u = get_unit(it);
       if (u >= p.num_units) break;
       const uint32_t unit = p.units[u];
-      const int qt = unit & 0xFFFF, h = (unit >> 16) & 0xFF, b = unit >> 24;
+      const int qt = unit & 0xFFFF, h = unit_head(unit), b = unit >> 24;
       const int beg = p.tile_off[qt], n = p.tile_off[qt + 1] - beg;
       const int q_row = qt * 128 + row_in_tile;
       const bool valid = q_row < p.q_len;
@@ -298,13 +316,24 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
     if (lane == 0) {
       uint32_t kv_it = 0, q_it = 0;
       for (uint32_t it = 0;; ++it) {
-        const int u = atomicAdd(&p.sched[0], 1);
-        mbar_wait(u_empty, (it & 1) ^ 1);
-        *reinterpret_cast<volatile int*>(unit_slot) = u;
-        mbar_arrive(u_full);
+        int u;
+        if (!MC || crank == 0) {
+          u = atomicAdd(&p.sched[0], 1);
+          mbar_wait(u_empty, (it & 1) ^ 1);
+          *reinterpret_cast<volatile int*>(unit_slot) = u;
+          if constexpr (MC) {  // the same ticket to the peer CTA
+            st_cluster_u32(mapa_shared(smem_u32(unit_slot), 1), static_cast<uint32_t>(u));
+            mbar_arrive_cluster(mapa_shared(smem_u32(u_full), 1));
+          }
+          mbar_arrive(u_full);
+        } else {  // MC peer: take the leader's ticket
+          mbar_wait_cluster(u_full, it & 1);
+          u = *reinterpret_cast<volatile int*>(unit_slot);
+          mbar_arrive_cluster(mapa_shared(smem_u32(u_empty), 0));
+        }
         if (u >= p.num_units) break;
         const uint32_t unit = p.units[u];
-        const int qt = unit & 0xFFFF, h = (unit >> 16) & 0xFF, b = unit >> 24;
+        const int qt = unit & 0xFFFF, h = unit_head(unit), b = unit >> 24;
         const int beg = p.tile_off[qt], n = p.tile_off[qt + 1] - beg;
         if (n == 0) continue;
         mbar_wait(q_empty, (q_it & 1) ^ 1);
@@ -320,17 +349,27 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
           const uint32_t ks = kv_it % NK, vs = kv_it % NV;
           mbar_wait(&k_empty[ks], ((kv_it / NK) & 1) ^ 1);
           mbar_arrive_expect_tx(&k_full[ks], C::kTileBytes);
-          for (int sb = 0; sb < C::kSub; ++sb)
-            tma_load_4d(sK + ks * C::kTileBytes + sb * C::kSubBytes, &p.tm_k, &k_full[ks], sb * 64, kvh,
-                        kt * 128, b);
+          if constexpr (MC) {  // my half of the tile, to both CTAs
+            tma_load_4d_mc(sK + ks * C::kTileBytes + crank * C::kSubBytes, &p.tm_k, &k_full[ks], int(crank) * 64,
+                           kvh, kt * 128, b, uint16_t(0x3));
+          } else {
+            for (int sb = 0; sb < C::kSub; ++sb)
+              tma_load_4d(sK + ks * C::kTileBytes + sb * C::kSubBytes, &p.tm_k, &k_full[ks], sb * 64, kvh,
+                          kt * 128, b);
+          }
           mbar_wait(&v_empty[vs], ((kv_it / NV) & 1) ^ 1);
           mbar_arrive_expect_tx(&v_full[vs], C::kTileBytes);
-          for (int sb = 0; sb < C::kSub; ++sb)
-            tma_load_4d(sV + vs * C::kTileBytes + sb * C::kSubBytes, &p.tm_v, &v_full[vs], sb * 64, kvh,
-                        kt * 128, b);
+          if constexpr (MC) {
+            tma_load_4d_mc(sV + vs * C::kTileBytes + crank * C::kSubBytes, &p.tm_v, &v_full[vs], int(crank) * 64,
+                           kvh, kt * 128, b, uint16_t(0x3));
+          } else {
+            for (int sb = 0; sb < C::kSub; ++sb)
+              tma_load_4d(sV + vs * C::kTileBytes + sb * C::kSubBytes, &p.tm_v, &v_full[vs], sb * 64, kvh,
+                          kt * 128, b);
+          }
         }
       }
-      if (atomicAdd(&p.sched[1], 1) == static_cast<int>(gridDim.x) - 1) {
+      if (crank == 0 && atomicAdd(&p.sched[1], 1) == static_cast<int>(gridDim.x) / (MC ? 2 : 1) - 1) {
         p.sched[0] = 0;
         p.sched[1] = 0;
         __threadfence();
@@ -370,7 +409,12 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
       tc_fence_after();
       ss(kDP, do_desc, v_desc0, t % NV, VN{});
       bwd_commit(dp_full);
-      bwd_commit(&v_empty[t % NV]);
+      if constexpr (MC) {  // V(t) is free in both CTAs once both MMA warps used it
+        if (elect_one()) mma_commit_mc(&v_empty[t % NV], uint16_t(0x3));
+        __syncwarp();
+      } else {
+        bwd_commit(&v_empty[t % NV]);
+      }
     };
     for (uint32_t it = 0;; ++it) {
       const int u = get_unit(it);
@@ -412,7 +456,12 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
             __syncwarp();
           }
         });
-        bwd_commit(&k_empty[t % NK]);
+        if constexpr (MC) {
+          if (elect_one()) mma_commit_mc(&k_empty[t % NK], uint16_t(0x3));
+          __syncwarp();
+        } else {
+          bwd_commit(&k_empty[t % NK]);
+        }
       }
       bwd_commit(dq_full);
       kv_it += n;
@@ -420,6 +469,7 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (MC) cluster_sync();  // no remote traffic may target an exited CTA
   tc_fence_after();
   if (warp == C::kMmaWarp) tmem_dealloc(tmem, 512);
 }
@@ -797,21 +847,36 @@ __global__ void cast_rows_kernel(const float* src, const float* src2, uint16_t* 
 
 }  // namespace
 
-cudaError_t launch_bwd_dq(const BwdParams& p, int hs, int grid, cudaStream_t stream) {
-  if (hs == 128) {
-    static std::atomic<uint64_t> done{0};
-    const cudaError_t once = ensure_smem_attr(fa_bwd_dq_kernel<128>, BwdCfg<128>::kDqSmemBytes, done);
-    if (once != cudaSuccess) return once;
-    fa_bwd_dq_kernel<128><<<grid, BwdCfg<128>::kThreads, BwdCfg<128>::kDqSmemBytes, stream>>>(p);
-  } else if (hs == 64) {
-    static std::atomic<uint64_t> done{0};
-    const cudaError_t once = ensure_smem_attr(fa_bwd_dq_kernel<64>, BwdCfg<64>::kDqSmemBytes, done);
-    if (once != cudaSuccess) return once;
-    fa_bwd_dq_kernel<64><<<grid, BwdCfg<64>::kThreads, BwdCfg<64>::kDqSmemBytes, stream>>>(p);
-  } else {
-    return cudaErrorInvalidValue;
+template <int HS, int MC>
+static cudaError_t launch_dq_impl(const BwdParams& p, int grid, cudaStream_t stream) {
+  using C = BwdCfg<HS>;
+  auto kern = fa_bwd_dq_kernel<HS, MC>;
+  static std::atomic<uint64_t> done{0};
+  const cudaError_t once = ensure_smem_attr(kern, C::kDqSmemBytes, done);
+  if (once != cudaSuccess) return once;
+  if constexpr (MC) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid & ~1), 1, 1);
+    cfg.blockDim = dim3(C::kThreads, 1, 1);
+    cfg.dynamicSmemBytes = C::kDqSmemBytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, p);
   }
+  kern<<<grid, C::kThreads, C::kDqSmemBytes, stream>>>(p);
   return cudaGetLastError();
+}
+
+cudaError_t launch_bwd_dq(const BwdParams& p, int hs, int grid, cudaStream_t stream) {
+  if (hs == 128) return p.cluster ? launch_dq_impl<128, 1>(p, grid, stream) : launch_dq_impl<128, 0>(p, grid, stream);
+  if (hs == 64 && !p.cluster) return launch_dq_impl<64, 0>(p, grid, stream);
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_bwd_dkdv(const BwdParams& p, int hs, int grid, cudaStream_t stream) {
