@@ -253,8 +253,14 @@ def run_ours(a):
     mesh = ProcessMesh(U, R)
     comm = None
     if distributed:
-        comm = (Comm.p2p_from_torch_distributed(local) if a.transport == "p2p"
-                else Comm.from_torch_distributed(local))
+        if a.transport == "nccl":
+            try:
+                comm = Comm.from_torch_distributed(local)
+            except Exception as e:  # every rank fails the same init the same way
+                print(f"NCCL transport unavailable ({e}); using the peer-memory transport", file=sys.stderr)
+                a.transport = "p2p (nccl init failed)"
+        if comm is None:
+            comm = Comm.p2p_from_torch_distributed(local)
     causal = not a.non_causal
     eng = UspAttention(mesh, rank=rank, seq_len=a.seq_len, heads=a.heads, kv_heads=a.kv_heads,
                        head_size=a.head_size, causal=causal, device=local, comm=comm)
