@@ -1013,6 +1013,11 @@ class Engine {
       return !e || std::atoi(e) != 0;
     }();
     bwd_cluster_ = bwd_cluster_env && hsk_ == 128 && group % 2 == 0;
+    static const bool dkdv_cluster_env = [] {
+      const char* e = std::getenv("USP_BWD_DKDV_CLUSTER");
+      return !e || std::atoi(e) != 0;
+    }();
+    dkdv_cluster_ = dkdv_cluster_env && hsk_ == 128;
     const auto my_pos = head_positions(shape_, cfg_.rank);
     for (int t = 0; t < R_; ++t) {
       const int src = ring_source(r_, t, R_);
@@ -1021,7 +1026,9 @@ class Engine {
       // dQ: t = 0 writes every row (empties included), later steps accumulate
       StepPlan fq = plan_step(my_pos, k_pos, shape_.causal, B_, hl_, t == 0, group);
       // dK/dV: t = 0 (own) and t = 1 (new partial) write every key row
-      upload_plan(bs.dkdv, transpose_plan(fq, B_, kvl_, t <= 1));
+      // (over key-tile pairs when 2-CTA clusters share the Q / dO tiles)
+      upload_plan(bs.dkdv, dkdv_cluster_ ? transpose_plan_pairs(fq, B_, kvl_, t <= 1)
+                                         : transpose_plan(fq, B_, kvl_, t <= 1));
       if (bwd_cluster_)  // dQ over head pairs (2-CTA clusters sharing K/V by multicast)
         upload_plan(bs.dq, plan_step(my_pos, k_pos, shape_.causal, B_, hl_ / 2, t == 0, group / 2));
       else
@@ -1062,7 +1069,7 @@ class Engine {
     p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(double(hs_)));
     p.inv_scale = static_cast<float>(1.0 / std::sqrt(double(hs_)));
     p.accumulate = accumulate ? 1 : 0;
-    p.cluster = (is_dq && bwd_cluster_) ? 1 : 0;
+    p.cluster = (is_dq ? bwd_cluster_ : dkdv_cluster_) ? 1 : 0;
     const int reserve = (R_ > 1 && tr_) ? tr_->reserved_sms() : 0;
     const int slots = std::max(1, num_sms_ - reserve);
     const int grid = p.cluster ? std::max(2, std::min(2 * p.num_units, slots) & ~1) : std::min(p.num_units, slots);
@@ -1198,6 +1205,7 @@ class Engine {
   FwdTiling tiling_{};
   bool cluster_ = false;
   bool bwd_cluster_ = false;
+  bool dkdv_cluster_ = false;
   int cluster_mode_ = 0;
   int64_t B_ = 1, T_ = 0, Tr_ = 0;
   int num_sms_ = 148;

@@ -480,9 +480,16 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
 // Q / dO tiles stream through the slot ring; K, V stay resident per unit.
 // dV / dK k-steps are issued per 32-query chunk as soon as that chunk's
 // P^T / dS^T are in TMEM.
-template <int HS>
+// MC = 1: a 2-CTA cluster runs the two key tiles of a key-tile pair (units
+// and CSR over pairs, transpose_plan_pairs): both walk the same q-tile list
+// (the union of the two tiles'), each CTA TMA-loads one 64-column half of
+// every Q / dO tile multicast to both, and a slot is refilled once both MMA
+// warps released it (count-2 empty barriers, multicast commits). Halves the
+// L2 -> SM traffic of the streamed operands; K / V stay per CTA.
+template <int HS, int MC>
 __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(const __grid_constant__ BwdParams p) {
   using C = BwdCfg<HS>;
+  static_assert(!MC || HS == 128, "cluster mode needs two 64-column halves");
   constexpr int NS = C::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -520,26 +527,40 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
     }
     mbar_init(acc_full, 1);
     mbar_init(u_full, 1);
-    mbar_init(u_empty, C::kCompute + 1);
+    // compute warps + MMA warp (of both CTAs, + the peer's TMA warp, with MC)
+    mbar_init(u_empty, MC ? 2 * (C::kCompute + 1) + 1 : C::kCompute + 1);
     for (int s = 0; s < NS; ++s) {
       mbar_init(&qd_full[s], 1);
-      mbar_init(&qd_empty[s], 1);
+      mbar_init(&qd_empty[s], MC ? 2 : 1);
     }
     fence_barrier_init();
   }
   if (warp == C::kMmaWarp) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
+  if constexpr (MC) cluster_sync();  // the peer's barriers exist before any remote arrive
   tc_fence_after();
+  const uint32_t crank = MC ? cluster_ctarank() : 0u;
+  // CSR row of a unit (key tile, or key-tile pair with MC) and this CTA's key tile
+  auto unit_row = [](uint32_t unit) { return int(unit & 0xFFFF); };
+  auto unit_ktile = [&](uint32_t unit) { return MC ? int(unit & 0xFFFF) * 2 + int(crank) : int(unit & 0xFFFF); };
   const uint32_t tmem = *tmem_slot;
   if (tmem != 0) __trap();
   const int group = p.heads / p.kv_heads;
 
   auto get_unit = [&](uint32_t it) {
-    mbar_wait(u_full, it & 1);
+    if constexpr (MC)
+      mbar_wait_cluster(u_full, it & 1);
+    else
+      mbar_wait(u_full, it & 1);
     const int u = *reinterpret_cast<volatile int*>(unit_slot);
     __syncwarp();
-    if (lane == 0) mbar_arrive(u_empty);
+    if (lane == 0) {
+      if constexpr (MC)
+        mbar_arrive_cluster(mapa_shared(smem_u32(u_empty), 0));  // the leader's slot
+      else
+        mbar_arrive(u_empty);
+    }
     return u;
   };
 
@@ -556,8 +577,8 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
       const int u = get_unit(it);
       if (u >= p.num_units) break;
       const uint32_t unit = p.units[u];
-      const int kt = unit & 0xFFFF, kvh = (unit >> 16) & 0xFF, b = unit >> 24;
-      const int beg = p.tile_off[kt], n = p.tile_off[kt + 1] - beg;
+      const int kt = unit_ktile(unit), row = unit_row(unit), kvh = (unit >> 16) & 0xFF, b = unit >> 24;
+      const int beg = p.tile_off[row], n = p.tile_off[row + 1] - beg;
       const int k_row = kt * 128 + key_in_tile;
       const int kpos = p.k_pos[k_row];
       // Per q tile, lse2 / delta / q positions of its 128 rows go through
@@ -657,14 +678,25 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
     if (lane == 0) {
       uint32_t qd_it = 0, kv_it = 0;
       for (uint32_t it = 0;; ++it) {
-        const int u = atomicAdd(&p.sched[0], 1);
-        mbar_wait(u_empty, (it & 1) ^ 1);
-        *reinterpret_cast<volatile int*>(unit_slot) = u;
-        mbar_arrive(u_full);
+        int u;
+        if (!MC || crank == 0) {
+          u = atomicAdd(&p.sched[0], 1);
+          mbar_wait(u_empty, (it & 1) ^ 1);
+          *reinterpret_cast<volatile int*>(unit_slot) = u;
+          if constexpr (MC) {  // the same ticket to the peer CTA
+            st_cluster_u32(mapa_shared(smem_u32(unit_slot), 1), static_cast<uint32_t>(u));
+            mbar_arrive_cluster(mapa_shared(smem_u32(u_full), 1));
+          }
+          mbar_arrive(u_full);
+        } else {  // MC peer: take the leader's ticket
+          mbar_wait_cluster(u_full, it & 1);
+          u = *reinterpret_cast<volatile int*>(unit_slot);
+          mbar_arrive_cluster(mapa_shared(smem_u32(u_empty), 0));
+        }
         if (u >= p.num_units) break;
         const uint32_t unit = p.units[u];
-        const int kt = unit & 0xFFFF, kvh = (unit >> 16) & 0xFF, b = unit >> 24;
-        const int beg = p.tile_off[kt], n = p.tile_off[kt + 1] - beg;
+        const int kt = unit_ktile(unit), row = unit_row(unit), kvh = (unit >> 16) & 0xFF, b = unit >> 24;
+        const int beg = p.tile_off[row], n = p.tile_off[row + 1] - beg;
         if (n == 0) continue;
         mbar_wait(kv_empty, (kv_it & 1) ^ 1);
         ++kv_it;
@@ -687,14 +719,19 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
                          p.qvec + ((static_cast<size_t>(b) * p.heads + h) * p.n_q_tiles + qt) * 384, C::kVecBytes,
                          &qd_full[slot]);
               const CUtensorMap* tm = which == 0 ? &p.tm_q : &p.tm_do;
-              for (int sb = 0; sb < C::kSub; ++sb)
-                tma_load_4d(sQD + slot * C::kTileBytes + sb * C::kSubBytes, tm, &qd_full[slot], sb * 64, h,
-                            qt * 128, b);
+              if constexpr (MC) {  // my half of the tile, to both CTAs
+                tma_load_4d_mc(sQD + slot * C::kTileBytes + crank * C::kSubBytes, tm, &qd_full[slot],
+                               int(crank) * 64, h, qt * 128, b, uint16_t(0x3));
+              } else {
+                for (int sb = 0; sb < C::kSub; ++sb)
+                  tma_load_4d(sQD + slot * C::kTileBytes + sb * C::kSubBytes, tm, &qd_full[slot], sb * 64, h,
+                              qt * 128, b);
+              }
             }
           }
         }
       }
-      if (atomicAdd(&p.sched[1], 1) == static_cast<int>(gridDim.x) - 1) {
+      if (crank == 0 && atomicAdd(&p.sched[1], 1) == static_cast<int>(gridDim.x) / (MC ? 2 : 1) - 1) {
         p.sched[0] = 0;
         p.sched[1] = 0;
         __threadfence();
@@ -710,8 +747,8 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
     for (uint32_t it = 0;; ++it) {
       const int u = get_unit(it);
       if (u >= p.num_units) break;
-      const int kt = p.units[u] & 0xFFFF;
-      const int n = p.tile_off[kt + 1] - p.tile_off[kt];
+      const int row = unit_row(p.units[u]);
+      const int n = p.tile_off[row + 1] - p.tile_off[row];
       if (n == 0) continue;
       mbar_wait(kv_full, kv_phase & 1);
       ++kv_phase;
@@ -780,8 +817,16 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
           ss(128, v_desc, (di + 2) % NS);
           bwd_commit(dp_full);
         }
-        bwd_commit(&qd_empty[qi % NS]);
-        bwd_commit(&qd_empty[di % NS]);
+        if constexpr (MC) {  // a slot is free once both CTAs' MMAs read it
+          if (elect_one()) {
+            mma_commit_mc(&qd_empty[qi % NS], uint16_t(0x3));
+            mma_commit_mc(&qd_empty[di % NS], uint16_t(0x3));
+          }
+          __syncwarp();
+        } else {
+          bwd_commit(&qd_empty[qi % NS]);
+          bwd_commit(&qd_empty[di % NS]);
+        }
       }
       bwd_commit(acc_full);
       bwd_commit(kv_empty);
@@ -790,6 +835,7 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (MC) cluster_sync();  // no remote traffic may target an exited CTA
   tc_fence_after();
   if (warp == C::kMmaWarp) tmem_dealloc(tmem, 512);
 }
@@ -879,21 +925,37 @@ cudaError_t launch_bwd_dq(const BwdParams& p, int hs, int grid, cudaStream_t str
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_bwd_dkdv(const BwdParams& p, int hs, int grid, cudaStream_t stream) {
-  if (hs == 128) {
-    static std::atomic<uint64_t> done{0};
-    const cudaError_t once = ensure_smem_attr(fa_bwd_dkdv_kernel<128>, BwdCfg<128>::kSmemBytes, done);
-    if (once != cudaSuccess) return once;
-    fa_bwd_dkdv_kernel<128><<<grid, BwdCfg<128>::kThreads, BwdCfg<128>::kSmemBytes, stream>>>(p);
-  } else if (hs == 64) {
-    static std::atomic<uint64_t> done{0};
-    const cudaError_t once = ensure_smem_attr(fa_bwd_dkdv_kernel<64>, BwdCfg<64>::kSmemBytes, done);
-    if (once != cudaSuccess) return once;
-    fa_bwd_dkdv_kernel<64><<<grid, BwdCfg<64>::kThreads, BwdCfg<64>::kSmemBytes, stream>>>(p);
-  } else {
-    return cudaErrorInvalidValue;
+template <int HS, int MC>
+static cudaError_t launch_dkdv_impl(const BwdParams& p, int grid, cudaStream_t stream) {
+  using C = BwdCfg<HS>;
+  auto kern = fa_bwd_dkdv_kernel<HS, MC>;
+  static std::atomic<uint64_t> done{0};
+  const cudaError_t once = ensure_smem_attr(kern, C::kSmemBytes, done);
+  if (once != cudaSuccess) return once;
+  if constexpr (MC) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid & ~1), 1, 1);
+    cfg.blockDim = dim3(C::kThreads, 1, 1);
+    cfg.dynamicSmemBytes = C::kSmemBytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, p);
   }
+  kern<<<grid, C::kThreads, C::kSmemBytes, stream>>>(p);
   return cudaGetLastError();
+}
+
+cudaError_t launch_bwd_dkdv(const BwdParams& p, int hs, int grid, cudaStream_t stream) {
+  if (hs == 128)
+    return p.cluster ? launch_dkdv_impl<128, 1>(p, grid, stream) : launch_dkdv_impl<128, 0>(p, grid, stream);
+  if (hs == 64 && !p.cluster) return launch_dkdv_impl<64, 0>(p, grid, stream);
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_bwd_delta(const void* o, const void* dout, float* delta, int64_t batch, int64_t q_len,

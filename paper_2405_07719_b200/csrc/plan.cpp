@@ -376,4 +376,57 @@ StepPlan transpose_plan(const StepPlan& f, int64_t batch, int kv_heads, bool inc
   return t;
 }
 
+StepPlan transpose_plan_pairs(const StepPlan& f, int64_t batch, int kv_heads, bool include_empty) {
+  const StepPlan one = transpose_plan(f, batch, kv_heads, include_empty);
+  StepPlan t = one;
+  const int n_pairs = (f.n_k_tiles + 1) / 2;
+  t.k_pos.resize(static_cast<size_t>(n_pairs) * 2 * kTileN, INT32_MAX);  // a missing odd tile is padding
+  t.tile_off.assign(n_pairs + 1, 0);
+  t.tile_list.clear();
+  std::vector<int> cost(n_pairs, 0);
+  for (int pr = 0; pr < n_pairs; ++pr) {
+    // union of the two key tiles' q-tile lists (both ascending); partial if
+    // partial for either tile or visible to only one of them
+    std::vector<std::pair<int, uint32_t>> merged;  // (q tile, flags: 1 = in a, 2 = in b, 4 = partial)
+    for (int side = 0; side < 2; ++side) {
+      const int kt = 2 * pr + side;
+      if (kt >= f.n_k_tiles) continue;
+      for (int e = one.tile_off[kt]; e < one.tile_off[kt + 1]; ++e) {
+        const uint32_t entry = static_cast<uint32_t>(one.tile_list[e]);
+        merged.push_back({static_cast<int>(entry & 0x7FFFFFFFu), (1u << side) | ((entry >> 31) ? 4u : 0u)});
+      }
+    }
+    std::sort(merged.begin(), merged.end());
+    for (size_t i = 0; i < merged.size();) {
+      uint32_t fl = 0;
+      const int qt = merged[i].first;
+      for (; i < merged.size() && merged[i].first == qt; ++i) fl |= merged[i].second;
+      const bool partial = (fl & 4u) || (fl & 3u) != 3u;
+      t.tile_list.push_back(static_cast<int32_t>(static_cast<uint32_t>(qt) | (partial ? 0x80000000u : 0u)));
+    }
+    t.tile_off[pr + 1] = static_cast<int32_t>(t.tile_list.size());
+    cost[pr] = t.tile_off[pr + 1] - t.tile_off[pr];
+  }
+  struct U {
+    int cost, pr, b, kvh;
+  };
+  std::vector<U> us;
+  for (int pr = 0; pr < n_pairs; ++pr) {
+    if (cost[pr] == 0 && !include_empty) continue;
+    for (int64_t b = 0; b < batch; ++b)
+      for (int h = 0; h < kv_heads; ++h) us.push_back({cost[pr], pr, static_cast<int>(b), h});
+  }
+  std::stable_sort(us.begin(), us.end(), [](const U& a, const U& b) {
+    if (a.b != b.b) return a.b < b.b;
+    if (a.kvh != b.kvh) return a.kvh < b.kvh;
+    if (a.cost != b.cost) return a.cost > b.cost;
+    return a.pr < b.pr;
+  });
+  t.units.clear();
+  for (const U& x : us)
+    t.units.push_back(static_cast<uint32_t>(x.pr) | (static_cast<uint32_t>(x.kvh) << 16) |
+                      (static_cast<uint32_t>(x.b) << 24));
+  return t;
+}
+
 }  // namespace uspb200

@@ -121,6 +121,11 @@ FwdTiling fwd_tiling(int local_heads, int local_kv_heads, int kernel_head_size, 
 // include_empty keeps key tiles no query sees (their dK/dV rows are
 // written as zeros when the kernel does not accumulate).
 StepPlan transpose_plan(const StepPlan& fwd, int64_t batch, int kv_heads, bool include_empty);
+// The same over PAIRS of adjacent key tiles (2p, 2p+1) for the dK/dV
+// kernel's 2-CTA clusters: CSR over pairs, list = union of the two tiles'
+// q tiles (partial when partial for either or seen by only one), units
+// pair | kv_head << 16 | b << 24; k_pos padded to a whole number of pairs.
+StepPlan transpose_plan_pairs(const StepPlan& fwd, int64_t batch, int kv_heads, bool include_empty);
 
 // One communication event of a rank's forward, in the reference ledger's
 // terms (src/simcomm/ledger.hpp:21-30, closed forms ledger.cpp:25-37).
