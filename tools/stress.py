@@ -9,7 +9,7 @@ from paper_2405_07719_b200 import ProcessMesh, UspAttention  # noqa: E402
 iters = int(sys.argv[1]) if len(sys.argv) > 1 else 300
 dev = torch.device("cuda", 0)
 for (L, hc, kv, hs, bwd) in ((2048, 32, 8, 128, True), (32768, 32, 8, 128, False), (4096, 8, 8, 64, True),
-                             (3000, 12, 4, 128, True)):
+                             (3000, 12, 4, 128, True), (2900, 8, 2, 128, True)):
     eng = UspAttention(ProcessMesh(1, 1), rank=0, seq_len=L, heads=hc, kv_heads=kv, head_size=hs, causal=True)
     g = torch.Generator(device=dev).manual_seed(L)
     q = torch.randn(eng.q_shape(), device=dev, dtype=torch.bfloat16, generator=g)
