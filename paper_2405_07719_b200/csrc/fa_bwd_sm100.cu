@@ -598,12 +598,17 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
         mbar_wait(s_full, g & 1);
         tc_fence_after();
         uint32_t pp2[2][16];  // bf16 P^T pairs, reused by phase 2
+        // both 32-column chunks of this warp in flight at once (one TMEM
+        // round trip per phase instead of two)
+        uint32_t sv2[64];
+        tmem_ld32(lane_base + (2 * hf) * 32, sv2);
+        tmem_ld32(lane_base + (2 * hf + 1) * 32, sv2 + 32);
+        tmem_ld_wait(sv2);
+        tmem_ld_wait(sv2 + 32);
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
           const int c = 2 * hf + cc;
-          uint32_t sv[32];
-          tmem_ld32(lane_base + c * 32, sv);
-          tmem_ld_wait(sv);
+          const uint32_t* sv = sv2 + 32 * cc;
           uint32_t* pp = pp2[cc];
 #pragma unroll
           for (int i4 = 0; i4 < 8; ++i4) {
@@ -633,12 +638,15 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
         // columns for the dK MMAs (S^T(i+1) is computed meanwhile)
         mbar_wait(dp_full, g & 1);
         tc_fence_after();
+        uint32_t dp2[64];
+        tmem_ld32(lane_base + 128 + (2 * hf) * 32, dp2);
+        tmem_ld32(lane_base + 128 + (2 * hf + 1) * 32, dp2 + 32);
+        tmem_ld_wait(dp2);
+        tmem_ld_wait(dp2 + 32);
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
           const int c = 2 * hf + cc;
-          uint32_t dp[32];
-          tmem_ld32(lane_base + 128 + c * 32, dp);
-          tmem_ld_wait(dp);
+          const uint32_t* dp = dp2 + 32 * cc;
           uint32_t pd[16];
 #pragma unroll
           for (int i4 = 0; i4 < 8; ++i4) {
