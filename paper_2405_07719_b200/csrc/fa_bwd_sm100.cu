@@ -32,6 +32,9 @@
 #ifndef USPB_DKDV_STAGES
 #define USPB_DKDV_STAGES 6
 #endif
+#ifndef USPB_DKDV_JOINT_ST
+#define USPB_DKDV_JOINT_ST 0  // 1: one TMEM store round trip per phase (measured slower: 265 -> 277 ms)
+#endif
 
 namespace uspb200 {
 namespace {
@@ -78,7 +81,7 @@ struct BwdCfg {
   static constexpr int kStages = (kBudget - 2 * kTileBytes) / kTileBytes > USPB_DKDV_STAGES
                                      ? USPB_DKDV_STAGES
                                      : (kBudget - 2 * kTileBytes) / kTileBytes;
-  static constexpr int kVecBytes = 3 * 128 * 4;  // lse2 | delta | q position of one q tile
+  static constexpr int kVecBytes = 3 * 128 * 4;  // -lse2 | -delta | q position of one q tile
   static constexpr int kSmemBytes = 1024 + 2 * kTileBytes + kStages * kTileBytes + 2048 + kStages * kVecBytes;
   // dq kernel: K tiles in a 3-slot ring (released after the tile's dQ MMAs),
   // V tiles in a 2-slot ring (released as soon as dP has been computed)
@@ -510,7 +513,7 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
   int* unit_slot = reinterpret_cast<int*>(tmem_slot + 2);
   uint64_t* u_full = reinterpret_cast<uint64_t*>(unit_slot + 2);
   uint64_t* u_empty = u_full + 1;
-  // [NS slots][lse2 128 | delta 128 | qpos 128]: the vector of the q tile whose
+  // [NS slots][-lse2 128 | -delta 128 | qpos 128]: the vector of the q tile whose
   // Q sits in ring slot s, bulk-copied by the TMA warp with that Q tile
   uint8_t* vec = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(u_empty + 1) + 15u) & ~uintptr_t(15));
   const uint32_t vec_s = smem_u32(vec);
@@ -613,11 +616,18 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
 #pragma unroll
           for (int i4 = 0; i4 < 8; ++i4) {
             const uint32_t col = (c * 32 + 4 * i4) * 4;
-            const float4 L4 = lds_f4(vb + col);
-            const float lv[4] = {L4.x, L4.y, L4.z, L4.w};
+            const float4 L4 = lds_f4(vb + col);  // -lse2 of 4 q rows
             float pv[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) pv[e] = ex2(fmaf(__uint_as_float(sv[4 * i4 + e]), sl2, -lv[e]));
+            {
+              const float2 x01 = ffma2(make_float2(__uint_as_float(sv[4 * i4]), __uint_as_float(sv[4 * i4 + 1])),
+                                       make_float2(sl2, sl2), make_float2(L4.x, L4.y));
+              const float2 x23 = ffma2(make_float2(__uint_as_float(sv[4 * i4 + 2]), __uint_as_float(sv[4 * i4 + 3])),
+                                       make_float2(sl2, sl2), make_float2(L4.z, L4.w));
+              pv[0] = ex2(x01.x);
+              pv[1] = ex2(x01.y);
+              pv[2] = ex2(x23.x);
+              pv[3] = ex2(x23.y);
+            }
             if (entry < 0) {
               const float4 Q4 = lds_f4(vb + 1024 + col);
               const int qv[4] = {__float_as_int(Q4.x), __float_as_int(Q4.y), __float_as_int(Q4.z),
@@ -629,16 +639,30 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
             pp[2 * i4] = pack_bf16x2_pos(pv[0], pv[1]);
             pp[2 * i4 + 1] = pack_bf16x2_pos(pv[2], pv[3]);
           }
+#if !USPB_DKDV_JOINT_ST
           st16(lane_base + packed_col(c), pp);
           tmem_st_wait();
           tc_fence_before();
           mbar_arrive(&p_ready[c]);
+#endif
         }
+#if USPB_DKDV_JOINT_ST
+        // one store round trip for both chunks: the 64 elements schedule
+        // as one block (the compute warps are latency-bound at two per
+        // scheduler)
+        st16(lane_base + packed_col(2 * hf), pp2[0]);
+        st16(lane_base + packed_col(2 * hf + 1), pp2[1]);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&p_ready[2 * hf]);
+        mbar_arrive(&p_ready[2 * hf + 1]);
+#endif
         // phase 2: dS^T = P^T (dP^T - delta), packed over the consumed dP^T
         // columns for the dK MMAs (S^T(i+1) is computed meanwhile)
         mbar_wait(dp_full, g & 1);
         tc_fence_after();
         uint32_t dp2[64];
+        uint32_t pd2[2][16];
         tmem_ld32(lane_base + 128 + (2 * hf) * 32, dp2);
         tmem_ld32(lane_base + 128 + (2 * hf + 1) * 32, dp2 + 32);
         tmem_ld_wait(dp2);
@@ -647,25 +671,37 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
         for (int cc = 0; cc < 2; ++cc) {
           const int c = 2 * hf + cc;
           const uint32_t* dp = dp2 + 32 * cc;
-          uint32_t pd[16];
+          uint32_t* pd = pd2[cc];
 #pragma unroll
           for (int i4 = 0; i4 < 8; ++i4) {
-            const float4 D4 = lds_f4(vb + 512 + (c * 32 + 4 * i4) * 4);
-            const float dv[4] = {D4.x, D4.y, D4.z, D4.w};
+            const float4 D4 = lds_f4(vb + 512 + (c * 32 + 4 * i4) * 4);  // -delta of 4 q rows
+            const float ndv[4] = {D4.x, D4.y, D4.z, D4.w};
 #pragma unroll
             for (int e = 0; e < 4; e += 2) {
               // P^T as the dV MMA consumed it (bf16), widened
               const uint32_t w = pp2[cc][2 * i4 + e / 2];
-              const float p0 = __uint_as_float(w << 16), p1 = __uint_as_float(w & 0xFFFF0000u);
-              pd[2 * i4 + e / 2] = pack_bf16x2_int(p0 * (__uint_as_float(dp[4 * i4 + e]) - dv[e]),
-                                                   p1 * (__uint_as_float(dp[4 * i4 + e + 1]) - dv[e + 1]));
+              const float2 pw = make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+              const float2 d = fadd2(make_float2(__uint_as_float(dp[4 * i4 + e]), __uint_as_float(dp[4 * i4 + e + 1])),
+                                     make_float2(ndv[e], ndv[e + 1]));
+              const float2 ds = fmul2(pw, d);
+              pd[2 * i4 + e / 2] = pack_bf16x2_int(ds.x, ds.y);
             }
           }
+#if !USPB_DKDV_JOINT_ST
           st16(lane_base + 128 + packed_col(c), pd);
           tmem_st_wait();
           tc_fence_before();
           mbar_arrive(&ds_ready[c]);
+#endif
         }
+#if USPB_DKDV_JOINT_ST
+        st16(lane_base + 128 + packed_col(2 * hf), pd2[0]);
+        st16(lane_base + 128 + packed_col(2 * hf + 1), pd2[1]);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&ds_ready[2 * hf]);
+        mbar_arrive(&ds_ready[2 * hf + 1]);
+#endif
       }
       // epilogue: warp half 0 stores dv (+)= dV, half 1 dk (+)= dK / sqrt(hs)
       const bool any = n > 0;
@@ -877,8 +913,9 @@ __global__ void delta_kernel(const uint16_t* o, const uint16_t* dout, float* del
     if (valid) delta[r] = acc;
     if (qvec) {
       float* v = qvec + ((b * heads + h) * n_qt + t / 128) * 384 + (t % 128);
-      v[0] = valid ? lse[r] * 1.4426950408889634f : INFINITY;  // padding rows: p = 0
-      v[128] = valid ? acc : 0.f;
+      // negated, for the dK/dV kernel's packed FFMA2 / FADD2
+      v[0] = valid ? -(lse[r] * 1.4426950408889634f) : -INFINITY;  // padding rows: p = 0
+      v[128] = valid ? -acc : -0.f;
       v[256] = __int_as_float(q_pos[t]);
     }
   }
