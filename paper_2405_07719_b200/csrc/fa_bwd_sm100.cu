@@ -294,10 +294,14 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
           }
           uint32_t pk[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float p0 = ex2(fmaf(__uint_as_float(s[2 * i]), sl2, -lse2));
-            const float p1 = ex2(fmaf(__uint_as_float(s[2 * i + 1]), sl2, -lse2));
-            pk[i] = pack_bf16x2_int(p0 * (__uint_as_float(dp[2 * i]) - dlt), p1 * (__uint_as_float(dp[2 * i + 1]) - dlt));
+          for (int i = 0; i < 16; ++i) {  // packed fp32x2: one issue slot per pair
+            const float2 x = ffma2(make_float2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])),
+                                   make_float2(sl2, sl2), make_float2(-lse2, -lse2));
+            const float2 pr = make_float2(ex2(x.x), ex2(x.y));
+            const float2 d = fadd2(make_float2(__uint_as_float(dp[2 * i]), __uint_as_float(dp[2 * i + 1])),
+                                   make_float2(-dlt, -dlt));
+            const float2 ds = fmul2(pr, d);
+            pk[i] = pack_bf16x2_int(ds.x, ds.y);
           }
           st16(lane_base + sb + packed_col(c), pk);  // dS chunk c, over already-consumed S columns
           tmem_st_wait();
