@@ -32,9 +32,6 @@
 #ifndef USPB_DKDV_STAGES
 #define USPB_DKDV_STAGES 6
 #endif
-#ifndef USPB_DKDV_JOINT_ST
-#define USPB_DKDV_JOINT_ST 0  // 1: one TMEM store round trip per phase (measured slower: 265 -> 277 ms)
-#endif
 
 namespace uspb200 {
 namespace {
@@ -612,61 +609,49 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
         tmem_ld32(lane_base + (2 * hf + 1) * 32, sv2 + 32);
         tmem_ld_wait(sv2);
         tmem_ld_wait(sv2 + 32);
+        // the mask test is hoisted out of the element loop: one straight-line
+        // block per chunk for the (common) full tiles
+        auto p_chunks = [&](auto masked) {
+          constexpr bool kMasked = decltype(masked)::value;
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          const int c = 2 * hf + cc;
-          const uint32_t* sv = sv2 + 32 * cc;
-          uint32_t* pp = pp2[cc];
+          for (int cc = 0; cc < 2; ++cc) {
+            const int c = 2 * hf + cc;
+            const uint32_t* sv = sv2 + 32 * cc;
+            uint32_t* pp = pp2[cc];
 #pragma unroll
-          for (int i4 = 0; i4 < 8; ++i4) {
-            const uint32_t col = (c * 32 + 4 * i4) * 4;
-            const float4 L4 = lds_f4(vb + col);  // -lse2 of 4 q rows
-            float pv[4];
-            {
+            for (int i4 = 0; i4 < 8; ++i4) {
+              const uint32_t col = (c * 32 + 4 * i4) * 4;
+              const float4 L4 = lds_f4(vb + col);  // -lse2 of 4 q rows
               const float2 x01 = ffma2(make_float2(__uint_as_float(sv[4 * i4]), __uint_as_float(sv[4 * i4 + 1])),
                                        make_float2(sl2, sl2), make_float2(L4.x, L4.y));
               const float2 x23 = ffma2(make_float2(__uint_as_float(sv[4 * i4 + 2]), __uint_as_float(sv[4 * i4 + 3])),
                                        make_float2(sl2, sl2), make_float2(L4.z, L4.w));
-              pv[0] = ex2(x01.x);
-              pv[1] = ex2(x01.y);
-              pv[2] = ex2(x23.x);
-              pv[3] = ex2(x23.y);
-            }
-            if (entry < 0) {
-              const float4 Q4 = lds_f4(vb + 1024 + col);
-              const int qv[4] = {__float_as_int(Q4.x), __float_as_int(Q4.y), __float_as_int(Q4.z),
-                                 __float_as_int(Q4.w)};
+              float pv[4] = {ex2(x01.x), ex2(x01.y), ex2(x23.x), ex2(x23.y)};
+              if constexpr (kMasked) {
+                const float4 Q4 = lds_f4(vb + 1024 + col);
+                const int qv[4] = {__float_as_int(Q4.x), __float_as_int(Q4.y), __float_as_int(Q4.z),
+                                   __float_as_int(Q4.w)};
 #pragma unroll
-              for (int e = 0; e < 4; ++e)
-                if (kpos > qv[e]) pv[e] = 0.f;
+                for (int e = 0; e < 4; ++e) pv[e] = kpos > qv[e] ? 0.f : pv[e];
+              }
+              pp[2 * i4] = pack_bf16x2_pos(pv[0], pv[1]);
+              pp[2 * i4 + 1] = pack_bf16x2_pos(pv[2], pv[3]);
             }
-            pp[2 * i4] = pack_bf16x2_pos(pv[0], pv[1]);
-            pp[2 * i4 + 1] = pack_bf16x2_pos(pv[2], pv[3]);
+            st16(lane_base + packed_col(c), pp);
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&p_ready[c]);
           }
-#if !USPB_DKDV_JOINT_ST
-          st16(lane_base + packed_col(c), pp);
-          tmem_st_wait();
-          tc_fence_before();
-          mbar_arrive(&p_ready[c]);
-#endif
-        }
-#if USPB_DKDV_JOINT_ST
-        // one store round trip for both chunks: the 64 elements schedule
-        // as one block (the compute warps are latency-bound at two per
-        // scheduler)
-        st16(lane_base + packed_col(2 * hf), pp2[0]);
-        st16(lane_base + packed_col(2 * hf + 1), pp2[1]);
-        tmem_st_wait();
-        tc_fence_before();
-        mbar_arrive(&p_ready[2 * hf]);
-        mbar_arrive(&p_ready[2 * hf + 1]);
-#endif
+        };
+        if (entry < 0)
+          p_chunks(std::true_type{});
+        else
+          p_chunks(std::false_type{});
         // phase 2: dS^T = P^T (dP^T - delta), packed over the consumed dP^T
         // columns for the dK MMAs (S^T(i+1) is computed meanwhile)
         mbar_wait(dp_full, g & 1);
         tc_fence_after();
         uint32_t dp2[64];
-        uint32_t pd2[2][16];
         tmem_ld32(lane_base + 128 + (2 * hf) * 32, dp2);
         tmem_ld32(lane_base + 128 + (2 * hf + 1) * 32, dp2 + 32);
         tmem_ld_wait(dp2);
@@ -675,7 +660,7 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
         for (int cc = 0; cc < 2; ++cc) {
           const int c = 2 * hf + cc;
           const uint32_t* dp = dp2 + 32 * cc;
-          uint32_t* pd = pd2[cc];
+          uint32_t pd[16];
 #pragma unroll
           for (int i4 = 0; i4 < 8; ++i4) {
             const float4 D4 = lds_f4(vb + 512 + (c * 32 + 4 * i4) * 4);  // -delta of 4 q rows
@@ -691,21 +676,11 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
               pd[2 * i4 + e / 2] = pack_bf16x2_int(ds.x, ds.y);
             }
           }
-#if !USPB_DKDV_JOINT_ST
           st16(lane_base + 128 + packed_col(c), pd);
           tmem_st_wait();
           tc_fence_before();
           mbar_arrive(&ds_ready[c]);
-#endif
         }
-#if USPB_DKDV_JOINT_ST
-        st16(lane_base + 128 + packed_col(2 * hf), pd2[0]);
-        st16(lane_base + 128 + packed_col(2 * hf + 1), pd2[1]);
-        tmem_st_wait();
-        tc_fence_before();
-        mbar_arrive(&ds_ready[2 * hf]);
-        mbar_arrive(&ds_ready[2 * hf + 1]);
-#endif
       }
       // epilogue: warp half 0 stores dv (+)= dV, half 1 dk (+)= dK / sqrt(hs)
       const bool any = n > 0;
