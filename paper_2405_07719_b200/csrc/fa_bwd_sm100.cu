@@ -29,6 +29,15 @@
 #ifndef USPB_DQ_KSLOTS
 #define USPB_DQ_KSLOTS 3
 #endif
+#ifndef USPB_DBG_NOEXP
+#define USPB_DBG_NOEXP 0
+#endif
+#ifndef USPB_DBG_NOCOMPUTE
+#define USPB_DBG_NOCOMPUTE 0
+#endif
+#ifndef USPB_DKDV_PAIRW
+#define USPB_DKDV_PAIRW 1  // one hand-off barrier per chunk pair (see the dK/dV kernel)
+#endif
 #ifndef USPB_DKDV_STAGES
 #define USPB_DKDV_STAGES 6
 #endif
@@ -526,8 +535,10 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
     mbar_init(s_full, 1);
     mbar_init(dp_full, 1);
     for (int c = 0; c < 4; ++c) {
-      mbar_init(&p_ready[c], 128);
-      mbar_init(&ds_ready[c], 128);
+      // PAIRW: barrier k collects chunk k of both warp halves (chunks k and
+      // 2 + k land together), so the MMA warp waits twice per phase, not 4x
+      mbar_init(&p_ready[c], USPB_DKDV_PAIRW ? 256 : 128);
+      mbar_init(&ds_ready[c], USPB_DKDV_PAIRW ? 256 : 128);
     }
     mbar_init(acc_full, 1);
     mbar_init(u_full, 1);
@@ -619,14 +630,18 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
             const uint32_t* sv = sv2 + 32 * cc;
             uint32_t* pp = pp2[cc];
 #pragma unroll
-            for (int i4 = 0; i4 < 8; ++i4) {
+            for (int i4 = 0; i4 < (USPB_DBG_NOCOMPUTE ? 0 : 8); ++i4) {
               const uint32_t col = (c * 32 + 4 * i4) * 4;
               const float4 L4 = lds_f4(vb + col);  // -lse2 of 4 q rows
               const float2 x01 = ffma2(make_float2(__uint_as_float(sv[4 * i4]), __uint_as_float(sv[4 * i4 + 1])),
                                        make_float2(sl2, sl2), make_float2(L4.x, L4.y));
               const float2 x23 = ffma2(make_float2(__uint_as_float(sv[4 * i4 + 2]), __uint_as_float(sv[4 * i4 + 3])),
                                        make_float2(sl2, sl2), make_float2(L4.z, L4.w));
+#if USPB_DBG_NOEXP
+              float pv[4] = {x01.x, x01.y, x23.x, x23.y};
+#else
               float pv[4] = {ex2(x01.x), ex2(x01.y), ex2(x23.x), ex2(x23.y)};
+#endif
               if constexpr (kMasked) {
                 const float4 Q4 = lds_f4(vb + 1024 + col);
                 const int qv[4] = {__float_as_int(Q4.x), __float_as_int(Q4.y), __float_as_int(Q4.z),
@@ -640,7 +655,7 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
             st16(lane_base + packed_col(c), pp);
             tmem_st_wait();
             tc_fence_before();
-            mbar_arrive(&p_ready[c]);
+            mbar_arrive(&p_ready[USPB_DKDV_PAIRW ? cc : c]);
           }
         };
         if (entry < 0)
@@ -662,7 +677,7 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
           const uint32_t* dp = dp2 + 32 * cc;
           uint32_t pd[16];
 #pragma unroll
-          for (int i4 = 0; i4 < 8; ++i4) {
+          for (int i4 = 0; i4 < (USPB_DBG_NOCOMPUTE ? 0 : 8); ++i4) {
             const float4 D4 = lds_f4(vb + 512 + (c * 32 + 4 * i4) * 4);  // -delta of 4 q rows
             const float ndv[4] = {D4.x, D4.y, D4.z, D4.w};
 #pragma unroll
@@ -679,7 +694,7 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
           st16(lane_base + 128 + packed_col(c), pd);
           tmem_st_wait();
           tc_fence_before();
-          mbar_arrive(&ds_ready[c]);
+          mbar_arrive(&ds_ready[USPB_DKDV_PAIRW ? cc : c]);
         }
       }
       // epilogue: warp half 0 stores dv (+)= dV, half 1 dk (+)= dK / sqrt(hs)
@@ -810,8 +825,10 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
 #pragma unroll
         for (int n4 = 0; n4 < 4; ++n4) {
           const int c = chunk_at(n4);
-          mbar_wait(&p_ready[c], g & 1);
-          tc_fence_after();
+          if (!USPB_DKDV_PAIRW || (n4 & 1) == 0) {
+            mbar_wait(&p_ready[USPB_DKDV_PAIRW ? n4 >> 1 : c], g & 1);
+            tc_fence_after();
+          }
           if (elect_one())
             mma_ts_k2(256, packed_col(c), dbd + static_cast<uint64_t>(c * 256), C::kIdescTS, (acc | n4) ? 1u : 0u);
           __syncwarp();
@@ -827,8 +844,10 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
 #pragma unroll
         for (int n4 = 0; n4 < 4; ++n4) {
           const int c = chunk_at(n4);
-          mbar_wait(&ds_ready[c], g & 1);
-          tc_fence_after();
+          if (!USPB_DKDV_PAIRW || (n4 & 1) == 0) {
+            mbar_wait(&ds_ready[USPB_DKDV_PAIRW ? n4 >> 1 : c], g & 1);
+            tc_fence_after();
+          }
           if (elect_one())
             mma_ts_k2(256 + HS, 128 + packed_col(c), qbd + static_cast<uint64_t>(c * 256), C::kIdescTS,
                       (acc | n4) ? 1u : 0u);
