@@ -197,7 +197,8 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
     mbar_init(&s_full[0], 1);
     mbar_init(&s_full[1], 1);
     mbar_init(dp_full, 1);
-    for (int c = 0; c < 8; ++c) mbar_init(&chunk_ready[c], 128);
+    // with PAIRW, barrier (parity, k) collects chunk k of both warp halves
+    for (int c = 0; c < 8; ++c) mbar_init(&chunk_ready[c], USPB_DKDV_PAIRW ? 256 : 128);
     mbar_init(dq_full, 1);
     mbar_init(u_full, 1);
     // compute warps + MMA warp (of both CTAs, + the peer's TMA warp, with MC)
@@ -312,7 +313,7 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
           st16(lane_base + sb + packed_col(c), pk);  // dS chunk c, over already-consumed S columns
           tmem_st_wait();
           tc_fence_before();
-          mbar_arrive(&chunk_ready[(g & 1) * 4 + c]);
+          mbar_arrive(&chunk_ready[(g & 1) * 4 + (USPB_DKDV_PAIRW ? cc : c)]);
         }
       }
       // epilogue: dq (+)= dQ / sqrt(hs); warp half hf stores half the columns
@@ -461,8 +462,10 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
 #pragma unroll
           for (int n4 = 0; n4 < 4; ++n4) {
             const int c = chunk_at(n4);
-            mbar_wait(&chunk_ready[(g & 1) * 4 + c], (g >> 1) & 1);
-            tc_fence_after();
+            if (!USPB_DKDV_PAIRW || (n4 & 1) == 0) {
+              mbar_wait(&chunk_ready[(g & 1) * 4 + (USPB_DKDV_PAIRW ? n4 >> 1 : c)], (g >> 1) & 1);
+              tc_fence_after();
+            }
             if (elect_one())
               mma_ts_k2(kDQ, sb + packed_col(c), bd + static_cast<uint64_t>(c * 256), C::kIdescTS,
                         (j > 0 || n4 > 0) ? 1u : 0u);
