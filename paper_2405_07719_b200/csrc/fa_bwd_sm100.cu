@@ -38,6 +38,9 @@
 #ifndef USPB_DKDV_PAIRW
 #define USPB_DKDV_PAIRW 1  // one hand-off barrier per chunk pair (see the dK/dV kernel)
 #endif
+#ifndef USPB_DKDV_QD1
+#define USPB_DKDV_QD1 0  // 1: Q and dO of a q tile on one barrier (measured slower, 247 -> 255 ms: S(i+1) then waits for dO)
+#endif
 #ifndef USPB_DKDV_STAGES
 #define USPB_DKDV_STAGES 6
 #endif
@@ -96,7 +99,7 @@ struct BwdCfg {
   static_assert(kDqSmemBytes <= 227 * 1024, "dq smem");
   static constexpr uint32_t kIdescSS = idesc_bf16_f32(128, 128, 0, 0);  // S / dP
   static constexpr uint32_t kIdescTS = idesc_bf16_f32(128, HS, 0, 1);   // acc += X * tile
-  static_assert(kStages >= 2, "smem");
+  static_assert(kStages >= 2 && kStages % 2 == 0, "smem; Q / dO slot pairs");
 };
 
 // The 32-column chunks of a tile in the order their packed operands become
@@ -754,19 +757,23 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
               const uint32_t slot = qd_it % NS;
               mbar_wait(&qd_empty[slot], ((qd_it / NS) & 1) ^ 1);
               ++qd_it;
-              mbar_arrive_expect_tx(&qd_full[slot], C::kTileBytes + (which == 0 ? C::kVecBytes : 0));
+              // QD1: Q, dO and the vector all complete on the Q slot's barrier
+              // (the MMA warp then waits once per q tile); NS is even, so Q
+              // always sits in an even slot and its dO in the next one
+              uint64_t* full = &qd_full[USPB_DKDV_QD1 && which == 1 ? slot - 1 : slot];
+              if (!USPB_DKDV_QD1 || which == 0)
+                mbar_arrive_expect_tx(full, (USPB_DKDV_QD1 ? 2 : 1) * C::kTileBytes + (which == 0 ? C::kVecBytes : 0));
               if (which == 0)
                 bulk_g2s(vec + slot * C::kVecBytes,
                          p.qvec + ((static_cast<size_t>(b) * p.heads + h) * p.n_q_tiles + qt) * 384, C::kVecBytes,
-                         &qd_full[slot]);
+                         full);
               const CUtensorMap* tm = which == 0 ? &p.tm_q : &p.tm_do;
               if constexpr (MC) {  // my half of the tile, to both CTAs
-                tma_load_4d_mc(sQD + slot * C::kTileBytes + crank * C::kSubBytes, tm, &qd_full[slot],
-                               int(crank) * 64, h, qt * 128, b, uint16_t(0x3));
+                tma_load_4d_mc(sQD + slot * C::kTileBytes + crank * C::kSubBytes, tm, full, int(crank) * 64, h,
+                               qt * 128, b, uint16_t(0x3));
               } else {
                 for (int sb = 0; sb < C::kSub; ++sb)
-                  tma_load_4d(sQD + slot * C::kTileBytes + sb * C::kSubBytes, tm, &qd_full[slot], sb * 64, h,
-                              qt * 128, b);
+                  tma_load_4d(sQD + slot * C::kTileBytes + sb * C::kSubBytes, tm, full, sb * 64, h, qt * 128, b);
               }
             }
           }
@@ -809,6 +816,7 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
         });
       };
       auto wait_qd = [&](uint32_t x) {
+        if (USPB_DKDV_QD1 && (x & 1)) return;  // dO completed with its Q tile (waited before S)
         mbar_wait(&qd_full[x % NS], (x / NS) & 1);
         tc_fence_after();
       };
