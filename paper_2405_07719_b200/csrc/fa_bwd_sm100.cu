@@ -41,6 +41,9 @@
 #ifndef USPB_DKDV_QD1
 #define USPB_DKDV_QD1 0  // 1: Q and dO of a q tile on one barrier (measured slower, 247 -> 255 ms: S(i+1) then waits for dO)
 #endif
+#ifndef USPB_DKDV_SWAP
+#define USPB_DKDV_SWAP 1  // Q / dO slot roles alternate per ring round (qd_slot)
+#endif
 #ifndef USPB_DKDV_STAGES
 #define USPB_DKDV_STAGES 6
 #endif
@@ -104,6 +107,16 @@ struct BwdCfg {
 
 // The 32-column chunks of a tile in the order their packed operands become
 // ready (warp half 0 does chunks 0,1, half 1 does 2,3, concurrently).
+// dK/dV Q / dO ring: position 2T + w (w = 0 Q, 1 dO of the T-th q tile of
+// this CTA) -> slot. Tile T uses the slot pair 2 (T mod NS/2); with SWAP the
+// roles alternate per round, so Q(T + NS/2) lands in dO(T)'s slot, which is
+// released right after the dV(T) MMAs — one phase before Q(T)'s slot (after
+// dK(T)) — and the next S^T's operand arrives earlier.
+template <int NS>
+__device__ __forceinline__ uint32_t qd_slot(uint32_t pos) {
+  const uint32_t t = pos >> 1, w = pos & 1u, round = t / (NS / 2);
+  return 2u * (t % (NS / 2)) + (w ^ (USPB_DKDV_SWAP ? (round & 1u) : 0u));
+}
 __device__ __forceinline__ int chunk_at(int n) { return ((n & 1) << 1) | (n >> 1); }
 // TMEM column (within an S / dP buffer) of chunk c's packed bf16 result:
 // each warp half writes only inside the 64 columns it reads (half 0 owns
@@ -610,8 +623,8 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
       for (int i = 0; i < total; ++i, ++g) {
         const int entry = p.tile_list[beg + i % n];
         // this q tile's lse2 / delta / positions came with its Q tile (ring
-        // slot 2g % NS; the slot is not refilled before this tile's dK MMAs)
-        const uint32_t qslot = (2 * g) % NS;
+        // slot qd_slot(2g); the slot is not refilled before this tile's dK MMAs)
+        const uint32_t qslot = qd_slot<NS>(2 * g);
         mbar_wait(&qd_full[qslot], ((2 * g) / NS) & 1);
         const uint32_t vb = vec_s + qslot * C::kVecBytes;
         // phase 1: P^T = exp(S^T - lse) (thread = key row), packed over the
@@ -754,13 +767,12 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
           for (int j = 0; j < n; ++j) {
             const int qt = p.tile_list[beg + j] & 0x7FFFFFFF;
             for (int which = 0; which < 2; ++which) {
-              const uint32_t slot = qd_it % NS;
+              const uint32_t slot = qd_slot<NS>(qd_it);
               mbar_wait(&qd_empty[slot], ((qd_it / NS) & 1) ^ 1);
               ++qd_it;
               // QD1: Q, dO and the vector all complete on the Q slot's barrier
-              // (the MMA warp then waits once per q tile); NS is even, so Q
-              // always sits in an even slot and its dO in the next one
-              uint64_t* full = &qd_full[USPB_DKDV_QD1 && which == 1 ? slot - 1 : slot];
+              // (the MMA warp then waits once per q tile)
+              uint64_t* full = &qd_full[USPB_DKDV_QD1 && which == 1 ? qd_slot<NS>(qd_it - 2) : slot];
               if (!USPB_DKDV_QD1 || which == 0)
                 mbar_arrive_expect_tx(full, (USPB_DKDV_QD1 ? 2 : 1) * C::kTileBytes + (which == 0 ? C::kVecBytes : 0));
               if (which == 0)
@@ -817,20 +829,20 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
       };
       auto wait_qd = [&](uint32_t x) {
         if (USPB_DKDV_QD1 && (x & 1)) return;  // dO completed with its Q tile (waited before S)
-        mbar_wait(&qd_full[x % NS], (x / NS) & 1);
+        mbar_wait(&qd_full[qd_slot<NS>(x)], (x / NS) & 1);
         tc_fence_after();
       };
       // S^T(0) = K Q(0)^T, dP^T(0) = V dO(0)^T
       wait_qd(qd_it);
-      ss(0, k_desc, qd_it % NS);
+      ss(0, k_desc, qd_slot<NS>(qd_it));
       bwd_commit(s_full);
       wait_qd(qd_it + 1);
-      ss(128, v_desc, (qd_it + 1) % NS);
+      ss(128, v_desc, qd_slot<NS>(qd_it + 1));
       bwd_commit(dp_full);
       for (int i = 0; i < total; ++i, ++g) {
         const uint32_t qi = qd_it + 2 * i, di = qi + 1;
-        const uint64_t dbd = qdmn_desc0 + static_cast<uint64_t>((((di % NS) * C::kTileBytes)) >> 4);
-        const uint64_t qbd = qdmn_desc0 + static_cast<uint64_t>((((qi % NS) * C::kTileBytes)) >> 4);
+        const uint64_t dbd = qdmn_desc0 + static_cast<uint64_t>(((qd_slot<NS>(di) * C::kTileBytes)) >> 4);
+        const uint64_t qbd = qdmn_desc0 + static_cast<uint64_t>(((qd_slot<NS>(qi) * C::kTileBytes)) >> 4);
         const uint32_t acc = i > 0 ? 1u : 0u;
         // dV += P^T dO(i), chunk by chunk as P^T lands
 #pragma unroll
@@ -844,11 +856,18 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
             mma_ts_k2(256, packed_col(c), dbd + static_cast<uint64_t>(c * 256), C::kIdescTS, (acc | n4) ? 1u : 0u);
           __syncwarp();
         }
+        // dO(i) is read by nothing after dV(i): release its slot now
+        if constexpr (MC) {  // a slot is free once both CTAs' MMAs read it
+          if (elect_one()) mma_commit_mc(&qd_empty[qd_slot<NS>(di)], uint16_t(0x3));
+          __syncwarp();
+        } else {
+          bwd_commit(&qd_empty[qd_slot<NS>(di)]);
+        }
         // S^T(i+1) over the S^T region (its P^T is consumed by the dV MMAs
         // issued above): overlaps this tile's dS^T work
         if (i + 1 < total) {
           wait_qd(qi + 2);
-          ss(0, k_desc, (qi + 2) % NS);
+          ss(0, k_desc, qd_slot<NS>(qi + 2));
           bwd_commit(s_full);
         }
         // dK += dS^T Q(i), chunk by chunk as dS^T lands
@@ -867,18 +886,14 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
         // dP^T(i+1) over the dP^T region (its dS^T is consumed by the dK MMAs)
         if (i + 1 < total) {
           wait_qd(di + 2);
-          ss(128, v_desc, (di + 2) % NS);
+          ss(128, v_desc, qd_slot<NS>(di + 2));
           bwd_commit(dp_full);
         }
-        if constexpr (MC) {  // a slot is free once both CTAs' MMAs read it
-          if (elect_one()) {
-            mma_commit_mc(&qd_empty[qi % NS], uint16_t(0x3));
-            mma_commit_mc(&qd_empty[di % NS], uint16_t(0x3));
-          }
+        if constexpr (MC) {
+          if (elect_one()) mma_commit_mc(&qd_empty[qd_slot<NS>(qi)], uint16_t(0x3));
           __syncwarp();
         } else {
-          bwd_commit(&qd_empty[qi % NS]);
-          bwd_commit(&qd_empty[di % NS]);
+          bwd_commit(&qd_empty[qd_slot<NS>(qi)]);
         }
       }
       bwd_commit(acc_full);
