@@ -1070,6 +1070,12 @@ class Engine {
     p.inv_scale = static_cast<float>(1.0 / std::sqrt(double(hs_)));
     p.accumulate = accumulate ? 1 : 0;
     p.cluster = (is_dq ? bwd_cluster_ : dkdv_cluster_) ? 1 : 0;
+    static const char* bwd_trace = std::getenv("USP_BWD_TRACE");  // development timeline
+    if (bwd_trace && std::string(bwd_trace) == (is_dq ? "dq" : "dkdv")) {
+      if (!trace_buf_.p) trace_buf_ = DevBuf(sizeof(unsigned long long) * kTraceTiles * kTraceEvents);
+      USPB_CHECK(cudaMemsetAsync(trace_buf_.p, 0, trace_buf_.bytes, st));
+      p.trace = trace_buf_.as<unsigned long long>();
+    }
     const int reserve = (R_ > 1 && tr_) ? tr_->reserved_sms() : 0;
     const int slots = std::max(1, num_sms_ - reserve);
     const int grid = p.cluster ? std::max(2, std::min(2 * p.num_units, slots) & ~1) : std::min(p.num_units, slots);

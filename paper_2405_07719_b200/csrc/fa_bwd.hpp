@@ -30,7 +30,7 @@ struct BwdParams {
   const int32_t* k_pos;
   int* sched;                // unit tickets, zero between launches
   // dK/dV kernel: per (batch, q head, 128-row q tile) the 3 x 128 floats
-  // {lse * log2(e) (INF on padding rows), delta, q position} laid out
+  // {-lse * log2(e) (-INF on padding rows), -delta, q position} laid out
   // contiguously ([b][h][q tile][3][128], filled by launch_bwd_delta) so the
   // TMA warp bulk-copies them next to the Q tile
   const float* qvec;
@@ -42,6 +42,9 @@ struct BwdParams {
   float scale_log2;  // log2(e) / sqrt(head_size)
   float inv_scale;   // 1 / sqrt(head_size)
   int accumulate;    // 0: write the fp32 outputs, 1: add into them
+  // development (USPB_TRACE builds, USP_BWD_TRACE=dq|dkdv): clock64 stamps of
+  // CTA 0, [event][q tile] over the first kTraceTiles tiles; tools/trace_bwd.py
+  unsigned long long* trace;
 };
 
 cudaError_t launch_bwd_dq(const BwdParams& p, int hs, int grid, cudaStream_t stream);

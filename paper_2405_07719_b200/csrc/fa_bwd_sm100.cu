@@ -63,6 +63,18 @@ __device__ __forceinline__ void bwd_dispatch_slot(uint32_t slot, F&& f) {
   }
 }
 
+__device__ __forceinline__ void bwd_trace(const BwdParams& p, int ev, uint32_t i) {
+#ifdef USPB_TRACE
+  if (p.trace != nullptr && blockIdx.x == 0 && i < static_cast<uint32_t>(kTraceTiles)) {
+    unsigned long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+    p.trace[ev * kTraceTiles + i] = c;
+  }
+#else
+  (void)p, (void)ev, (void)i;
+#endif
+}
+
 __device__ __forceinline__ void bwd_commit(uint64_t* bar) {
   if (elect_one()) mma_commit(bar);
   __syncwarp();
@@ -629,7 +641,9 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
         const uint32_t vb = vec_s + qslot * C::kVecBytes;
         // phase 1: P^T = exp(S^T - lse) (thread = key row), packed over the
         // consumed S^T columns for the dV MMAs; fp32 P kept for phase 2
+        const bool tr = q4 == 0 && lane == 0;
         mbar_wait(s_full, g & 1);
+        if (tr) bwd_trace(p, 4 * hf + 0, g);
         tc_fence_after();
         uint32_t pp2[2][16];  // bf16 P^T pairs, reused by phase 2
         // both 32-column chunks of this warp in flight at once (one TMEM
@@ -681,9 +695,11 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
           p_chunks(std::true_type{});
         else
           p_chunks(std::false_type{});
+        if (tr) bwd_trace(p, 4 * hf + 1, g);
         // phase 2: dS^T = P^T (dP^T - delta), packed over the consumed dP^T
         // columns for the dK MMAs (S^T(i+1) is computed meanwhile)
         mbar_wait(dp_full, g & 1);
+        if (tr) bwd_trace(p, 4 * hf + 2, g);
         tc_fence_after();
         uint32_t dp2[64];
         tmem_ld32(lane_base + 128 + (2 * hf) * 32, dp2);
@@ -715,6 +731,7 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
           tc_fence_before();
           mbar_arrive(&ds_ready[USPB_DKDV_PAIRW ? cc : c]);
         }
+        if (tr) bwd_trace(p, 4 * hf + 3, g);
       }
       // epilogue: warp half 0 stores dv (+)= dV, half 1 dk (+)= dK / sqrt(hs)
       const bool any = n > 0;
@@ -769,6 +786,7 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
             for (int which = 0; which < 2; ++which) {
               const uint32_t slot = qd_slot<NS>(qd_it);
               mbar_wait(&qd_empty[slot], ((qd_it / NS) & 1) ^ 1);
+              bwd_trace(p, 14 + which, qd_it >> 1);
               ++qd_it;
               // QD1: Q, dO and the vector all complete on the Q slot's barrier
               // (the MMA warp then waits once per q tile)
@@ -850,6 +868,7 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
           const int c = chunk_at(n4);
           if (!USPB_DKDV_PAIRW || (n4 & 1) == 0) {
             mbar_wait(&p_ready[USPB_DKDV_PAIRW ? n4 >> 1 : c], g & 1);
+            if (lane == 0) bwd_trace(p, 8 + (n4 >> 1), g);
             tc_fence_after();
           }
           if (elect_one())
@@ -869,6 +888,7 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
           wait_qd(qi + 2);
           ss(0, k_desc, qd_slot<NS>(qi + 2));
           bwd_commit(s_full);
+          if (lane == 0) bwd_trace(p, 10, g);
         }
         // dK += dS^T Q(i), chunk by chunk as dS^T lands
 #pragma unroll
@@ -876,6 +896,7 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
           const int c = chunk_at(n4);
           if (!USPB_DKDV_PAIRW || (n4 & 1) == 0) {
             mbar_wait(&ds_ready[USPB_DKDV_PAIRW ? n4 >> 1 : c], g & 1);
+            if (lane == 0) bwd_trace(p, 11 + (n4 >> 1), g);
             tc_fence_after();
           }
           if (elect_one())
@@ -888,6 +909,7 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
           wait_qd(di + 2);
           ss(128, v_desc, qd_slot<NS>(di + 2));
           bwd_commit(dp_full);
+          if (lane == 0) bwd_trace(p, 13, g);
         }
         if constexpr (MC) {
           if (elect_one()) mma_commit_mc(&qd_empty[qd_slot<NS>(qi)], uint16_t(0x3));
