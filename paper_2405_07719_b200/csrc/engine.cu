@@ -654,7 +654,11 @@ class Engine {
     const double up_s_per_row = double((H_ + 2 * KV_) * hs_ * 2) / 50e9;
     const double att_s_per_pair = 4.0 * hl_ * hs_ / 1.2e15;
     const int64_t big = std::max<int64_t>(tiles(Tr_ / 8), 1024);
-    const int64_t tail = Tr_ > 4 * 8192 ? 8192 : 0;
+    static const int64_t tail_rows = [] {  // development knob (default 8192 rows)
+      const char* e = std::getenv("USP_HOST_TAIL");
+      return e ? std::max<int64_t>(0, std::atoll(e)) : int64_t(8192);
+    }();
+    const int64_t tail = Tr_ > 4 * 8192 ? tiles(tail_rows) : 0;
     int64_t prev = 0, r = 1024;
     while (r < Tr_ - tail) {
       b.push_back(r);
