@@ -294,8 +294,11 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
       for (int j = 0; j < n; ++j, ++g) {
         const int entry = p.tile_list[beg + j];
         const uint32_t sb = (g & 1) ? kS1 : 0u;
+        const bool tr = q4 == 0 && lane == 0;
         mbar_wait(&s_full[g & 1], (g >> 1) & 1);
+        if (tr) bwd_trace(p, 4 * hf + 0, g);
         mbar_wait(dp_full, g & 1);
+        if (tr) bwd_trace(p, 4 * hf + 1, g);
         tc_fence_after();
         // Both of this warp's chunks of S and dP into registers at once, so
         // the dP buffer is released before the elementwise work: dP(j+1) is
@@ -343,6 +346,7 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
           tc_fence_before();
           mbar_arrive(&chunk_ready[(g & 1) * 4 + (USPB_DKDV_PAIRW ? cc : c)]);
         }
+        if (tr) bwd_trace(p, 4 * hf + 2, g);
       }
       // epilogue: dq (+)= dQ / sqrt(hs); warp half hf stores half the columns
       if (n > 0) {
@@ -390,6 +394,7 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
           const int kt = p.tile_list[beg + j] & 0x7FFFFFFF;
           const uint32_t ks = kv_it % NK, vs = kv_it % NV;
           mbar_wait(&k_empty[ks], ((kv_it / NK) & 1) ^ 1);
+          bwd_trace(p, 14, kv_it);
           mbar_arrive_expect_tx(&k_full[ks], C::kTileBytes);
           if constexpr (MC) {  // my half of the tile, to both CTAs
             tma_load_4d_mc(sK + ks * C::kTileBytes + crank * C::kSubBytes, &p.tm_k, &k_full[ks], int(crank) * 64,
@@ -400,6 +405,7 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
                           kt * 128, b);
           }
           mbar_wait(&v_empty[vs], ((kv_it / NV) & 1) ^ 1);
+          bwd_trace(p, 15, kv_it);
           mbar_arrive_expect_tx(&v_full[vs], C::kTileBytes);
           if constexpr (MC) {
             tma_load_4d_mc(sV + vs * C::kTileBytes + crank * C::kSubBytes, &p.tm_v, &v_full[vs], int(crank) * 64,
@@ -477,8 +483,11 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
           // is in registers: both overlap tile j's elementwise work
           issue_s(t + 1, ((g + 1) & 1) ? kS1 : 0u);
           bwd_commit(&s_full[(g + 1) & 1]);
+          if (lane == 0) bwd_trace(p, 8, g);
           mbar_wait(dp_free, g & 1);
+          if (lane == 0) bwd_trace(p, 9, g);
           issue_dp(t + 1);
+          if (lane == 0) bwd_trace(p, 10, g);
         } else {
           bwd_commit(q_empty);  // every MMA reading Q / dO has been issued
         }
@@ -492,6 +501,7 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
             const int c = chunk_at(n4);
             if (!USPB_DKDV_PAIRW || (n4 & 1) == 0) {
               mbar_wait(&chunk_ready[(g & 1) * 4 + (USPB_DKDV_PAIRW ? n4 >> 1 : c)], (g >> 1) & 1);
+              if (lane == 0) bwd_trace(p, 11 + (n4 >> 1), g);
               tc_fence_after();
             }
             if (elect_one())
