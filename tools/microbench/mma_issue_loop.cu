@@ -11,8 +11,12 @@
 #include "../../paper_2405_07719_b200/csrc/ptx_sm100.cuh"
 using namespace uspb200::ptx;
 
-template <int MODE>  // 0: 24 MMAs back to back per tile; 1: the dQ pattern; 2: pattern without waits
-__global__ void __launch_bounds__(32, 1) k(unsigned long long* out, int tiles) {
+// MODE 0: 24 MMAs back to back per tile; 1: the dQ pattern; 2: pattern
+// without waits; 3-5: the dQ pattern while 8 "compute" warps loop on their
+// own TMEM columns (3: tcgen05.ld/st only, 4: ld/st + ex2/FFMA2 on the
+// values, 5: ex2/FFMA2 only) — what the real kernels run next to the MMAs.
+template <int MODE>
+__global__ void __launch_bounds__(288, 1) k(unsigned long long* out, int tiles) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bars[8];
   __shared__ uint32_t tslot;
@@ -22,11 +26,49 @@ __global__ void __launch_bounds__(32, 1) k(unsigned long long* out, int tiles) {
     for (int i = 0; i < 8; ++i) mbar_init(&bars[i], 1);
     fence_barrier_init();
   }
-  tmem_alloc(&tslot, 512);
-  __syncwarp();
+  __shared__ volatile int stop;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) stop = 0;
+  if (warp == 0) tmem_alloc(&tslot, 512);
+  __syncthreads();
   fence_proxy_async_smem();
   tc_fence_after();
   const uint32_t tmem = tslot;
+  if (warp > 0) {  // background compute warps 1..8 on TMEM columns 0..127 of their lane quarter
+    if (MODE >= 3) {
+      const int q = (warp - 1) & 3, h = (warp - 1) >> 2;
+      const uint32_t lb = tmem + (static_cast<uint32_t>(q * 32) << 16) + h * 64;
+      uint32_t r[64];
+      float acc = 0.f;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) r[i] = __float_as_uint(float(lane + i) * 1e-3f);
+      while (!stop) {
+        if (MODE != 5) {
+          tmem_ld32(lb, r);
+          tmem_ld32(lb + 32, r + 32);
+          tmem_ld_wait(r);
+          tmem_ld_wait(r + 32);
+        }
+        if (MODE != 3) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float2 x = ffma2(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])),
+                                   make_float2(0.5f, 0.5f), make_float2(-1.f, -1.f));
+            r[2 * i] = __float_as_uint(ex2(x.x));
+            r[2 * i + 1] = __float_as_uint(ex2(x.y));
+          }
+        }
+        if (MODE != 5) {
+          tmem_st32(lb, r);
+          tmem_st_wait();
+        }
+        acc += __uint_as_float(r[0]) + __uint_as_float(r[63]);
+      }
+      if (acc == 1234.5f) out[1] = 1;
+    }
+    __syncthreads();
+    return;
+  }
   const uint32_t sa = smem_u32(base);
   const uint64_t ad = smem_desc_sw128(sa, 16, 1024);
   const uint64_t bd = smem_desc_sw128(sa + 32768, 16, 1024);
@@ -42,7 +84,7 @@ __global__ void __launch_bounds__(32, 1) k(unsigned long long* out, int tiles) {
     __syncwarp();
   };
   auto wait_done = [&](int b, int t) {  // a phase completed by this thread's own arrive
-    if (MODE == 1) {
+    if (MODE == 1 || MODE >= 3) {
       if (threadIdx.x == 0) mbar_arrive(&bars[b]);
       mbar_wait(&bars[b], t & 1);
       tc_fence_after();
@@ -76,7 +118,8 @@ __global__ void __launch_bounds__(32, 1) k(unsigned long long* out, int tiles) {
   mbar_wait(&bars[7], MODE == 0 ? 0 : (tiles & 1));
   const unsigned long long t1 = clock64();
   if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = (t1 - t0) / (tiles - 2);
-  __syncwarp();
+  if (threadIdx.x == 0) stop = 1;
+  __syncthreads();
   tmem_dealloc(tmem, 512);
 }
 
@@ -86,13 +129,15 @@ void run() {
   cudaMalloc(&d, 8);
   auto kern = k<MODE>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-  kern<<<148, 32, 100 * 1024>>>(d, 8);
+  kern<<<148, 288, 100 * 1024>>>(d, 8);
   cudaDeviceSynchronize();
-  kern<<<148, 32, 100 * 1024>>>(d, 202);
+  kern<<<148, 288, 100 * 1024>>>(d, 202);
   const cudaError_t e = cudaDeviceSynchronize();
   unsigned long long h = 0;
   cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-  const char* name[] = {"24 MMAs back to back", "dQ pattern (4 completed waits, 5 commits)", "dQ pattern, commits only"};
+  const char* name[] = {"24 MMAs back to back", "dQ pattern (4 completed waits, 5 commits)", "dQ pattern, commits only",
+                        "dQ pattern + 8 warps TMEM ld/st", "dQ pattern + 8 warps TMEM ld/st + ex2/FFMA2",
+                        "dQ pattern + 8 warps ex2/FFMA2"};
   printf("%-44s: %llu clk per tile (24 x 66 = 1584)  %s\n", name[MODE], h, cudaGetErrorString(e));
   cudaFree(d);
 }
@@ -101,5 +146,8 @@ int main() {
   run<0>();
   run<2>();
   run<1>();
+  run<3>();
+  run<4>();
+  run<5>();
   return 0;
 }
