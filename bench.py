@@ -8,8 +8,22 @@ One "step" = one USP attention forward (usp_attn_fwd through the C ABI) of
 the Llama-3-8B attention layer (hc=32, kv=8, hs=128, bs=1) at L=128K,
 causal with zigzag load balance, over a U x R mesh of N GPUs (default pure
 ring, U=1, R=N: config c3; N=1 is the single-GPU kernel). Inputs are
-synthetic bf16, resident in HBM; Q alone is 1 GiB, larger than the 126 MB
-L2, so no flush is needed between steps. Prints ONE JSON line on rank 0.
+synthetic: U[-1, 1) (the reference generator's range) drawn in
+fp32 by a seeded torch generator on the GPU, rounded to bf16 and resident in
+HBM; Q alone is 1 GiB, larger than the 126 MB L2, so no flush is needed
+between steps. Prints ONE JSON line on rank 0.
+
+Without WORLD_SIZE in the environment, --gpus N > 1 re-launches itself
+under torch.distributed.run (N local ranks, 127.0.0.1).
+
+Beside the throughput the line carries: `parity` (sampled query rows of the
+timed forward against the fp64 oracle on the same bf16 inputs, and against
+the reference's own fp32 SoftmaxState on the un-rounded inputs), `roofline`
+(the attention kernel vs the bf16 tensor peak), `whole_forward` (SURVEY
+§8(d)'s T_roof = A2A/BW + sum_t max(F_t/P, KV_t/BW) against the measured
+forward), `stages_ms_per_step` (pack / a2a / per-ring-step attention / the
+exposed part of each K/V shift / a2a out / unpack, CUDA events on the
+forward's stream) and `cpu_baseline`.
 
 --impl reference times the reference's own CPU implementation
 (oracle/_ref/libuspref.so: usp_attention<float> on U*R rank threads,
@@ -34,6 +48,22 @@ METRIC = "USP attn fwd TFLOP/s, L=128K Llama3-8B layer, 1/2/4/8 B200; % of BF16 
 UNIT = "TFLOP/s"
 
 
+def self_launch_if_needed(a) -> bool:
+    """--gpus N > 1 without a torch.distributed environment: run N local ranks
+    under torch.distributed.run (the driver may call `python bench.py --gpus N`)."""
+    if a.gpus <= 1 or "WORLD_SIZE" in os.environ or a.impl == "reference":
+        return False
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    rc = subprocess.run(cmd).returncode
+    raise SystemExit(rc)
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -53,6 +83,10 @@ def parse():
     ap.add_argument("--skip-cpu-baseline", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--parity-rows", type=int, default=12, help="sampled query rows checked vs the fp64 oracle")
+    ap.add_argument("--parity-ref-rows", type=int, default=4,
+                    help="sampled rows checked vs the reference's fp32 SoftmaxState")
+    ap.add_argument("--skip-parity", action="store_true")
     return ap.parse_args()
 
 
@@ -218,6 +252,165 @@ def run_reference_arm(a):
 
 
 # ------------------------------------------------------------------- ours
+def global_inputs(a, dev):
+    """Global Q, K, V (fp32, U[-1, 1)) from one seeded stream in Q, K, V order
+    (the reference fills Q, K, V from one UniformSource, commands.cpp:90-102)."""
+    import torch
+
+    gen = torch.Generator(device=dev).manual_seed(0)
+    L = a.seq_len
+
+    def draw(h):
+        return torch.rand((1, L, h, a.head_size), device=dev, dtype=torch.float32, generator=gen).mul_(2).sub_(1)
+
+    return draw(a.heads), draw(a.kv_heads), draw(a.kv_heads)
+
+
+def parity_block(a, eng, g, out, lse, positions, U, rank_u):
+    """Sampled rows of this rank's timed forward vs (i) the fp64 oracle on the
+    same bf16 inputs and (ii) the reference's own fp32 SoftmaxState on the
+    un-rounded fp32 inputs (commands.cpp:142-158)."""
+    import numpy as np
+    import torch
+
+    from oracle.oracle import Oracle, Reference
+
+    t0 = time.perf_counter()
+    T = len(positions)
+    hl = a.heads // U
+    rng = np.random.default_rng(7)
+    cand = [0, 1, T // 2 - 1, T // 2, T - 2, T - 1] + rng.integers(0, T, size=64).tolist()
+    rows = sorted(set(cand))[: max(1, a.parity_rows)]
+    rows = sorted(set([0, T - 1] + rows))[: max(2, a.parity_rows)]
+    qpos = np.array([positions[i] for i in rows], np.int64)
+    qf, kf, vf = g
+    bf = lambda t: t.to(torch.bfloat16).double().cpu().numpy()  # noqa: E731
+    q_rows_b = bf(qf[:, torch.tensor(qpos, device=qf.device)])
+    kb, vb = bf(kf), bf(vf)
+    kpos = np.arange(a.seq_len, dtype=np.int64)
+    causal = not a.non_causal
+    ref_o, ref_l = Oracle.softmax_rows(q_rows_b, kb, vb, causal, qpos, kpos)
+    got_o = out[:, torch.tensor(rows, device=out.device)].double().cpu().numpy()
+    hp = eng.head_positions()
+    hidx = {p: i for i, p in enumerate(hp)}
+    got_l = lse[:, torch.tensor([hidx[int(p)] for p in qpos], device=lse.device)].double().cpu().numpy()
+    ref_l_loc = ref_l[:, :, rank_u * hl:(rank_u + 1) * hl]
+
+    def errs(got, want):
+        d = np.abs(got - want)
+        return float(d.max()), float(np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-300))
+
+    o_abs, o_rel = errs(got_o, ref_o)
+    l_abs, _ = errs(got_l, ref_l_loc)
+    tol = {"o_max_abs": 5e-3, "o_rel_l2": 3e-3, "lse_max_abs": 1e-4}
+    blk = {"rows": len(rows), "heads": a.heads, "keys": a.seq_len,
+           "oracle": "fp64 SoftmaxState restatement (oracle/usp_oracle.c, pinned bitwise to the reference) on "
+                     "the same bf16-rounded inputs; O rows in positions_for order, LSE head-sharded",
+           "o_max_abs": o_abs, "o_rel_l2": o_rel, "lse_max_abs": l_abs, "tol": tol,
+           "pass": o_abs <= tol["o_max_abs"] and o_rel <= tol["o_rel_l2"] and l_abs <= tol["lse_max_abs"]}
+    nref = min(a.parity_ref_rows, len(rows))
+    if nref > 0 and Reference.available():
+        import concurrent.futures as cf
+
+        sel = np.linspace(0, len(rows) - 1, nref).astype(int)
+        qf_rows = qf[:, torch.tensor(qpos[sel], device=qf.device)].double().cpu().numpy()
+        kd, vd = kf.double().cpu().numpy(), vf.double().cpu().numpy()
+
+        def one(j):
+            return Reference.softmax_rows(qf_rows[:, j:j + 1], kd, vd, causal, qpos[sel][j:j + 1], kpos,
+                                          precision="fp32")
+
+        with cf.ThreadPoolExecutor(max_workers=nref) as ex:
+            res = list(ex.map(one, range(nref)))
+        r_o = np.concatenate([r[0] for r in res], axis=1)
+        r_l = np.concatenate([r[1] for r in res], axis=1)[:, :, rank_u * hl:(rank_u + 1) * hl]
+        fo_abs, fo_rel = errs(got_o[:, sel], r_o)
+        fl_abs, _ = errs(got_l[:, sel], r_l)
+        blk["vs_reference_fp32"] = {
+            "rows": nref, "o_max_abs": fo_abs, "o_rel_l2": fo_rel, "lse_max_abs": fl_abs,
+            "reference": "the reference's SoftmaxState<float>::update/finalize/logsumexp (oracle/_ref, built "
+                         "from /root/reference sources) on the un-rounded fp32 inputs: the difference includes "
+                         "the bf16 rounding of Q/K/V the GPU path takes"}
+    blk["seconds"] = time.perf_counter() - t0
+    return blk
+
+
+def nccl_bandwidth(dev, world, U, R, rank, same_dev):
+    """Measured NCCL bus bandwidth on this node for the two exchanges (GB/s of
+    bytes sent per rank): all_to_all over the Ulysses rows and the ring
+    send/recv over the columns, 64 MiB per rank, CUDA events, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    if world == 1 or same_dev:
+        return None
+    out = {}
+    nbytes = 64 << 20
+    x = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    y = torch.empty_like(x)
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # all_to_all over the whole world as a proxy for one Ulysses row (every
+    # peer is one NVSwitch hop away)
+    for _ in range(3):
+        dist.all_to_all_single(y, x)
+    torch.cuda.synchronize(dev)
+    s0.record()
+    for _ in range(5):
+        dist.all_to_all_single(y, x)
+    s1.record()
+    torch.cuda.synchronize(dev)
+    ms = s0.elapsed_time(s1) / 5
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    out["a2a_gbs"] = nbytes * (world - 1) / world / (t.item() * 1e-3) / 1e9
+    nxt, prv = (rank + 1) % world, (rank - 1) % world
+    for it in range(8):
+        if it == 3:
+            torch.cuda.synchronize(dev)
+            s0.record()
+        ops = [dist.P2POp(dist.isend, x, nxt), dist.P2POp(dist.irecv, y, prv)]
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+    s1.record()
+    torch.cuda.synchronize(dev)
+    ms = s0.elapsed_time(s1) / 5
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    out["p2p_gbs"] = nbytes / (t.item() * 1e-3) / 1e9
+    out["kind"] = "measured: torch.distributed NCCL all_to_all_single / ring send-recv, 64 MiB per rank"
+    return out
+
+
+def whole_forward_roofline(eng, U, R, ms, peak, bw):
+    """T_roof = A2A_bytes/BW_a2a + sum_t max(F_t/P, KV_t/BW_p2p)
+    per rank; frac = T_roof / T_measured."""
+    from paper_2405_07719_b200.usp import forward_ledger, schedule
+
+    cfg = eng.cfg
+    led = forward_ledger(cfg)
+    a2a = sum(e["bytes_sent"] for e in led if e["kind"] == 3)
+    nominal = 900.0
+    bw_a2a = (bw or {}).get("a2a_gbs") or nominal
+    bw_p2p = (bw or {}).get("p2p_gbs") or nominal
+    hl = cfg.heads // U
+    t = a2a / (bw_a2a * 1e9)
+    terms, comm_bound = [], 0
+    for st in range(R):
+        info = schedule(cfg, st)
+        f = 4.0 * cfg.batch * hl * cfg.head_size * info.visible_pairs
+        tc = f / (peak * 1e12)
+        tk = info.ring_bytes_sent / (bw_p2p * 1e9)
+        terms.append(max(tc, tk))
+        comm_bound += tk > tc
+    t += sum(terms)
+    return {"t_roof_ms": t * 1e3, "t_measured_ms": ms, "frac": (t * 1e3) / ms, "a2a_bytes_per_rank": a2a,
+            "kv_bytes_per_shift": schedule(cfg, 0).ring_bytes_sent if R > 1 else 0,
+            "bw_a2a_gbs": bw_a2a, "bw_p2p_gbs": bw_p2p,
+            "bw_kind": (bw or {}).get("kind", "nominal NVLink 5 (900 GB/s per direction)") if U * R > 1 else "n/a",
+            "peak_tflops": peak, "ring_steps_comm_bound": comm_bound,
+            "a2a_ms": a2a / (bw_a2a * 1e9) * 1e3}
+
+
 def run_ours(a):
     import torch
     import torch.distributed as dist
@@ -264,10 +457,16 @@ def run_ours(a):
     causal = not a.non_causal
     eng = UspAttention(mesh, rank=rank, seq_len=a.seq_len, heads=a.heads, kv_heads=a.kv_heads,
                        head_size=a.head_size, causal=causal, device=local, comm=comm)
-    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
-    q = torch.randn(eng.q_shape(), device=dev, dtype=torch.bfloat16, generator=gen)
-    k = torch.randn(eng.kv_shape(), device=dev, dtype=torch.bfloat16, generator=gen)
-    v = torch.randn(eng.kv_shape(), device=dev, dtype=torch.bfloat16, generator=gen)
+    # global U[-1, 1) inputs (identical on every rank: same seed), this rank's
+    # rows = ShardSpec::positions_for(rank) (zigzag when causal)
+    positions = eng.positions()
+    pos_t = torch.tensor(positions, dtype=torch.long, device=dev)
+    g = global_inputs(a, dev)
+    q, k, v = (x[:, pos_t].to(torch.bfloat16).contiguous() for x in g)
+    if rank != 0 or a.skip_parity:
+        del g
+        g = None
+    torch.cuda.empty_cache()
     o, lse = eng.alloc_outputs()
     stream = torch.cuda.current_stream(dev)
 
@@ -305,6 +504,7 @@ def run_ours(a):
     clk = clocks.stop()
     ms = t0.elapsed_time(t1) / a.steps
     kts = eng.kernel_times()
+    stages = {x["stage"]: x["ms_total"] / a.steps for x in eng.stage_times()}
     eng.enable_timing(False)
     ms = max_over_ranks(ms)
 
@@ -366,8 +566,19 @@ def run_ours(a):
                "path": "paper_2405_07719_b200.UspAttention.forward_host -> usp_attn_fwd_host (C ABI, pinned host "
                        "buffers; H2D/D2H pipelined against the attention in sequence chunks at U=R=1)"}
 
+    bw = nccl_bandwidth(dev, world, U, R, rank, same_dev) if distributed else None
+    whole = whole_forward_roofline(eng, U, R, ms, peak, bw)
+
+    parity = None
+    if rank == 0 and not a.skip_parity:
+        try:
+            parity = parity_block(a, eng, g, o, lse, positions, U, mesh.ulysses_coord(rank))
+        except Exception as e:  # reported, not fatal
+            parity = {"error": repr(e)}
+    g = None
+
     cpu = None
-    if rank == 0 and n == 1 and not a.skip_cpu_baseline:
+    if rank == 0 and not a.skip_cpu_baseline:
         try:
             cpu = cpu_reference_sample(a, repeats=2)
         except Exception as e:  # reported, not fatal
@@ -377,11 +588,13 @@ def run_ours(a):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "bf16", "data": "synthetic (torch.randn bf16, resident in HBM)",
+            "dtype": "bf16",
+            "data": "synthetic U[-1,1) (seeded torch generator, fp32 rounded to bf16), resident in HBM",
             "config": workload_config(a, n, U, R),
             "pct_of_peak_per_gpu": value / n / peak * 100.0,
             "tokens_per_s": a.seq_len / (ms * 1e-3),
-            "roofline": roofline, "cpu_baseline": cpu, "clocks": clk, "e2e": e2e,
+            "roofline": roofline, "whole_forward": whole, "stages_ms_per_step": stages, "parity": parity,
+            "cpu_baseline": cpu, "clocks": clk, "e2e": e2e,
             "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
@@ -392,6 +605,7 @@ def run_ours(a):
 
 def main():
     a = parse()
+    self_launch_if_needed(a)
     if a.impl == "reference":
         run_reference_arm(a)
     else:

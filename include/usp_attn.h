@@ -195,6 +195,26 @@ USP_API void usp_engine_destroy(usp_engine* engine);
  * were recorded since the last call (-1 on error). */
 USP_API usp_status usp_engine_enable_timing(usp_engine* engine, int32_t on);
 USP_API int32_t usp_engine_kernel_times(usp_engine* engine, float* ms, int32_t cap);
+/* Per-stage breakdown of the forwards run while timing was on (events on
+ * the caller's stream after each stage; a stage's time is the gap to the
+ * previous one): pack, a2a_in (or pack_a2a_in for the direct peer-memory
+ * exchange), wait<t> (exposed part of the K/V shift into ring step t),
+ * attn<t>, a2a_out, unpack; shift<t> is the K/V transfer itself on the comm
+ * stream. Summed per name over the forwards (count = how many). Synchronises
+ * and clears; returns the number of stages (written up to cap), -1 on error. */
+typedef struct usp_stage_time {
+  char name[24];
+  double ms_total;
+  int32_t count;
+} usp_stage_time;
+USP_API int32_t usp_engine_stage_times(usp_engine* engine, usp_stage_time* out, int32_t cap);
+/* Parity instrumentation (tests): while on, the forward kernel counts every
+ * (warp, key tile) whose lazy O rescale fired, i.e. the running row max grew
+ * by more than 8 in log2 units and O was multiplied by alpha = 2^(m_old -
+ * m_new) (SoftmaxState::update's rescale, attention.cpp:209-226). Turning it
+ * on or off resets the count; rescale_count synchronises the device. */
+USP_API usp_status usp_engine_debug_counters(usp_engine* engine, int32_t on);
+USP_API usp_status usp_engine_rescale_count(usp_engine* engine, int64_t* out);
 
 /* Runs usp_attn_fwd on every rank of a local world, one host thread per
  * rank (engines[i] must belong to rank i); blocks until all are issued. */

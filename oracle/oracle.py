@@ -180,8 +180,9 @@ class Reference(_Lib):
         lib.ref_uniform_stream.argtypes = [ctypes.c_uint64, ctypes.c_double, ctypes.c_double, _i64, _f64p]
         lib.ref_reference_attention_f64.argtypes = [_f64p, _f64p, _f64p, _i64, _i64, _i64, _i64, _i64, _int,
                                                     ctypes.c_void_p, _f64p]
-        lib.ref_softmax_rows_f64.argtypes = [_f64p, _f64p, _f64p, _i64, _i64, _i64, _i64, _i64, _i64, _int,
-                                             _i64p, _i64p, _f64p, _f64p]
+        for name in ("ref_softmax_rows_f64", "ref_softmax_rows_f32"):
+            getattr(lib, name).argtypes = [_f64p, _f64p, _f64p, _i64, _i64, _i64, _i64, _i64, _i64, _int,
+                                           _i64p, _i64p, _f64p, _f64p]
         lib.ref_zigzag_partition.argtypes = [_i64, _int, _i64p]
         lib.ref_positions_for.argtypes = [_int, _int, _i64, _int, _int, _i64p]
         lib.ref_causal_pair_counts.argtypes = [_i64p, _int, _i64, _i64p]
@@ -212,12 +213,17 @@ class Reference(_Lib):
         return out
 
     @classmethod
-    def softmax_rows(cls, q, k, v, causal: bool, q_pos, k_pos):
+    def softmax_rows(cls, q, k, v, causal: bool, q_pos, k_pos, precision: str = "fp64"):
+        """The reference's SoftmaxState<T>::update + finalize + logsumexp of
+        query rows ``q`` against keys ``k_pos``; precision "fp32" runs
+        SoftmaxState<float> on the float-cast inputs (the reference's fp32
+        path), results widened to fp64."""
         q, k, v = _as(q), _as(k), _as(v)
         b, n, h, d = q.shape
         out = np.empty_like(q)
         lse = np.empty((b, n, h), np.float64)
-        cls._check(cls.lib().ref_softmax_rows_f64(q, k, v, b, n, k.shape[1], h, k.shape[2], d, int(causal),
+        fn = cls.lib().ref_softmax_rows_f64 if precision == "fp64" else cls.lib().ref_softmax_rows_f32
+        cls._check(fn(q, k, v, b, n, k.shape[1], h, k.shape[2], d, int(causal),
                                                   _as(q_pos, np.int64), _as(k_pos, np.int64), out, lse))
         return out, lse
 

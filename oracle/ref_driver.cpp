@@ -126,6 +126,26 @@ int usp_forward_impl(const double* q, const double* k, const double* v,
     }
   });
 }
+template <class T>
+int softmax_rows_impl(const double* q, const double* k, const double* v, int64_t batch, int64_t q_len,
+                      int64_t k_len, int64_t heads, int64_t kv_heads, int64_t hs, int causal,
+                      const int64_t* q_pos, const int64_t* k_pos, double* out, double* lse) {
+  return guarded([&] {
+    const auto tq = make<T>(q, batch, q_len, heads, hs);
+    const auto tk = make<T>(k, batch, k_len, kv_heads, hs);
+    const auto tv = make<T>(v, batch, k_len, kv_heads, hs);
+    numerics::SoftmaxState<T> st(batch, q_len, heads, hs);
+    const auto mask =
+        causal ? numerics::BlockMask::causal(
+                     std::span<const int64_t>(q_pos, static_cast<size_t>(q_len)),
+                     std::span<const int64_t>(k_pos, static_cast<size_t>(k_len)))
+               : numerics::BlockMask::none();
+    st.update(tq, tk, tv, mask);
+    const auto l = st.logsumexp();
+    for (size_t i = 0; i < l.size(); ++i) lse[i] = static_cast<double>(l[i]);
+    unload(st.finalize(), out);
+  });
+}
 }  // namespace
 
 extern "C" {
@@ -156,26 +176,25 @@ int ref_reference_attention_f64(const double* q, const double* k, const double* 
 
 // One SoftmaxState update of a query subset against a key block, then
 // finalize() + logsumexp(); the sampled-row oracle of SURVEY §8(c) step 5.
+// The _f32 variant is the reference's own fp32 path (commands.cpp:142-153
+// casts the generator's doubles to float), used by bench.py's parity block
+// for "bf16 GPU vs fp32 CPU".
 int ref_softmax_rows_f64(const double* q, const double* k, const double* v,
                          int64_t batch, int64_t q_len, int64_t k_len, int64_t heads,
                          int64_t kv_heads, int64_t hs, int causal,
                          const int64_t* q_pos, const int64_t* k_pos, double* out,
                          double* lse) {
-  return guarded([&] {
-    const auto tq = make<double>(q, batch, q_len, heads, hs);
-    const auto tk = make<double>(k, batch, k_len, kv_heads, hs);
-    const auto tv = make<double>(v, batch, k_len, kv_heads, hs);
-    numerics::SoftmaxState<double> st(batch, q_len, heads, hs);
-    const auto mask =
-        causal ? numerics::BlockMask::causal(
-                     std::span<const int64_t>(q_pos, static_cast<size_t>(q_len)),
-                     std::span<const int64_t>(k_pos, static_cast<size_t>(k_len)))
-               : numerics::BlockMask::none();
-    st.update(tq, tk, tv, mask);
-    const auto l = st.logsumexp();
-    std::memcpy(lse, l.data(), l.size() * sizeof(double));
-    unload(st.finalize(), out);
-  });
+  return softmax_rows_impl<double>(q, k, v, batch, q_len, k_len, heads, kv_heads, hs, causal, q_pos,
+                                   k_pos, out, lse);
+}
+
+int ref_softmax_rows_f32(const double* q, const double* k, const double* v,
+                         int64_t batch, int64_t q_len, int64_t k_len, int64_t heads,
+                         int64_t kv_heads, int64_t hs, int causal,
+                         const int64_t* q_pos, const int64_t* k_pos, double* out,
+                         double* lse) {
+  return softmax_rows_impl<float>(q, k, v, batch, q_len, k_len, heads, kv_heads, hs, causal, q_pos,
+                                  k_pos, out, lse);
 }
 
 int ref_zigzag_partition(int64_t seq_len, int ring, int64_t* out) {

@@ -73,13 +73,18 @@ class UspLedgerEntry(ctypes.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
 
+class UspStageTime(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 24), ("ms_total", ctypes.c_double), ("count", ctypes.c_int32)]
+
+
 # Every symbol include/usp_attn.h declares (tests check the .so exports them).
 EXPORTS = [
     "usp_config_validate", "usp_zigzag_partition", "usp_positions_for", "usp_head_positions",
     "usp_causal_pair_counts", "usp_schedule", "usp_step_plan", "usp_forward_ledger", "usp_engine_ledger", "usp_rank_flops", "usp_nccl_unique_id",
     "usp_comm_create_nccl", "usp_comm_create_local", "usp_comm_destroy", "usp_engine_create",
     "usp_attn_fwd", "usp_engine_last_launches", "usp_engine_destroy", "usp_engine_enable_timing",
-    "usp_engine_kernel_times", "usp_local_world_fwd", "usp_attn_bwd", "usp_local_world_bwd",
+    "usp_engine_kernel_times", "usp_engine_debug_counters", "usp_engine_rescale_count",
+    "usp_engine_stage_times", "usp_local_world_fwd", "usp_attn_bwd", "usp_local_world_bwd",
     "usp_backward_ledger", "usp_attn_fwd_host", "usp_comm_create_p2p",
     "usp_last_error", "usp_version",
 ]
@@ -127,6 +132,9 @@ def _declare(lib):
         "usp_engine_destroy": (None, [vp]),
         "usp_engine_enable_timing": (st, [vp, ctypes.c_int32]),
         "usp_engine_kernel_times": (ctypes.c_int32, [vp, P(ctypes.c_float), ctypes.c_int32]),
+        "usp_engine_debug_counters": (st, [vp, ctypes.c_int32]),
+        "usp_engine_stage_times": (ctypes.c_int32, [vp, P(UspStageTime), ctypes.c_int32]),
+        "usp_engine_rescale_count": (st, [vp, i64p]),
         "usp_local_world_fwd": (st, [P(vp), ctypes.c_int32, P(vp), P(vp), P(vp), P(vp), P(vp), P(vp)]),
         "usp_last_error": (ctypes.c_char_p, []),
         "uspsim_run": (st, [ctypes.c_char_p, P(vp)]),

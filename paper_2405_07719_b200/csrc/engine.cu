@@ -227,7 +227,16 @@ class Engine {
   }
 
   ~Engine() {
+    if (tr_) {
+      try {  // peer-memory mappings of this engine's buffers (advice r1)
+        tr_->release_buffers({q_h_.p, kv0_.p, o_h_.p, send_.p, recv_.p, o_send_.p, o_recv_.p, kv_ring_[0].p,
+                              kv_ring_[1].p, do_h_.p, grad_h_.p, grad_recv_.p, acc_dkv_[0].p, acc_dkv_[1].p,
+                              own_dkv_.p, dq_acc_.p});
+      } catch (...) {
+      }
+    }
     for (auto e : event_pool_) cudaEventDestroy(e);
+    for (auto e : stage_pool_) cudaEventDestroy(e);
     for (auto e : ev_pre_) cudaEventDestroy(e);
     for (auto e : ev_recv_) cudaEventDestroy(e);
     for (auto e : ev_acc_) cudaEventDestroy(e);
@@ -264,6 +273,7 @@ class Engine {
     launches_ = 0;
     ledger_.clear();
     have_fwd_ = false;
+    stage_begin(st);
     const size_t e = 2;
     const bool reshape = U_ > 1 || hs_ != hsk_;
     const void* qh = q;
@@ -295,6 +305,7 @@ class Engine {
         pack_part(v, static_cast<uint8_t*>(pkv[m]) + kv_bytes_ + u_ * kv_part_, KV_, kvl_, m, st);
       }
       tr_->ulysses_done(*groups_, st);  // every member's parts for me have landed
+      stage(st, "pack_a2a_in");
       record_a2a(0, q_part_);
       record_a2a(1, kv_part_);
       record_a2a(2, kv_part_);
@@ -309,6 +320,7 @@ class Engine {
       pack_heads(q, sq, H_, hl_, st);
       pack_heads(k, sk, KV_, kvl_, st);
       pack_heads(v, sv, KV_, kvl_, st);
+      stage(st, "pack");
       uint8_t* rq = B_ > 1 ? recv_.as<uint8_t>() : nullptr;
       uint8_t* rk = rq ? rq + U_ * q_part_ : nullptr;
       uint8_t* rv = rk ? rk + U_ * kv_part_ : nullptr;
@@ -321,6 +333,7 @@ class Engine {
         parts[2][p] = {sv + p * kv_part_, rv ? rv + p * kv_part_ : kv0 + kv_bytes_ + p * kv_part_};
       }
       tr_->all_to_all(*groups_, parts, {q_part_, kv_part_, kv_part_}, st);
+      stage(st, "a2a_in");
       record_a2a(0, q_part_);
       record_a2a(1, kv_part_);
       record_a2a(2, kv_part_);
@@ -328,6 +341,7 @@ class Engine {
         gather_seq(rq, q_h_.p, hl_, st);
         gather_seq(rk, kv0, kvl_, st);
         gather_seq(rv, kv0 + kv_bytes_, kvl_, st);
+        stage(st, "unpack_in");
       }
       qh = q_h_.p;
       kh = kv0;
@@ -343,6 +357,7 @@ class Engine {
       pad_rows(q, q_h_.p, B_ * T_ * H_, st);
       pad_rows(k, kv0, B_ * T_ * KV_, st);
       pad_rows(v, kv0 + kv_bytes_, B_ * T_ * KV_, st);
+      stage(st, "pad");
       qh = q_h_.p;
       kh = kv0;
       vh = kv0 + kv_bytes_;
@@ -372,34 +387,45 @@ class Engine {
         USPB_CHECK(cudaStreamWaitEvent(comm_stream_, ev_pre_[t], 0));
         record_shift(1);
         record_shift(2);
+        cudaEvent_t sh0 = side_event(comm_stream_);
         tr_->ring_shift(*groups_, {kbuf(t), vbuf(t)},
                         {const_cast<void*>(kbuf(t + 1)), const_cast<void*>(vbuf(t + 1))},
                         {kv_bytes_, kv_bytes_}, comm_stream_);
+        side_span("shift" + std::to_string(t + 1), sh0, side_event(comm_stream_));
         USPB_CHECK(cudaEventRecord(ev_recv_[t], comm_stream_));
       }
-      if (t > 0) USPB_CHECK(cudaStreamWaitEvent(st, ev_recv_[t - 1], 0));
+      if (t > 0) {
+        USPB_CHECK(cudaStreamWaitEvent(st, ev_recv_[t - 1], 0));
+        stage(st, "wait" + std::to_string(t));  // exposed part of the shift into step t
+      }
       const bool last = t == R_ - 1;
       if (direct_o && last) tr_->ulysses_ready(*groups_, st);  // every member's o_recv_ is free
       launch_step(t, tm_q, kbuf(t), vbuf(t), o_heads, lse, st, direct_o && last ? o_peer : nullptr);
+      stage(st, "attn" + std::to_string(t));
     }
 
     // -- 3. Ulysses out: [peer][b][T][H/U] -> (b, T, H, hs)
     if (direct_o) {
       tr_->ulysses_done(*groups_, st);  // every member's rows for me have landed
+      stage(st, "a2a_out");
       record_a2a(3, q_part_);
       unpack_heads(o_recv_.p, o, st);
+      stage(st, "unpack");
     } else if (U_ > 1) {
       uint8_t* osend = o_h_.as<uint8_t>();
       if (B_ > 1) {
         split_seq(o_h_.p, o_send_.p, st);
         osend = o_send_.as<uint8_t>();
+        stage(st, "pack_out");
       }
       std::vector<std::vector<A2APart>> parts(1, std::vector<A2APart>(U_));
       for (int p = 0; p < U_; ++p)
         parts[0][p] = {osend + p * q_part_, o_recv_.as<uint8_t>() + p * q_part_};
       tr_->all_to_all(*groups_, parts, {q_part_}, st);
+      stage(st, "a2a_out");
       record_a2a(3, q_part_);
       unpack_heads(o_recv_.p, o, st);
+      stage(st, "unpack");
     } else {
       record_a2a(3, q_part_);
     }
@@ -412,6 +438,7 @@ class Engine {
       rp.hs_src = hsk_;
       rp.hs_dst = hs_;
       permute(rp, st);
+      stage(st, "unpad");
     }
     (void)e;
     have_fwd_ = true;
@@ -1149,6 +1176,7 @@ class Engine {
       return e ? std::atoi(e) : 0;
     }();
     p.debug_flags = dbg;
+    p.rescale_count = count_rescale_ ? dbg_count_.as<unsigned long long>() : nullptr;
     static const bool trace = std::getenv("USP_FA_TRACE") != nullptr;
     if (trace) {
       if (!trace_buf_.p) trace_buf_ = DevBuf(sizeof(unsigned long long) * kTraceTiles * kTraceEvents);
@@ -1185,9 +1213,69 @@ class Engine {
   }
 
  public:
+  // Per-stage timing of the forward (bench.py's breakdown): while timing is
+  // on, fwd() records an event on the caller's stream after every stage
+  // (pack, a2a_in, wait<t> = the exposed part of the K/V shift into step t,
+  // attn<t>, a2a_out, unpack, ...); a stage's time is the gap to the previous
+  // event. Comm-stream spans (shift<t>: the K/V transfer itself) are timed
+  // between their own two events.
+  struct StageTime {
+    std::string name;
+    double ms = 0;
+    int count = 0;
+  };
+  std::vector<StageTime> stage_times() {
+    std::vector<StageTime> out;
+    auto add = [&](const std::string& n, float ms) {
+      for (auto& x : out)
+        if (x.name == n) {
+          x.ms += ms;
+          ++x.count;
+          return;
+        }
+      out.push_back({n, ms, 1});
+    };
+    for (const auto& run : stage_runs_) {
+      for (size_t i = 1; i < run.size(); ++i) {
+        USPB_CHECK(cudaEventSynchronize(run[i].second));
+        float ms = 0.f;
+        USPB_CHECK(cudaEventElapsedTime(&ms, run[i - 1].second, run[i].second));
+        add(run[i].first, ms);
+      }
+    }
+    for (const auto& sp : side_spans_) {
+      USPB_CHECK(cudaEventSynchronize(sp.end));
+      float ms = 0.f;
+      USPB_CHECK(cudaEventElapsedTime(&ms, sp.begin, sp.end));
+      add(sp.name, ms);
+    }
+    stage_runs_.clear();
+    side_spans_.clear();
+    stage_used_ = 0;
+    return out;
+  }
+
+  // Parity instrumentation: counts the forward kernel's lazy O rescales.
+  void debug_counters(bool on) {
+    USPB_CHECK(cudaSetDevice(cfg_.device));
+    if (!dbg_count_.p) dbg_count_ = DevBuf(sizeof(unsigned long long));
+    USPB_CHECK(cudaMemset(dbg_count_.p, 0, sizeof(unsigned long long)));
+    count_rescale_ = on;
+  }
+  int64_t rescale_count() {
+    if (!dbg_count_.p) return 0;
+    USPB_CHECK(cudaSetDevice(cfg_.device));
+    unsigned long long v = 0;
+    USPB_CHECK(cudaDeviceSynchronize());
+    USPB_CHECK(cudaMemcpy(&v, dbg_count_.p, sizeof(v), cudaMemcpyDeviceToHost));
+    return static_cast<int64_t>(v);
+  }
   void enable_timing(bool on) {
     timing_ = on;
     timed_.clear();
+    stage_runs_.clear();
+    side_spans_.clear();
+    stage_used_ = 0;
   }
   int kernel_times(float* ms, int cap) {
     int n = 0;
@@ -1203,7 +1291,45 @@ class Engine {
   }
 
  private:
+  struct SideSpan {
+    std::string name;
+    cudaEvent_t begin, end;
+  };
+  std::vector<std::vector<std::pair<std::string, cudaEvent_t>>> stage_runs_;
+  std::vector<SideSpan> side_spans_;
+  std::vector<cudaEvent_t> stage_pool_;
+  size_t stage_used_ = 0;
+  cudaEvent_t stage_event() {
+    if (stage_used_ == stage_pool_.size()) {
+      cudaEvent_t e;
+      USPB_CHECK(cudaEventCreate(&e));
+      stage_pool_.push_back(e);
+    }
+    return stage_pool_[stage_used_++];
+  }
+  void stage_begin(cudaStream_t st) {
+    if (!timing_) return;
+    stage_runs_.emplace_back();
+    stage(st, "begin");
+  }
+  void stage(cudaStream_t st, const std::string& name) {
+    if (!timing_ || stage_runs_.empty()) return;
+    cudaEvent_t e = stage_event();
+    USPB_CHECK(cudaEventRecord(e, st));
+    stage_runs_.back().emplace_back(name, e);
+  }
+  cudaEvent_t side_event(cudaStream_t st) {
+    if (!timing_) return nullptr;
+    cudaEvent_t e = stage_event();
+    USPB_CHECK(cudaEventRecord(e, st));
+    return e;
+  }
+  void side_span(const std::string& name, cudaEvent_t b, cudaEvent_t e) {
+    if (b && e) side_spans_.push_back({name, b, e});
+  }
   bool timing_ = false;
+  bool count_rescale_ = false;
+  DevBuf dbg_count_;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed_;
   std::vector<cudaEvent_t> event_pool_;
 
@@ -1538,6 +1664,33 @@ usp_status usp_engine_enable_timing(usp_engine* engine, int32_t on) {
     if (!engine) throw_invalid("engine is null");
     engine->impl->enable_timing(on != 0);
   });
+}
+
+int32_t usp_engine_stage_times(usp_engine* engine, usp_stage_time* out, int32_t cap) {
+  if (!engine) return -1;
+  int32_t n = -1;
+  if (guarded([&] {
+        const auto st = engine->impl->stage_times();
+        for (size_t i = 0; i < st.size() && static_cast<int32_t>(i) < cap && out; ++i) {
+          std::memset(&out[i], 0, sizeof(out[i]));
+          std::strncpy(out[i].name, st[i].name.c_str(), sizeof(out[i].name) - 1);
+          out[i].ms_total = st[i].ms;
+          out[i].count = st[i].count;
+        }
+        n = static_cast<int32_t>(st.size());
+      }) != USP_OK)
+    return -1;
+  return n;
+}
+
+usp_status usp_engine_debug_counters(usp_engine* engine, int32_t on) {
+  if (!engine) return USP_INVALID_INPUT;
+  return guarded([&] { engine->impl->debug_counters(on != 0); });
+}
+
+usp_status usp_engine_rescale_count(usp_engine* engine, int64_t* out) {
+  if (!engine || !out) return USP_INVALID_INPUT;
+  return guarded([&] { *out = engine->impl->rescale_count(); });
 }
 
 int32_t usp_engine_kernel_times(usp_engine* engine, float* ms, int32_t cap) {

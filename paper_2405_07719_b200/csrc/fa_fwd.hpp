@@ -69,6 +69,10 @@ struct FwdParams {
   // first kTraceTiles tiles, [event][tile]; see tools/trace_fa.py.
   unsigned long long* trace;
   int debug_flags;  // development: bit 0 = skip the softmax math (pipeline-only timing)
+  // Parity instrumentation (nullptr in production): +1 per (warp, key tile)
+  // whose lazy O rescale fired (running max grew by > 8 in log2 units), so
+  // the tests can prove the alpha != 1 branch ran (usp_engine_debug_counters).
+  unsigned long long* rescale_count;
 };
 
 // cudaFuncSetAttribute is per device: opt a kernel in to its dynamic shared

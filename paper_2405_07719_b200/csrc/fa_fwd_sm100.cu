@@ -386,6 +386,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
 #pragma unroll
         for (int c = 0; c < KC / 64; ++c) tmem_st32(p_addr + c * 32, s + c * 32);
         if (__any_sync(0xffffffffu, alpha != 1.f)) {
+          if (p.rescale_count != nullptr && lane == 0) atomicAdd(p.rescale_count, 1ull);
 #pragma unroll
           for (int c = 0; c < HS / SPL / 32; ++c) {
             uint32_t o[32];

@@ -92,6 +92,10 @@ void UspShape::validate() const {
     throw_invalid(os.str());
   }
   if (batch > 255) throw_invalid("batch above 255 is not supported by the work-unit encoding");
+  // work units carry the (local) head index in 8 bits (plan.cpp units,
+  // kernels decode (unit >> 16) & 0xFF)
+  if (heads / ulysses > 256 || kv_heads / ulysses > 256)
+    throw_invalid("more than 256 heads per Ulysses rank is not supported by the work-unit encoding");
   if (tokens_per_ring_rank() > INT32_MAX / 2 || seq_len > INT32_MAX / 2)
     throw_invalid("sequence length exceeds the int32 position range");
   if ((tokens_per_ring_rank() + kTileM - 1) / kTileM > 65535)

@@ -16,6 +16,7 @@
 #include <condition_variable>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <sstream>
 #include <string>
@@ -228,8 +229,14 @@ class NcclTransport final : public Transport {
   int world_size() const override { return n_; }
   int reserved_sms() const override { return env_int("USP_RESERVED_SMS", max_ctas_); }
 
+  // Engines of the same mesh share the two sub-communicators: the splits
+  // are collective over the world and every rank creates its engines in the
+  // same order, so every rank hits (or misses) this cache together.
   std::shared_ptr<Groups> make_groups(int rank, const std::vector<int>& ug,
                                       const std::vector<int>& rg) override {
+    const auto key = std::make_pair(ug, rg);
+    auto hit = groups_.find(key);
+    if (hit != groups_.end()) return hit->second;
     auto g = std::make_shared<Groups>();
     g->rank = rank;
     g->ulysses = ug;
@@ -249,6 +256,7 @@ class NcclTransport final : public Transport {
     owned_.push_back(rc);
     g->ulysses_comm = uc;
     g->ring_comm = rc;
+    groups_.emplace(key, g);
     return g;
   }
 
@@ -296,6 +304,7 @@ class NcclTransport final : public Transport {
   int max_ctas_ = 2;
   ncclComm_t world_ = nullptr;
   std::vector<ncclComm_t> owned_;
+  std::map<std::pair<std::vector<int>, std::vector<int>>, std::shared_ptr<Groups>> groups_;
 };
 
 std::unique_ptr<Transport> make_nccl_transport(const unsigned char id[128], int world_size,

@@ -60,6 +60,9 @@ class Transport {
   virtual void* ulysses_peer_ptr(const Groups&, const void*, int, size_t) { return nullptr; }
   virtual void ulysses_ready(const Groups&, cudaStream_t) {}
   virtual void ulysses_done(const Groups&, cudaStream_t) {}
+  // An engine is being destroyed: drop whatever the transport keeps about
+  // these local buffers (peer-memory mappings). Local, not collective.
+  virtual void release_buffers(const std::vector<const void*>&) {}
 };
 
 std::unique_ptr<Transport> make_local_transport(int world_size);

@@ -136,6 +136,20 @@ class P2PTransport final : public Transport {
     return g;
   }
 
+  void release_buffers(const std::vector<const void*>& bufs) override {
+    const DriverApi& api = driver();
+    for (const void* b : bufs) {
+      if (!b) continue;
+      CUdeviceptr base = 0;
+      size_t size = 0;
+      if (api.addr_range(&base, &size, reinterpret_cast<CUdeviceptr>(b)) != CUDA_SUCCESS) continue;
+      auto it = regs_.find(base);
+      if (it == regs_.end()) continue;
+      close_peers(it->second.peers);
+      regs_.erase(it);
+    }
+  }
+
   void all_to_all(const Groups& g, const std::vector<std::vector<A2APart>>& parts,
                   const std::vector<size_t>& bytes, cudaStream_t stream) override {
     const int me = index_in(g.ulysses, g.rank);

@@ -157,23 +157,27 @@ def step_plan(cfg: UspConfig, step: int):
     return off, lst[: sizes[1]]
 
 
-def forward_ledger(cfg: UspConfig) -> list[dict]:
-    """Planned collectives of one rank's forward (reference CommLedger terms)."""
-    buf = (UspLedgerEntry * 64)()
-    n = lib().usp_forward_ledger(ctypes.byref(cfg), buf, 64)
+def _read_ledger(call) -> list[dict]:
+    """Two-pass read of a ledger C function (cap 0 returns the size)."""
+    n = call(None, 0)
     if n < 0:
         check(2)
-    return [buf[i].as_dict() for i in range(min(n, 64))]
+    buf = (UspLedgerEntry * max(n, 1))()
+    m = call(buf, n)
+    if m < 0:
+        check(2)
+    return [buf[i].as_dict() for i in range(min(m, n))]
+
+
+def forward_ledger(cfg: UspConfig) -> list[dict]:
+    """Planned collectives of one rank's forward (reference CommLedger terms)."""
+    return _read_ledger(lambda buf, cap: lib().usp_forward_ledger(ctypes.byref(cfg), buf, cap))
 
 
 def backward_ledger(cfg: UspConfig) -> list[dict]:
     """Planned collectives of one rank's forward + backward
     (usp_attention.cpp:68-89, ring_attention.cpp:79-155)."""
-    buf = (UspLedgerEntry * 256)()
-    n = lib().usp_backward_ledger(ctypes.byref(cfg), buf, 256)
-    if n < 0:
-        check(2)
-    return [buf[i].as_dict() for i in range(min(n, 256))]
+    return _read_ledger(lambda buf, cap: lib().usp_backward_ledger(ctypes.byref(cfg), buf, cap))
 
 
 def rank_flops(cfg: UspConfig) -> float:
@@ -362,9 +366,31 @@ class UspAttention:
 
     def ledger(self) -> list[dict]:
         """Collectives issued by the last forward (reference CommLedger terms)."""
-        buf = (UspLedgerEntry * 64)()
-        n = lib().usp_engine_ledger(self._h, buf, 64)
-        return [buf[i].as_dict() for i in range(min(n, 64))]
+        return _read_ledger(lambda buf, cap: lib().usp_engine_ledger(self._h, buf, cap))
+
+    def stage_times(self) -> list[dict]:
+        """Per-stage breakdown of the forwards timed since enable_timing:
+        [{"stage", "ms_total", "count"}] (usp_engine_stage_times); syncs."""
+        from ._lib import UspStageTime
+
+        cap = 512
+        buf = (UspStageTime * cap)()
+        n = int(lib().usp_engine_stage_times(self._h, buf, cap))
+        if n < 0:
+            check(3)
+        return [{"stage": buf[i].name.decode(), "ms_total": buf[i].ms_total, "count": buf[i].count}
+                for i in range(min(n, cap))]
+
+    def debug_counters(self, on: bool = True) -> None:
+        """Parity instrumentation: count the forward kernel's lazy O rescales
+        (resets the count)."""
+        check(lib().usp_engine_debug_counters(self._h, int(on)))
+
+    def rescale_count(self) -> int:
+        """(warp, key tile) rescales of O since debug_counters(True); syncs."""
+        out = ctypes.c_int64()
+        check(lib().usp_engine_rescale_count(self._h, ctypes.byref(out)))
+        return int(out.value)
 
     def enable_timing(self, on: bool = True) -> None:
         """Record CUDA events around every attention-kernel launch."""
@@ -505,14 +531,26 @@ def local_world_backward(engines: Sequence[UspAttention], fwds: Sequence[UspForw
                                     arr(map(_ptr, dvs)), arr([s.cuda_stream for s in streams])))
 
 
+# usp_attention() reuses one engine per configuration (workspace, plans and
+# the transport's sub-communicators are built once, as a layer would).
+_ENGINE_CACHE: "dict[tuple, UspAttention]" = {}
+_ENGINE_CACHE_SIZE = 8
+
+
 def usp_attention(mesh: ProcessMesh, q, k, v, positions: Sequence[int], causal: bool, *,
                   rank: int, seq_len: int, comm: Optional[Comm] = None, device: int = 0) -> UspForward:
     """Functional form of the reference's usp_attention (usp_attention.hpp:41-47)
     for one rank. ``positions`` must be ShardSpec(mesh, L, causal).positions_for(rank),
     the only layout the reference produces; the engine checks it."""
     b, t, hc, hs = q.shape
-    eng = UspAttention(mesh, rank=rank, seq_len=seq_len, heads=hc, kv_heads=k.shape[2], head_size=hs,
-                       causal=causal, batch=b, device=device, comm=comm)
+    key = (mesh.ulysses, mesh.ring, rank, seq_len, hc, k.shape[2], hs, bool(causal), b, device, id(comm))
+    eng = _ENGINE_CACHE.pop(key, None)
+    if eng is None:
+        eng = UspAttention(mesh, rank=rank, seq_len=seq_len, heads=hc, kv_heads=k.shape[2], head_size=hs,
+                           causal=causal, batch=b, device=device, comm=comm)
+    _ENGINE_CACHE[key] = eng  # most recently used last
+    while len(_ENGINE_CACHE) > _ENGINE_CACHE_SIZE:
+        _ENGINE_CACHE.pop(next(iter(_ENGINE_CACHE))).close()
     if list(positions) != eng.positions():
         raise UspInvalidInput(2, "positions must carry one original index per local token "
                                  "in ShardSpec::positions_for order")

@@ -13,19 +13,16 @@ place_rows; LSE in the head-sharded layout of the rank that owns each row.
 Inputs: uniform [-1, 1) from a seeded torch generator on the GPU, rounded to
 bf16 (the reference generator's host stream would need 4-8 GB of fp64 here);
 the oracle runs on the same bf16 values widened to fp64.
-Tolerance: as tests/test_gpu_parity.py (O max-abs 1e-2, LSE max-abs 2e-3).
+Tolerance: as tests/test_gpu_parity.py (O max-abs 5e-3, LSE max-abs 1e-4).
 """
 import numpy as np
 import pytest
 import torch
 
 from oracle.oracle import Oracle
-from tests.usp_harness import UspCase, errors, run_usp_gpu, widen
+from tests.usp_harness import LSE_TOL, O_TOL, UspCase, errors, run_usp_gpu, widen
 
 pytestmark = pytest.mark.gpu
-
-O_TOL = 1e-2
-LSE_TOL = 2e-3
 K = 1024
 
 

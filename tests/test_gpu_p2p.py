@@ -31,7 +31,8 @@ def _worker(rank, world, U, R, port, L, hc, kv, hs, causal, errq):
 
         from oracle.oracle import Oracle, oracle_reference_attention_grad
         from paper_2405_07719_b200 import Comm, ProcessMesh, UspAttention, UspForward
-        from tests.usp_harness import UspCase, errors, make_globals_with_dout, to_bf16, widen
+        from tests.usp_harness import (O_REL_L2, O_TOL, UspCase, errors, make_globals_with_dout, to_bf16,
+                                       widen)
 
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -69,7 +70,7 @@ def _worker(rank, world, U, R, port, L, hc, kv, hs, causal, errq):
         ref = Oracle.reference_attention(qd, kd, vd, causal)
         p = pos.cpu().numpy()
         eo = errors(widen(fwd.out), ref[:, p])
-        assert eo["max_abs"] <= 1e-2 and eo["rel_l2"] <= 1e-2, (rank, eo)
+        assert eo["max_abs"] <= O_TOL and eo["rel_l2"] <= O_REL_L2, (rank, eo)
         # gradients: gather every shard on all ranks, compare with the oracle
         gq, gk, gv = oracle_reference_attention_grad(qd, kd, vd, dod, causal)
         for got, want in ((grads.dq, gq), (grads.dk, gk), (grads.dv, gv)):

@@ -6,20 +6,17 @@ commands.cpp:142-153 widens fp32), isolating kernel error from input
 quantisation. The oracle itself is pinned bitwise to the reference
 (tests/test_oracle.py).
 
-Tolerance (bf16 in / fp32 accumulate vs fp64, stated per SURVEY §8(c)):
-  O   max-abs <= 1e-2 and relative L2 <= 1e-2
-  LSE max-abs <= 2e-3 (natural log)
+Tolerance (bf16 in / fp32 accumulate vs fp64; usp_harness):
+  O   max-abs <= 5e-3 and relative L2 <= 3e-3
+  LSE max-abs <= 1e-4 (natural log)
 """
 import numpy as np
 import pytest
 import torch
 
 from oracle.oracle import Oracle
-from tests.usp_harness import UspCase, errors, make_globals, run_usp_gpu, to_bf16, widen
-
-O_TOL = 1e-2
-O_REL_L2 = 1e-2
-LSE_TOL = 2e-3
+from tests.usp_harness import (LSE_TOL, O_REL_L2, O_TOL, UspCase, errors, make_globals, run_usp_gpu, to_bf16,
+                                widen)
 
 pytestmark = pytest.mark.gpu
 

@@ -74,6 +74,11 @@ def test_validation_messages():
     assert st == 2
     st, msg = validate(head_size=256)
     assert st == 2 and "128" in msg
+    # 8-bit head field of the work units: > 256 local heads is rejected, not
+    # silently aliased into the batch byte (round-1 advice)
+    st, msg = validate(heads=512, kv_heads=8)
+    assert st == 2 and "256 heads" in msg
+    assert validate(heads=512, kv_heads=8, ulysses_degree=2)[0] == 0
 
 
 @pytest.mark.parametrize("U,R,L", [(1, 1, 131072), (1, 8, 131072), (4, 2, 212992), (2, 4, 32768), (8, 1, 32768)])
