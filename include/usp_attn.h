@@ -144,6 +144,24 @@ typedef int (*usp_allgather_fn)(const void* send, void* recv, size_t bytes, void
 USP_API usp_status usp_comm_create_p2p(int32_t world_size, int32_t rank, int32_t device,
                                        usp_allgather_fn allgather, void* ctx, usp_comm** out);
 USP_API void usp_comm_destroy(usp_comm* comm);
+/* Failure detection (the reference World's stuck / mismatched-collective
+ * diagnosis, world.cpp:89-113 and 152-165). Every transport bounds how long
+ * a collective waits for its peers: the local transport's host rendezvous
+ * (keyed by group and call number, with a signature check), the NCCL
+ * transport's non-blocking init/split/launch polling and its watchdog over
+ * enqueued collectives (ncclCommGetAsyncError + completion events; on
+ * timeout or error every communicator is aborted). Default 600 s, or
+ * USP_COMM_TIMEOUT_S. A failed comm reports USP_INTERNAL_ERROR from every
+ * later call with the failure ("collective mismatch on group [...] call #k:
+ * rank a called X but rank b called Y", "collective deadlock ...",
+ * "ring_shift call #k on ring group [...] did not complete within ...").
+ * usp_comm_status returns USP_OK while healthy. */
+USP_API usp_status usp_comm_set_timeout(usp_comm* comm, double seconds);
+USP_API usp_status usp_comm_status(usp_comm* comm);
+/* Tests: one host rendezvous of `rank` on group `members` under `signature`
+ * (local transport only; no GPU work). */
+USP_API usp_status usp_comm_debug_rendezvous(usp_comm* comm, int32_t rank, const int32_t* members,
+                                             int32_t n, const char* signature);
 
 /* ---- engine -------------------------------------------------------------- */
 
@@ -195,6 +213,19 @@ USP_API void usp_engine_destroy(usp_engine* engine);
  * were recorded since the last call (-1 on error). */
 USP_API usp_status usp_engine_enable_timing(usp_engine* engine, int32_t on);
 USP_API int32_t usp_engine_kernel_times(usp_engine* engine, float* ms, int32_t cap);
+/* Ring overlap sizing of an engine: the K+V bytes of one ring
+ * shift, the shortest ring step it hides behind (estimated from the step's
+ * visible pairs), the bandwidth that needs, the CTAs given to the ring
+ * communicator (NCCL maxCTAs) and the SMs the attention grid leaves free for
+ * them (0 on the copy-engine transports). */
+typedef struct usp_engine_info {
+  int32_t num_sms, reserved_sms, ring_ctas;
+  double kv_shift_bytes, ring_step_ms_est, required_gbs;
+} usp_engine_info;
+USP_API usp_status usp_engine_get_info(const usp_engine* engine, usp_engine_info* out);
+/* Overrides the SMs the attention grid leaves free for a concurrent
+ * communication kernel (0 .. #SMs-1). */
+USP_API usp_status usp_engine_set_reserved_sms(usp_engine* engine, int32_t n);
 /* Per-stage breakdown of the forwards run while timing was on (events on
  * the caller's stream after each stage; a stage's time is the gap to the
  * previous one): pack, a2a_in (or pack_a2a_in for the direct peer-memory

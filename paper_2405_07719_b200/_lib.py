@@ -73,6 +73,12 @@ class UspLedgerEntry(ctypes.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
 
+class UspEngineInfo(ctypes.Structure):
+    _fields_ = [("num_sms", ctypes.c_int32), ("reserved_sms", ctypes.c_int32), ("ring_ctas", ctypes.c_int32),
+                ("kv_shift_bytes", ctypes.c_double), ("ring_step_ms_est", ctypes.c_double),
+                ("required_gbs", ctypes.c_double)]
+
+
 class UspStageTime(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char * 24), ("ms_total", ctypes.c_double), ("count", ctypes.c_int32)]
 
@@ -84,7 +90,7 @@ EXPORTS = [
     "usp_comm_create_nccl", "usp_comm_create_local", "usp_comm_destroy", "usp_engine_create",
     "usp_attn_fwd", "usp_engine_last_launches", "usp_engine_destroy", "usp_engine_enable_timing",
     "usp_engine_kernel_times", "usp_engine_debug_counters", "usp_engine_rescale_count",
-    "usp_engine_stage_times", "usp_local_world_fwd", "usp_attn_bwd", "usp_local_world_bwd",
+    "usp_engine_stage_times", "usp_engine_get_info", "usp_engine_set_reserved_sms", "usp_comm_set_timeout", "usp_comm_status", "usp_comm_debug_rendezvous", "usp_local_world_fwd", "usp_attn_bwd", "usp_local_world_bwd",
     "usp_backward_ledger", "usp_attn_fwd_host", "usp_comm_create_p2p",
     "usp_last_error", "usp_version",
 ]
@@ -125,6 +131,9 @@ def _declare(lib):
         "usp_comm_create_local": (st, [ctypes.c_int32, P(vp)]),
         "usp_comm_create_p2p": (st, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ALLGATHER_FN, vp, P(vp)]),
         "usp_comm_destroy": (None, [vp]),
+        "usp_comm_set_timeout": (st, [vp, ctypes.c_double]),
+        "usp_comm_status": (st, [vp]),
+        "usp_comm_debug_rendezvous": (st, [vp, ctypes.c_int32, P(ctypes.c_int32), ctypes.c_int32, ctypes.c_char_p]),
         "usp_engine_create": (st, [P(UspConfig), vp, P(vp)]),
         "usp_attn_fwd": (st, [vp, vp, vp, vp, vp, vp, vp]),
         "usp_attn_fwd_host": (st, [vp, vp, vp, vp, vp, vp, vp]),
@@ -134,6 +143,8 @@ def _declare(lib):
         "usp_engine_kernel_times": (ctypes.c_int32, [vp, P(ctypes.c_float), ctypes.c_int32]),
         "usp_engine_debug_counters": (st, [vp, ctypes.c_int32]),
         "usp_engine_stage_times": (ctypes.c_int32, [vp, P(UspStageTime), ctypes.c_int32]),
+        "usp_engine_get_info": (st, [vp, P(UspEngineInfo)]),
+        "usp_engine_set_reserved_sms": (st, [vp, ctypes.c_int32]),
         "usp_engine_rescale_count": (st, [vp, i64p]),
         "usp_local_world_fwd": (st, [P(vp), ctypes.c_int32, P(vp), P(vp), P(vp), P(vp), P(vp), P(vp)]),
         "usp_last_error": (ctypes.c_char_p, []),

@@ -166,8 +166,6 @@ class Engine {
     }();
     cluster_mode_ = cluster_ ? (cluster_mode == 2 ? 2 : 1) : 0;
 
-    if (tr_) groups_ = tr_->make_groups(c.rank, shape_.mesh.ulysses_group(c.rank),
-                                        shape_.mesh.ring_group(c.rank));
 
     const size_t e = 2;  // bf16
     const bool reshape = U_ > 1 || hs_ != hsk_;
@@ -224,7 +222,55 @@ class Engine {
       st.units = upload(st.host.units);
       steps_.push_back(std::move(st));
     }
+
+    // Ring overlap sizing. The K+V block shifted after step t
+    // must land before step t+1 starts, i.e. within step t's attention:
+    // required bandwidth = 2 * kv_bytes / t_step(t), t_step from the
+    // step's visible pairs at the measured forward rate (kFwdTflops), taken
+    // with 2x margin over the shortest shifted-behind step. An NVLink
+    // send/recv channel of NCCL moves >= kCtaGBs (conservative; measured on
+    // the box by tools/overlap_nccl.py), so the ring communicator gets
+    // ceil(2 * required / kCtaGBs) CTAs (1..16) and, because a CTA needs an
+    // SM the persistent attention grid would otherwise hold, the attention
+    // grid leaves that many SMs free (NCCL transport only; the copy-engine
+    // transports take no SMs).
+    if (R_ > 1) {
+      constexpr double kFwdTflops = 1300.0, kCtaGBs = 20.0;
+      double t_min = 1e30;
+      for (int t = 0; t + 1 < R_; ++t) {
+        const double f = 4.0 * double(B_) * hl_ * hs_ * double(steps_[t].host.visible_pairs);
+        t_min = std::min(t_min, f / (kFwdTflops * 1e12));
+      }
+      kv_shift_bytes_ = 2.0 * double(kv_bytes_);
+      step_ms_est_ = t_min * 1e3;
+      required_gbs_ = t_min > 0 && t_min < 1e29 ? kv_shift_bytes_ / t_min / 1e9 : 0.0;
+      ring_ctas_ = std::min(16, std::max(1, static_cast<int>(std::ceil(2.0 * required_gbs_ / kCtaGBs))));
+      reserved_sms_ = (tr_ && tr_->comm_uses_sms()) ? ring_ctas_ : 0;
+    }
+    if (tr_) groups_ = tr_->make_groups(c.rank, shape_.mesh.ulysses_group(c.rank),
+                                        shape_.mesh.ring_group(c.rank), ring_ctas_);
   }
+
+ public:
+  struct Info {
+    int num_sms, reserved_sms, ring_ctas;
+    double kv_shift_bytes, step_ms_est, required_gbs;
+  };
+  Info info() const {
+    return {num_sms_, reserved_sms_, ring_ctas_, kv_shift_bytes_, step_ms_est_, required_gbs_};
+  }
+  // SMs the attention grid leaves free for a concurrent communication kernel
+  // (default: the sizing above).
+  void set_reserved_sms(int n) {
+    if (n < 0 || n >= num_sms_) throw_invalid("reserved SMs must be in [0, #SMs)");
+    reserved_sms_ = n;
+  }
+
+ private:
+  int ring_ctas_ = 1, reserved_sms_ = 0;
+  double kv_shift_bytes_ = 0, step_ms_est_ = 0, required_gbs_ = 0;
+
+ public:
 
   ~Engine() {
     if (tr_) {
@@ -1107,7 +1153,7 @@ class Engine {
       USPB_CHECK(cudaMemsetAsync(trace_buf_.p, 0, trace_buf_.bytes, st));
       p.trace = trace_buf_.as<unsigned long long>();
     }
-    const int reserve = (R_ > 1 && tr_) ? tr_->reserved_sms() : 0;
+    const int reserve = reserved_sms_;
     const int slots = std::max(1, num_sms_ - reserve);
     const int grid = p.cluster ? std::max(2, std::min(2 * p.num_units, slots) & ~1) : std::min(p.num_units, slots);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -1183,7 +1229,7 @@ class Engine {
       USPB_CHECK(cudaMemsetAsync(trace_buf_.p, 0, trace_buf_.bytes, st));
       p.trace = trace_buf_.as<unsigned long long>();
     }
-    const int reserve = (R_ > 1 && tr_) ? tr_->reserved_sms() : 0;
+    const int reserve = reserved_sms_;
     const int slots = std::max(1, num_sms_ - reserve);
     // cluster mode: two CTAs (one per SM of a TPC) per unit, an even grid
     const int grid = cluster_ ? std::max(2, std::min(2 * p.num_units, slots) & ~1) : std::min(p.num_units, slots);
@@ -1608,6 +1654,31 @@ usp_status usp_comm_create_p2p(int32_t world_size, int32_t rank, int32_t device,
 
 void usp_comm_destroy(usp_comm* comm) { delete comm; }
 
+usp_status usp_comm_set_timeout(usp_comm* comm, double seconds) {
+  if (!comm || !(seconds > 0)) {
+    g_last_error = "usp_comm_set_timeout: a comm and a positive timeout are required";
+    return USP_INVALID_INPUT;
+  }
+  comm->impl->set_timeout(seconds);
+  return USP_OK;
+}
+
+usp_status usp_comm_status(usp_comm* comm) {
+  if (!comm) return USP_INVALID_INPUT;
+  return guarded([&] {
+    const std::string st = comm->impl->status();
+    if (!st.empty()) throw Error(ErrorCode::kCommMismatch, st);
+  });
+}
+
+usp_status usp_comm_debug_rendezvous(usp_comm* comm, int32_t rank, const int32_t* members, int32_t n,
+                                     const char* signature) {
+  if (!comm || !members || n < 1 || !signature) return USP_INVALID_INPUT;
+  return guarded([&] {
+    comm->impl->debug_rendezvous(std::vector<int>(members, members + n), rank, signature);
+  });
+}
+
 usp_status usp_engine_create(const usp_config* cfg, usp_comm* comm, usp_engine** out) {
   if (!out) return USP_INVALID_INPUT;
   *out = nullptr;
@@ -1681,6 +1752,24 @@ int32_t usp_engine_stage_times(usp_engine* engine, usp_stage_time* out, int32_t 
       }) != USP_OK)
     return -1;
   return n;
+}
+
+usp_status usp_engine_get_info(const usp_engine* engine, usp_engine_info* out) {
+  if (!engine || !out) return USP_INVALID_INPUT;
+  return guarded([&] {
+    const auto i = engine->impl->info();
+    out->num_sms = i.num_sms;
+    out->reserved_sms = i.reserved_sms;
+    out->ring_ctas = i.ring_ctas;
+    out->kv_shift_bytes = i.kv_shift_bytes;
+    out->ring_step_ms_est = i.step_ms_est;
+    out->required_gbs = i.required_gbs;
+  });
+}
+
+usp_status usp_engine_set_reserved_sms(usp_engine* engine, int32_t n) {
+  if (!engine) return USP_INVALID_INPUT;
+  return guarded([&] { engine->impl->set_reserved_sms(n); });
 }
 
 usp_status usp_engine_debug_counters(usp_engine* engine, int32_t on) {

@@ -14,7 +14,10 @@
 
 #include <cstddef>
 #include <memory>
+#include <string>
 #include <vector>
+
+#include "plan.hpp"
 
 namespace uspb200 {
 
@@ -35,9 +38,11 @@ class Transport {
  public:
   virtual ~Transport() = default;
   virtual int world_size() const = 0;
-  // Collective over the world: builds this rank's sub-groups.
+  // Collective over the world: builds this rank's sub-groups. ring_ctas:
+  // how many CTAs (SMs) the ring exchange may use while the attention
+  // kernel runs (NCCL maxCTAs of the ring communicator; Engine sizes it).
   virtual std::shared_ptr<Groups> make_groups(int rank, const std::vector<int>& ulysses_group,
-                                              const std::vector<int>& ring_group) = 0;
+                                              const std::vector<int>& ring_group, int ring_ctas) = 0;
   // Several tensors exchanged in one collective over the Ulysses group:
   // parts[t][p] for tensor t and member index p, bytes[t] per part.
   virtual void all_to_all(const Groups& g, const std::vector<std::vector<A2APart>>& parts,
@@ -46,9 +51,9 @@ class Transport {
   virtual void ring_shift(const Groups& g, const std::vector<const void*>& send,
                           const std::vector<void*>& recv, const std::vector<size_t>& bytes,
                           cudaStream_t stream) = 0;
-  // NCCL kernels occupy SMs (the attention grid leaves room for them);
-  // the local transport uses copy engines.
-  virtual int reserved_sms() const = 0;
+  // NCCL kernels occupy SMs (the attention grid leaves ring_ctas SMs for
+  // them); the local and peer-memory transports use copy engines.
+  virtual bool comm_uses_sms() const = 0;
 
   // Peer memory (optional): the address, valid on this rank's device, of
   // Ulysses member m's copy of the symmetric buffer holding `local`
@@ -63,6 +68,25 @@ class Transport {
   // An engine is being destroyed: drop whatever the transport keeps about
   // these local buffers (peer-memory mappings). Local, not collective.
   virtual void release_buffers(const std::vector<const void*>&) {}
+
+  // Failure detection (the reference World's stuck/mismatched-collective
+  // diagnosis, src/simcomm/world.cpp:89-113, 152-165). timeout: how long a
+  // collective may wait for its peers (host rendezvous, NCCL init/split, a
+  // collective's completion on the GPU) before the transport reports it.
+  // status(): empty while healthy, else the failure (the comm is then dead:
+  // NCCL communicators aborted, every later collective throws it again).
+  virtual void set_timeout(double seconds) { timeout_s_ = seconds; }
+  double timeout() const { return timeout_s_; }
+  virtual std::string status() { return {}; }
+  // Host-side rendezvous of `rank` on group `members` under `signature`
+  // (tests: the local transport's mismatch / deadlock diagnosis without a GPU).
+  virtual void debug_rendezvous(const std::vector<int>&, int, const std::string&) {
+    throw_invalid("debug_rendezvous: only the local transport has a host rendezvous");
+  }
+
+ protected:
+  double timeout_s_ = default_timeout();
+  static double default_timeout();
 };
 
 std::unique_ptr<Transport> make_local_transport(int world_size);

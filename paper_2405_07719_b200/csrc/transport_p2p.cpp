@@ -9,7 +9,7 @@
 //     the same order on symmetric allocations, so the exchange is collective);
 //   * data moves with stream-ordered cudaMemcpyAsync into the peer mapping:
 //     copy engines, no SMs, so a ring shift runs beside an attention kernel
-//     that owns every SM (reserved_sms() == 0);
+//     that owns every SM (comm_uses_sms() == false);
 //   * ordering across processes uses GPU stream memory operations on a small
 //     IPC-shared signal array: the receiver publishes "my buffer is free for
 //     collective e" (cuStreamWriteValue64 into the sender's signals), the
@@ -124,10 +124,10 @@ class P2PTransport final : public Transport {
   }
 
   int world_size() const override { return n_; }
-  int reserved_sms() const override { return 0; }  // copy engines + stream memops only
+  bool comm_uses_sms() const override { return false; }  // copy engines + stream memops only
 
-  std::shared_ptr<Groups> make_groups(int rank, const std::vector<int>& ug,
-                                      const std::vector<int>& rg) override {
+  std::shared_ptr<Groups> make_groups(int rank, const std::vector<int>& ug, const std::vector<int>& rg,
+                                      int) override {
     if (rank != rank_) throw_invalid("p2p transport: engine rank differs from the transport's rank");
     auto g = std::make_shared<Groups>();
     g->rank = rank;

@@ -273,6 +273,20 @@ class Comm:
 
         return cls.p2p(world, rank, device, allgather)
 
+    def set_timeout(self, seconds: float) -> None:
+        """How long a collective may wait for its peers before the comm
+        reports it (usp_comm_set_timeout)."""
+        check(lib().usp_comm_set_timeout(self._h, float(seconds)))
+
+    def status(self) -> None:
+        """Raises UspError with the failure if the comm has failed."""
+        check(lib().usp_comm_status(self._h))
+
+    def debug_rendezvous(self, rank: int, members: Sequence[int], signature: str) -> None:
+        """Tests: one host rendezvous (local transport) without GPU work."""
+        arr = (ctypes.c_int32 * len(members))(*members)
+        check(lib().usp_comm_debug_rendezvous(self._h, rank, arr, len(members), signature.encode()))
+
     def close(self) -> None:
         if self._h:
             lib().usp_comm_destroy(self._h)
@@ -367,6 +381,17 @@ class UspAttention:
     def ledger(self) -> list[dict]:
         """Collectives issued by the last forward (reference CommLedger terms)."""
         return _read_ledger(lambda buf, cap: lib().usp_engine_ledger(self._h, buf, cap))
+
+    def info(self) -> dict:
+        """Ring overlap sizing (usp_engine_get_info)."""
+        from ._lib import UspEngineInfo
+
+        i = UspEngineInfo()
+        check(lib().usp_engine_get_info(self._h, ctypes.byref(i)))
+        return {f: getattr(i, f) for f, _ in i._fields_}
+
+    def set_reserved_sms(self, n: int) -> None:
+        check(lib().usp_engine_set_reserved_sms(self._h, int(n)))
 
     def stage_times(self) -> list[dict]:
         """Per-stage breakdown of the forwards timed since enable_timing:

@@ -24,9 +24,10 @@ def _run(L, hc, kv, hs, causal, batch=1, seed=0):
     eng = UspAttention(ProcessMesh(1, 1), rank=0, seq_len=L, heads=hc, kv_heads=kv, head_size=hs,
                        causal=causal, batch=batch, device=0)
     g = torch.Generator(device=dev).manual_seed(seed)
-    q = torch.randn(eng.q_shape(), device=dev, dtype=torch.bfloat16, generator=g)
-    k = torch.randn(eng.kv_shape(), device=dev, dtype=torch.bfloat16, generator=g)
-    v = torch.randn(eng.kv_shape(), device=dev, dtype=torch.bfloat16, generator=g)
+    # U[-1, 1) like the reference generator (the gates in usp_harness are
+    # stated for that input range)
+    u = lambda shape: (torch.rand(shape, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)  # noqa: E731
+    q, k, v = u(eng.q_shape()), u(eng.kv_shape()), u(eng.kv_shape())
     o, lse = eng.alloc_outputs()
     eng.forward(q, k, v, o, lse)
     torch.cuda.synchronize()
