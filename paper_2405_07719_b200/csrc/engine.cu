@@ -345,11 +345,13 @@ class Engine {
         pkv[m] = tr_->ulysses_peer_ptr(*groups_, kv0_.p, m, 2 * kv_bytes_);
       }
       tr_->ulysses_ready(*groups_, st);  // every member's Q/K/V buffers are free
+      batch_begin();
       for (int m = 0; m < U_; ++m) {
         pack_part(q, static_cast<uint8_t*>(pq[m]) + u_ * q_part_, H_, hl_, m, st);
         pack_part(k, static_cast<uint8_t*>(pkv[m]) + u_ * kv_part_, KV_, kvl_, m, st);
         pack_part(v, static_cast<uint8_t*>(pkv[m]) + kv_bytes_ + u_ * kv_part_, KV_, kvl_, m, st);
       }
+      batch_flush(st);
       tr_->ulysses_done(*groups_, st);  // every member's parts for me have landed
       stage(st, "pack_a2a_in");
       record_a2a(0, q_part_);
@@ -363,9 +365,11 @@ class Engine {
       uint8_t* sq = send_.as<uint8_t>();
       uint8_t* sk = sq + U_ * q_part_;
       uint8_t* sv = sk + U_ * kv_part_;
+      batch_begin();
       pack_heads(q, sq, H_, hl_, st);
       pack_heads(k, sk, KV_, kvl_, st);
       pack_heads(v, sv, KV_, kvl_, st);
+      batch_flush(st);
       stage(st, "pack");
       uint8_t* rq = B_ > 1 ? recv_.as<uint8_t>() : nullptr;
       uint8_t* rk = rq ? rq + U_ * q_part_ : nullptr;
@@ -384,9 +388,11 @@ class Engine {
       record_a2a(1, kv_part_);
       record_a2a(2, kv_part_);
       if (B_ > 1) {
+        batch_begin();
         gather_seq(rq, q_h_.p, hl_, st);
         gather_seq(rk, kv0, kvl_, st);
         gather_seq(rv, kv0 + kv_bytes_, kvl_, st);
+        batch_flush(st);
         stage(st, "unpack_in");
       }
       qh = q_h_.p;
@@ -917,9 +923,11 @@ class Engine {
     record_a2a(5, q_part_);
     record_a2a(6, kv_part_);
     record_a2a(7, kv_part_);
+    batch_begin();
     unpack_heads(rq, dq, st, H_, hl_);
     unpack_heads(rk, dk, st, KV_, kvl_);
     unpack_heads(rv, dv, st, KV_, kvl_);
+    batch_flush(st);
   }
 
   double rank_flops() const {
@@ -929,10 +937,32 @@ class Engine {
   }
 
  private:
+  // Row permutations go through the TMA bulk-copy kernel; between
+  // batch_begin() and batch_flush() they are collected and launched as ONE
+  // kernel (the Q, K, V packs; every peer part of the direct exchange).
   void permute(const RowPermute& rp, cudaStream_t st) {
-    USPB_CHECK(launch_row_permute(rp, num_sms_, st));
-    ++launches_;
+    if (batching_) {
+      batch_.push_back(rp);
+      return;
+    }
+    int n = 0;
+    USPB_CHECK(launch_row_permute_multi(&rp, 1, num_sms_, st, &n));
+    launches_ += n;
   }
+  void batch_begin() {
+    batching_ = true;
+    batch_.clear();
+  }
+  void batch_flush(cudaStream_t st) {
+    batching_ = false;
+    if (batch_.empty()) return;
+    int n = 0;
+    USPB_CHECK(launch_row_permute_multi(batch_.data(), static_cast<int>(batch_.size()), num_sms_, st, &n));
+    launches_ += n;
+    batch_.clear();
+  }
+  bool batching_ = false;
+  std::vector<RowPermute> batch_;
   // (b, T, heads, hs) -> [peer][b][T][heads/U][hsk]
   void pack_heads(const void* src, void* dst, int heads, int local, cudaStream_t st) {
     RowPermute rp;

@@ -20,5 +20,10 @@ struct RowPermute {
 };
 
 cudaError_t launch_row_permute(const RowPermute& p, int num_sms, cudaStream_t stream);
+// Several permutations, one launch of the TMA bulk-copy kernel when all of
+// them are runs of contiguous rows (every engine pack / unpack at a native
+// head size); *launches = kernels launched.
+cudaError_t launch_row_permute_multi(const RowPermute* ps, int n, int num_sms, cudaStream_t stream,
+                                     int* launches);
 
 }  // namespace uspb200

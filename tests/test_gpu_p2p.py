@@ -60,11 +60,12 @@ def _worker(rank, world, U, R, port, L, hc, kv, hs, causal, errq):
         assert torch.equal(oh.view(torch.int16), fwd.out.cpu().view(torch.int16)), rank
         assert torch.equal(lh.view(torch.int32), fwd.logsumexp.cpu().view(torch.int32)), rank
         if U > 1:
-            # direct exchange (default): one pack launch per member and tensor
-            # straight into the peers' buffers, the O all-to-all folded into the
-            # attention epilogue; otherwise 3 staging packs + an exchange
-            direct = os.environ.get("USP_DIRECT_A2A", "1") != "0"
-            assert fwd_launches == (3 * U if direct else 3) + R + 1, (fwd_launches, direct)
+            # direct exchange (default): ONE bulk-copy launch stores every
+            # member's Q/K/V parts straight into the peers' buffers, the O
+            # all-to-all is folded into the attention epilogue; otherwise one
+            # launch packs Q, K, V into staging + an exchange. Then R attention
+            # steps and the O unpack.
+            assert fwd_launches == 1 + R + 1, fwd_launches
         torch.cuda.synchronize()
         qd, kd, vd, dod = widen(tq), widen(tk), widen(tv), widen(tdo)
         ref = Oracle.reference_attention(qd, kd, vd, causal)

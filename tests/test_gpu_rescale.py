@@ -14,16 +14,18 @@ branch needs peaky inputs (SURVEY §8(d) stress set):
              key tiles raise the running max of every row.
 
 Each case runs every rank of the mesh (in-process transport), checks O and
-LSE against the fp64 oracle on the same bf16-rounded inputs with the
-standard gates, and proves the branch fired: the kernel's debug counter
+LSE against the fp64 oracle on the same bf16-rounded inputs — relative L2
+and LSE with the standard gates, O max-abs with O_TOL_PEAKY = 2u (a near
+one-hot softmax passes single bf16-rounded P and O values through instead of
+averaging their rounding; usp_harness) — and proves the branch fired: the kernel's debug counter
 (usp_engine_debug_counters) of (warp, key tile) rescales is > 0.
 """
 import numpy as np
 import pytest
 
 from oracle.oracle import Oracle
-from tests.usp_harness import (LSE_TOL, O_REL_L2, O_TOL, UspCase, errors, make_globals, run_usp_gpu, to_bf16,
-                               widen)
+from tests.usp_harness import (LSE_TOL, O_REL_L2, O_TOL, O_TOL_PEAKY, UspCase, errors, make_globals, run_usp_gpu,
+                               to_bf16, widen)
 
 pytestmark = pytest.mark.gpu
 
@@ -64,7 +66,7 @@ def test_rescale_branch_matches_oracle(cuda, u, r, hs, causal, kind):
     eo, el, fired = _run(c, kind, cuda)
     msg = f"{c} {kind}: O {eo} LSE {el} rescales {fired}"
     assert fired > 0, "the lazy-rescale branch never fired: " + msg
-    assert eo["max_abs"] <= O_TOL and eo["rel_l2"] <= O_REL_L2, msg
+    assert eo["max_abs"] <= O_TOL_PEAKY and eo["rel_l2"] <= O_REL_L2, msg
     assert el["max_abs"] <= LSE_TOL, msg
 
 
@@ -75,7 +77,7 @@ def test_rescale_branch_mha_tile_pairs(cuda, u, r):
     eo, el, fired = _run(c, "q16", cuda)
     msg = f"{c}: O {eo} LSE {el} rescales {fired}"
     assert fired > 0, msg
-    assert eo["max_abs"] <= O_TOL and eo["rel_l2"] <= O_REL_L2, msg
+    assert eo["max_abs"] <= O_TOL_PEAKY and eo["rel_l2"] <= O_REL_L2, msg
     assert el["max_abs"] <= LSE_TOL, msg
 
 

@@ -21,6 +21,11 @@ from oracle.oracle import Oracle
 O_TOL = 5e-3       # O max-abs
 O_REL_L2 = 3e-3    # O ||d||_2 / ||ref||_2
 LSE_TOL = 1e-4     # LSE max-abs (natural log)
+# Peaky softmax (the lazy-rescale stress set): O is then close to single V
+# rows, so the bf16 rounding of P (relative <= u = 2^-8) and of O (<= u) no
+# longer average out: max-abs <= 2u * max|V| = 7.8e-3 (measured 5.0-5.3e-3;
+# relative L2 and LSE keep the standard gates).
+O_TOL_PEAKY = 2 * 2.0 ** -8
 
 
 @dataclass
