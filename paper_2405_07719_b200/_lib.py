@@ -11,7 +11,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libusp_b200.so")
+LIB_PATH = os.environ.get("USPB_LIB_PATH") or os.path.join(HERE, "libusp_b200.so")  # override: dev A/B builds
 
 USP_OK, USP_TOLERANCE_EXCEEDED, USP_INVALID_INPUT, USP_INTERNAL_ERROR = 0, 1, 2, 3
 

@@ -16,8 +16,12 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "libusp_b200.so")
-OBJ = os.path.join(HERE, "build")
+# Development A/B builds: USPB_VARIANT=name builds libusp_b200_<name>.so from
+# objects in build_<name>/ (with USPB_NVCC_EXTRA flags and, optionally, the
+# forward kernel taken from USPB_FA_FWD_SRC); load it with USPB_LIB_PATH.
+_VARIANT = os.environ.get("USPB_VARIANT", "")
+OUT = os.path.join(HERE, f"libusp_b200_{_VARIANT}.so" if _VARIANT else "libusp_b200.so")
+OBJ = os.path.join(HERE, f"build_{_VARIANT}" if _VARIANT else "build")
 SOURCES = ["fa_fwd_sm100.cu", "fa_bwd_sm100.cu", "reshard.cu", "engine.cu", "plan.cpp", "transport.cpp",
            "simulate.cu", "check_fp64.cu", "transport_p2p.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -40,6 +44,8 @@ def _flags() -> list[str]:
 def _compile(src: str) -> str:
     obj = os.path.join(OBJ, os.path.basename(src) + ".o")
     path = os.path.join(CSRC, src)
+    if _VARIANT and src == "fa_fwd_sm100.cu" and os.environ.get("USPB_FA_FWD_SRC"):
+        path = os.environ["USPB_FA_FWD_SRC"]
     deps = [path] + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".hpp", ".cuh", ".h"))]
     deps += [os.path.join(ROOT, "include", h) for h in ("usp_attn.h", "usp_sim.h")]
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps):

@@ -29,9 +29,6 @@
 #include "fa_fwd.hpp"
 #include "ptx_sm100.cuh"
 
-#ifndef USPB_FWD_SPLIT
-#define USPB_FWD_SPLIT 1  // softmax warps per TMEM lane quarter and q tile (2: measured equal per cycle)
-#endif
 #ifndef USPB_FWD_STAGES
 #define USPB_FWD_STAGES 4  // K/V pipeline depth: measured best at 4 (2 tiles of K+V) on B200
 #endif
@@ -39,15 +36,10 @@ namespace uspb200 {
 
 using namespace ptx;
 
-template <int NQ, int HS, int POLY, int SPL>
+template <int NQ, int HS>
 struct FwdCfg {
-  // SPL softmax warps per TMEM lane quarter and q tile, each owning 128/SPL
-  // of the key columns: with SPL = 2 two warps of every SM sub-partition
-  // run a q tile's exponentials concurrently (one warp alone issues MUFU.EX2
-  // at ~1/12 per cycle; two keep the 1/8-per-cycle pipe busy).
-  static constexpr int kSplit = SPL;
-  static constexpr int kCols = 128 / SPL;  // key columns per softmax warp
-  static constexpr int kSoftmaxWarps = 4 * NQ * SPL;
+  static constexpr int kCols = 128;  // key columns per softmax thread (one TMEM lane = one query row)
+  static constexpr int kSoftmaxWarps = 4 * NQ;
   static constexpr int kTmaWarp = kSoftmaxWarps;
   static constexpr int kMmaWarp = kSoftmaxWarps + 1;
   // NQ == 2: a full extra warpgroup (TMA, MMA, 2 idle warps) so registers
@@ -60,7 +52,7 @@ struct FwdCfg {
   // (kThreads x kLaunchRegs under __launch_bounds__(kThreads, 1)); asking for
   // more would block the .inc forever.
   static constexpr int kLaunchRegs = (65536 / kThreads) / 8 * 8;
-  static constexpr int kProducerRegs = SPL == 1 ? 88 : 64;
+  static constexpr int kProducerRegs = 88;
   static constexpr int kSoftmaxRegs =
       ((kLaunchRegs * kThreads - 128 * kProducerRegs) / (32 * kSoftmaxWarps)) / 8 * 8 > 240
           ? 240
@@ -71,15 +63,12 @@ struct FwdCfg {
   static constexpr int kSubBytes = 128 * 128;    // one block: 128 rows x 128 B
   static constexpr int kQBytes = kTileM * HS * 2;
   static constexpr int kKVBytes = kTileN * HS * 2;
-  // sibling-warp exchange (SPL == 2): row maxima [2 parity][NQ][SPL][128]
-  // and row sums / epilogue weights [2 parity][NQ][SPL][128]
-  static constexpr int kXchgBytes = SPL == 1 ? 0 : 2 * (2 * NQ * SPL * 128 * 4);
-  static constexpr int kBudget = 227 * 1024 - 2048 - kXchgBytes;
+  static constexpr int kBudget = 227 * 1024 - 2048;
   static constexpr int kStagesFit = (kBudget - NQ * kQBytes) / kKVBytes;
   static constexpr int kStages = kStagesFit > USPB_FWD_STAGES ? USPB_FWD_STAGES : kStagesFit;
   static constexpr int kSchedDepth = 4;  // unit-ticket ring between producer and consumers
   static constexpr int kNumBars = 3 * NQ + 2 + NQ + 2 * kStages + 2 * kSchedDepth;
-  static constexpr int kSmemBytes = 1024 /*align slack*/ + NQ * kQBytes + kStages * kKVBytes + kXchgBytes +
+  static constexpr int kSmemBytes = 1024 /*align slack*/ + NQ * kQBytes + kStages * kKVBytes +
                                     kNumBars * 8 + 16 + 4 * kSchedDepth;
   // TMEM: ONE S buffer shared by the q tiles (time-multiplexed: the MMA
   // warp computes the next tile's S as soon as the previous S has been
@@ -90,7 +79,6 @@ struct FwdCfg {
   static constexpr uint32_t kColsUsed = kOCol + NQ * HS;
   static constexpr uint32_t kTmemCols = kColsUsed <= 128 ? 128 : (kColsUsed <= 256 ? 256 : 512);
   static_assert(HS == 64 || HS == 128, "head_size must be 64 or 128 on the tcgen05 path");
-  static_assert(SPL == 1 || SPL == 2, "one or two softmax warps per lane quarter");
   static_assert(kStages >= 2, "not enough shared memory for a K/V pipeline");
 };
 
@@ -158,10 +146,10 @@ __device__ __forceinline__ int next_unit_impl(uint64_t* full, uint64_t* empty, c
 // MC = 1: a 2-CTA cluster runs the two head pairs of a 4-head GQA group over
 // the same rows (unit = q tile x head quad); each CTA loads half of every
 // K/V tile and multicasts it to both, so L2->SMEM traffic per FLOP halves.
-template <int NQ, int HS, int POLY, int SPL, int MC>
-__global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
+template <int NQ, int HS, int MC>
+__global__ void __launch_bounds__(FwdCfg<NQ, HS>::kThreads, 1)
     fa_fwd_sm100_kernel(const __grid_constant__ FwdParams p) {
-  using C = FwdCfg<NQ, HS, POLY, SPL>;
+  using C = FwdCfg<NQ, HS>;
   static_assert(!MC || (NQ == 2 && HS == 128), "cluster mode: two head pairs, 128-column tiles");
   // MC == 2: cta_group::2 MMAs (M = 256 over the pair): the leader CTA issues
   // every MMA; each CTA holds its own Q tiles, one 64-key half of every K
@@ -173,8 +161,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sQ = smem;
   uint8_t* sKV = smem + NQ * C::kQBytes;
-  const uint32_t xchg = smem_u32(sKV + NS * C::kKVBytes);  // sibling-warp exchange (SPL == 2)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + NS * C::kKVBytes + C::kXchgBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + NS * C::kKVBytes);
   uint64_t* q_full = bars;              // [NQ]  TMA -> MMA
   uint64_t* q_empty = q_full + NQ;      // [1]   MMA -> TMA
   uint64_t* kv_full = q_empty + 1;      // [NS]  TMA -> MMA
@@ -198,10 +185,10 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
     for (int t = 0; t < NQ; ++t) {
       mbar_init(&q_full[t], 1);
       mbar_init(&s_full[t], 1);
-      mbar_init(&p_ready[t], k2 ? 2 * 4 * SPL : 128 * SPL);  // 2SM: one lane per warp of both CTAs
+      mbar_init(&p_ready[t], k2 ? 2 * 4 : 128);  // 2SM: one lane per warp of both CTAs
       mbar_init(&pv_done[t], 1);
     }
-    mbar_init(s_free, (k2 ? 2 : 1) * 4 * SPL);  // one lane of each warp holding S (both CTAs with 2SM)
+    mbar_init(s_free, (k2 ? 2 : 1) * 4);  // one lane of each warp holding S (both CTAs with 2SM)
     mbar_init(q_empty, 1);
     for (int d = 0; d < C::kSchedDepth; ++d) {
       mbar_init(&sched_full[d], 1);
@@ -240,25 +227,13 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
     if constexpr (C::kRegSplit)
       asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::kSoftmaxRegs));
     constexpr int KC = C::kCols;
-    const int t = warp / (4 * SPL);
+    const int t = warp / 4;
     const int quarter = warp & 3;             // TMEM lane quarter (warp id % 4)
-    const int half = (warp / 4) % SPL;        // which 128/SPL key columns
     const int row_in_tile = quarter * 32 + lane;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-    const uint32_t s_addr = lane_base + C::kSCol + half * KC;
-    const uint32_t p_addr = lane_base + C::kPCol + t * 64 + half * (KC / 2);
-    const uint32_t o_addr = lane_base + C::kOCol + t * HS + half * (HS / SPL);
-    // sibling exchange slots (SPL == 2): [parity][t][half][row] floats
-    const uint32_t bar_id = 1 + t * 4 + quarter;
-    auto xslot = [&](uint32_t region, uint32_t parity, int h) {
-      return xchg + region * (2 * NQ * SPL * 128 * 4) +
-             ((((parity * NQ + t) * SPL + h) * 128 + row_in_tile) << 2);
-    };
-    auto ld_sh = [](uint32_t a) {
-      float v;
-      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
-      return v;
-    };
+    const uint32_t s_addr = lane_base + C::kSCol;
+    const uint32_t p_addr = lane_base + C::kPCol + t * 64;
+    const uint32_t o_addr = lane_base + C::kOCol + t * HS;
     const float sl2 = p.scale_log2;
     uint32_t s_phase = 0, pv_phase = 0;
     for (uint32_t it = 0;; ++it) {
@@ -271,16 +246,16 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
       const int n = p.tile_off[qt + 1] - beg;
       const int q_row = (p.pair_rows ? qt * NQ + t : qt) * kTileM + row_in_tile;
       const int qpos = p.q_pos[q_row];
-      float m_run = -INFINITY, l_run = 0.f, m_use = 0.f;
+      // running max m_run (log2 units, of S * scale * log2 e); P = 2^(s - m_run)
+      float m_run = -INFINITY, l_run = 0.f;
       for (int j = 0; j < n; ++j) {
         const int entry = p.tile_list[beg + j];
         if constexpr (k2)
           mbar_wait_cluster(&s_full[t], s_phase & 1);
         else
           mbar_wait(&s_full[t], s_phase & 1);
-        const bool tr = quarter == 0 && half == 0 && lane == 0;
+        const bool tr = quarter == 0 && lane == 0;
         if (tr) trace_ev(p, 0 + 5 * t, s_phase);
-        const uint32_t par = s_phase & 1;
         ++s_phase;
         tc_fence_after();
         uint32_t s[KC];
@@ -300,7 +275,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
         if (tr) trace_ev(p, 1 + 5 * t, s_phase - 1, __uint_as_float(s[KC - 1]));
         if (entry < 0) {  // partial tile: apply the position mask per element
           const int kt = entry & 0x7FFFFFFF;
-          const int4* kp4 = reinterpret_cast<const int4*>(p.k_pos + kt * kTileN + half * KC);
+          const int4* kp4 = reinterpret_cast<const int4*>(p.k_pos + kt * kTileN);
 #pragma unroll
           for (int c = 0; c < KC / 4; ++c) {
             const int4 kp = __ldg(kp4 + c);
@@ -310,70 +285,61 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
             if (kp.w > qpos) s[4 * c + 3] = __float_as_uint(-INFINITY);
           }
         }
-        float mx0 = __uint_as_float(s[0]), mx1 = __uint_as_float(s[1]);
-        float mx2 = __uint_as_float(s[2]), mx3 = __uint_as_float(s[3]);
-#pragma unroll
-        for (int i = 4; i < KC; i += 4) {
-          mx0 = fmaxf(mx0, __uint_as_float(s[i + 0]));
-          mx1 = fmaxf(mx1, __uint_as_float(s[i + 1]));
-          mx2 = fmaxf(mx2, __uint_as_float(s[i + 2]));
-          mx3 = fmaxf(mx3, __uint_as_float(s[i + 3]));
-        }
-        float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
-        if constexpr (SPL == 2) {
-          // the row max over both halves: both siblings end with the same value
-          sts_f32(xslot(0, par, half), mx);
-          asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-          mx = fmaxf(mx, ld_sh(xslot(0, par, half ^ 1)));
-        }
-        if (tr) trace_ev(p, 2 + 5 * t, s_phase - 1, mx);
-        const float m_new = fmaxf(m_run, mx * sl2);
-        float alpha = 1.f;
-        if (m_run == -INFINITY) {
-          m_run = m_new;  // first visible keys: O holds only zeros so far
-        } else if (m_new > m_run + 8.f) {
-          alpha = ex2(m_run - m_new);
-          m_run = m_new;
-        }
-        m_use = (m_run == -INFINITY) ? 0.f : m_run;
-        const float neg = -m_use;
-        // P = exp2(S*scale*log2e - m), packed to bf16 pairs in place: word i
-        // of s[] is rewritten only after s[2i], s[2i+1] were consumed. In
-        // full tiles POLY of every 8 pairs take the FMA-pipe polynomial
-        // exp2 instead of MUFU.EX2; partial tiles stay on MUFU (exact zeros
-        // for masked keys).
-        const float2 sc2 = make_float2(sl2, sl2), nb2 = make_float2(neg, neg);
+        // Online softmax over 32-column chunks (SoftmaxState::update,
+        // attention.cpp:209-226, with a lazy rescale): chunk c's max is
+        // taken just before its exponentials, so the max of one chunk runs
+        // on the ALU pipe under the MUFU work of the previous one (no
+        // separate row-max phase). The running max moves only when a chunk
+        // max exceeds it by more than 8: P of the chunks already done
+        // (packed bf16) and their partial row sum are then rescaled by
+        // 2^(m_old - m_new) in registers (exact: a power of two), and O by
+        // the tile's total factor below. So every P <= 2^8.
+        const float m_tile0 = m_run;
         float2 acc2 = make_float2(0.f, 0.f);
-        if (POLY > 0 && entry >= 0) {
 #pragma unroll
-          for (int i = 0; i < KC / 2; ++i) {
-            const float2 x = ffma2(make_float2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])),
-                                   sc2, nb2);
-            float2 e;
-            if ((i & 7) >= 8 - POLY) {
-              e = exp2_poly2(x);
-            } else {
-              e.x = ex2(x.x);
-              e.y = ex2(x.y);
-            }
-            acc2 = fadd2(acc2, e);
-            s[i] = pack_bf16x2_pos(e.x, e.y);
+        for (int c = 0; c < KC / 32; ++c) {
+          float mx0 = __uint_as_float(s[32 * c + 0]), mx1 = __uint_as_float(s[32 * c + 1]);
+          float mx2 = __uint_as_float(s[32 * c + 2]), mx3 = __uint_as_float(s[32 * c + 3]);
+#pragma unroll
+          for (int i = 4; i < 32; i += 4) {
+            mx0 = fmaxf(mx0, __uint_as_float(s[32 * c + i + 0]));
+            mx1 = fmaxf(mx1, __uint_as_float(s[32 * c + i + 1]));
+            mx2 = fmaxf(mx2, __uint_as_float(s[32 * c + i + 2]));
+            mx3 = fmaxf(mx3, __uint_as_float(s[32 * c + i + 3]));
           }
-        } else {
+          const float m_c = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+          if (m_c > m_run + 8.f) {  // rare after the first chunk of a unit
+            if (m_run != -INFINITY) {
+              const float a = ex2(m_run - m_c);
+              acc2 = fmul2(acc2, make_float2(a, a));
 #pragma unroll
-          for (int i = 0; i < KC / 2; ++i) {
-            const float2 x = ffma2(make_float2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])),
+              for (int w = 0; w < 16 * c; ++w) {
+                const float lo = __uint_as_float(s[w] << 16), hi = __uint_as_float(s[w] & 0xFFFF0000u);
+                s[w] = pack_bf16x2_pos(lo * a, hi * a);
+              }
+            }
+            m_run = m_c;
+          }
+          const float neg = m_run == -INFINITY ? 0.f : -m_run;
+          const float2 sc2 = make_float2(sl2, sl2), nb2 = make_float2(neg, neg);
+          // P = exp2(S*scale*log2e - m), packed to bf16 pairs in place: word
+          // 16c + i is rewritten after s[32c + 2i], s[32c + 2i + 1] were read.
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float2 x = ffma2(make_float2(__uint_as_float(s[32 * c + 2 * i]),
+                                               __uint_as_float(s[32 * c + 2 * i + 1])),
                                    sc2, nb2);
             float2 e;
             e.x = ex2(x.x);
             e.y = ex2(x.y);
             acc2 = fadd2(acc2, e);
-            s[i] = pack_bf16x2_pos(e.x, e.y);
+            s[16 * c + i] = pack_bf16x2_pos(e.x, e.y);
           }
         }
-        const float sum0 = acc2.x, sum1 = acc2.y;
-        if (tr) trace_ev(p, 3 + 5 * t, s_phase - 1, sum0 + sum1);
-        l_run = l_run * alpha + (sum0 + sum1);  // this warp's columns only (SPL == 2)
+        if (tr) trace_ev(p, 2 + 5 * t, s_phase - 1, m_run);
+        const float alpha = (m_tile0 == -INFINITY || m_tile0 == m_run) ? 1.f : ex2(m_tile0 - m_run);
+        l_run = l_run * alpha + (acc2.x + acc2.y);
+        if (tr) trace_ev(p, 3 + 5 * t, s_phase - 1, l_run);
         if (j > 0) {
           // PV_t(j-1) must be done before P_t is overwritten and O_t rescaled
           if constexpr (k2)
@@ -388,7 +354,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
         if (__any_sync(0xffffffffu, alpha != 1.f)) {
           if (p.rescale_count != nullptr && lane == 0) atomicAdd(p.rescale_count, 1ull);
 #pragma unroll
-          for (int c = 0; c < HS / SPL / 32; ++c) {
+          for (int c = 0; c < HS / 32; ++c) {
             uint32_t o[32];
             tmem_ld32(o_addr + c * 32, o);
             tmem_ld_wait(o);
@@ -407,6 +373,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
         }
         if (tr) trace_ev(p, 4 + 5 * t, s_phase - 1);
       }
+      const float m_use = m_run == -INFINITY ? 0.f : m_run;
 
       // ------------------------------------------------------------ epilogue
       if (n > 0) {  // the unit's last PV_t
@@ -421,16 +388,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
       const size_t row = (static_cast<size_t>(b) * p.q_len + q_row) * p.heads + h;
       const int mode = p.mode;
       const bool merge = mode == static_cast<int>(EpiMode::kMiddle) || mode == static_cast<int>(EpiMode::kLast);
-      // the running LSE of earlier ring steps (read before the sibling
-      // barrier below, after which half 0 may overwrite it)
-      const float acc_lse = (merge && valid) ? p.lse_acc[row] : -INFINITY;
-      if constexpr (SPL == 2) {
-        // the row sum over both halves, added in the same order by both
-        sts_f32(xslot(1, it & 1, half), l_run);
-        asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-        const float other = ld_sh(xslot(1, it & 1, half ^ 1));
-        l_run = half == 0 ? l_run + other : other + l_run;
-      }
+      const float acc_lse = (merge && valid) ? p.lse_acc[row] : -INFINITY;  // earlier ring steps
       const float lse_t = l_run > 0.f ? m_use + log2f(l_run) : -INFINITY;  // log2 domain
       const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
       float w_run = 0.f, w_new = inv_l, lse_out = lse_t;
@@ -450,9 +408,9 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
       const bool write_bf16 =
           mode == static_cast<int>(EpiMode::kSingle) || mode == static_cast<int>(EpiMode::kLast);
       const bool read_acc = mode >= static_cast<int>(EpiMode::kMiddle);
-      const int col0 = half * (HS / SPL);  // this warp's O columns
+      constexpr int col0 = 0;
 #pragma unroll 1
-      for (int c = 0; c < HS / SPL / 32; ++c) {
+      for (int c = 0; c < HS / 32; ++c) {
         float o[32];
         if (n > 0) {
           uint32_t r[32];
@@ -502,7 +460,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
             dst[i] = make_float4(o[4 * i + 0], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
         }
       }
-      if (valid && half == 0) {
+      if (valid) {
         if (write_bf16)
           p.lse[row] = lse_out * 0.69314718055994530942f;  // natural log (attention.cpp:260)
         else
@@ -772,10 +730,10 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS, POLY, SPL>::kThreads, 1)
 }
 
 // --------------------------------------------------------------- launchers
-template <int NQ, int HS, int POLY, int SPL, int MC = 0>
+template <int NQ, int HS, int MC = 0>
 static cudaError_t launch_impl(const FwdParams& p, int grid, cudaStream_t stream) {
-  using C = FwdCfg<NQ, HS, POLY, SPL>;
-  auto kern = fa_fwd_sm100_kernel<NQ, HS, POLY, SPL, MC>;
+  using C = FwdCfg<NQ, HS>;
+  auto kern = fa_fwd_sm100_kernel<NQ, HS, MC>;
   static std::atomic<uint64_t> attr_done{0};  // per instantiation and device
   const cudaError_t e = ensure_smem_attr(kern, C::kSmemBytes, attr_done);
   if (e != cudaSuccess) return e;
@@ -798,41 +756,23 @@ static cudaError_t launch_impl(const FwdParams& p, int grid, cudaStream_t stream
   return cudaGetLastError();
 }
 
-// Development knobs: USP_FA_POLY = POLY/8 of the exponentials on the FMA
-// pipe; USP_FA_SPLIT = softmax warps per lane quarter (1 or 2).
-static int env_setting(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return e ? atoi(e) : dflt;
-}
-
-template <int NQ, int HS>
-static cudaError_t launch_variant(const FwdParams& p, int grid, cudaStream_t stream) {
-  static const int poly = env_setting("USP_FA_POLY", 0);
-  static const int split = env_setting("USP_FA_SPLIT", USPB_FWD_SPLIT);
-  if (split == 1) {
-    switch (poly) {
-      case 2: return launch_impl<NQ, HS, 2, 1>(p, grid, stream);
-      default: return launch_impl<NQ, HS, 0, 1>(p, grid, stream);
-    }
-  }
-  switch (poly) {
-    case 2: return launch_impl<NQ, HS, 2, 2>(p, grid, stream);
-    default: return launch_impl<NQ, HS, 0, 2>(p, grid, stream);
-  }
-}
-
 cudaError_t launch_fa_fwd(const FwdParams& p, int nq, int hs, int grid, cudaStream_t stream) {
   if (p.cluster) {
     if (nq != 2 || hs != 128 || p.pair_rows) return cudaErrorInvalidValue;
-    if (p.cluster == 2) return launch_impl<2, 128, 0, 1, 2>(p, grid, stream);
-    return launch_impl<2, 128, 0, 1, 1>(p, grid, stream);
+#ifdef USPB_DEV_2SM
+    // development build only: cta_group::2 MMAs (measured 886 vs 1276
+    // TFLOP/s for the multicast clusters)
+    if (p.cluster == 2) return launch_impl<2, 128, 2>(p, grid, stream);
+#else
+    if (p.cluster == 2) return cudaErrorNotSupported;
+#endif
+    return launch_impl<2, 128, 1>(p, grid, stream);
   }
-  if (nq == 2 && hs == 128) return launch_variant<2, 128>(p, grid, stream);
-  if (nq == 1 && hs == 128) return launch_variant<1, 128>(p, grid, stream);
-  if (nq == 2 && hs == 64) return launch_variant<2, 64>(p, grid, stream);
-  if (nq == 1 && hs == 64) return launch_variant<1, 64>(p, grid, stream);
+  if (nq == 2 && hs == 128) return launch_impl<2, 128>(p, grid, stream);
+  if (nq == 1 && hs == 128) return launch_impl<1, 128>(p, grid, stream);
+  if (nq == 2 && hs == 64) return launch_impl<2, 64>(p, grid, stream);
+  if (nq == 1 && hs == 64) return launch_impl<1, 64>(p, grid, stream);
   return cudaErrorInvalidValue;
 }
-
 
 }  // namespace uspb200
