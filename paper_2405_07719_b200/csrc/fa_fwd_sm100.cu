@@ -285,61 +285,44 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS>::kThreads, 1)
             if (kp.w > qpos) s[4 * c + 3] = __float_as_uint(-INFINITY);
           }
         }
-        // Online softmax over 32-column chunks (SoftmaxState::update,
-        // attention.cpp:209-226, with a lazy rescale): chunk c's max is
-        // taken just before its exponentials, so the max of one chunk runs
-        // on the ALU pipe under the MUFU work of the previous one (no
-        // separate row-max phase). The running max moves only when a chunk
-        // max exceeds it by more than 8: P of the chunks already done
-        // (packed bf16) and their partial row sum are then rescaled by
-        // 2^(m_old - m_new) in registers (exact: a power of two), and O by
-        // the tile's total factor below. So every P <= 2^8.
-        const float m_tile0 = m_run;
+        float mx0 = __uint_as_float(s[0]), mx1 = __uint_as_float(s[1]);
+        float mx2 = __uint_as_float(s[2]), mx3 = __uint_as_float(s[3]);
+#pragma unroll
+        for (int i = 4; i < KC; i += 4) {
+          mx0 = fmaxf(mx0, __uint_as_float(s[i + 0]));
+          mx1 = fmaxf(mx1, __uint_as_float(s[i + 1]));
+          mx2 = fmaxf(mx2, __uint_as_float(s[i + 2]));
+          mx3 = fmaxf(mx3, __uint_as_float(s[i + 3]));
+        }
+        const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+        if (tr) trace_ev(p, 2 + 5 * t, s_phase - 1, mx);
+        // SoftmaxState::update (attention.cpp:209-226) with a lazy rescale:
+        // the running max only moves when the tile max exceeds it by more
+        // than 8 (log2 units), so P <= 2^8 and O is rescaled rarely.
+        const float m_new = fmaxf(m_run, mx * sl2);
+        float alpha = 1.f;
+        if (m_run == -INFINITY) {
+          m_run = m_new;  // first visible keys: O holds only zeros so far
+        } else if (m_new > m_run + 8.f) {
+          alpha = ex2(m_run - m_new);
+          m_run = m_new;
+        }
+        const float neg = m_run == -INFINITY ? 0.f : -m_run;
+        // P = exp2(S*scale*log2e - m), packed to bf16 pairs in place: word i
+        // of s[] is rewritten only after s[2i], s[2i+1] were consumed.
+        const float2 sc2 = make_float2(sl2, sl2), nb2 = make_float2(neg, neg);
         float2 acc2 = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int c = 0; c < KC / 32; ++c) {
-          float mx0 = __uint_as_float(s[32 * c + 0]), mx1 = __uint_as_float(s[32 * c + 1]);
-          float mx2 = __uint_as_float(s[32 * c + 2]), mx3 = __uint_as_float(s[32 * c + 3]);
-#pragma unroll
-          for (int i = 4; i < 32; i += 4) {
-            mx0 = fmaxf(mx0, __uint_as_float(s[32 * c + i + 0]));
-            mx1 = fmaxf(mx1, __uint_as_float(s[32 * c + i + 1]));
-            mx2 = fmaxf(mx2, __uint_as_float(s[32 * c + i + 2]));
-            mx3 = fmaxf(mx3, __uint_as_float(s[32 * c + i + 3]));
-          }
-          const float m_c = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
-          if (m_c > m_run + 8.f) {  // rare after the first chunk of a unit
-            if (m_run != -INFINITY) {
-              const float a = ex2(m_run - m_c);
-              acc2 = fmul2(acc2, make_float2(a, a));
-#pragma unroll
-              for (int w = 0; w < 16 * c; ++w) {
-                const float lo = __uint_as_float(s[w] << 16), hi = __uint_as_float(s[w] & 0xFFFF0000u);
-                s[w] = pack_bf16x2_pos(lo * a, hi * a);
-              }
-            }
-            m_run = m_c;
-          }
-          const float neg = m_run == -INFINITY ? 0.f : -m_run;
-          const float2 sc2 = make_float2(sl2, sl2), nb2 = make_float2(neg, neg);
-          // P = exp2(S*scale*log2e - m), packed to bf16 pairs in place: word
-          // 16c + i is rewritten after s[32c + 2i], s[32c + 2i + 1] were read.
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float2 x = ffma2(make_float2(__uint_as_float(s[32 * c + 2 * i]),
-                                               __uint_as_float(s[32 * c + 2 * i + 1])),
-                                   sc2, nb2);
-            float2 e;
-            e.x = ex2(x.x);
-            e.y = ex2(x.y);
-            acc2 = fadd2(acc2, e);
-            s[16 * c + i] = pack_bf16x2_pos(e.x, e.y);
-          }
+        for (int i = 0; i < KC / 2; ++i) {
+          const float2 x = ffma2(make_float2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), sc2, nb2);
+          float2 e;
+          e.x = ex2(x.x);
+          e.y = ex2(x.y);
+          acc2 = fadd2(acc2, e);
+          s[i] = pack_bf16x2_pos(e.x, e.y);
         }
-        if (tr) trace_ev(p, 2 + 5 * t, s_phase - 1, m_run);
-        const float alpha = (m_tile0 == -INFINITY || m_tile0 == m_run) ? 1.f : ex2(m_tile0 - m_run);
+        if (tr) trace_ev(p, 3 + 5 * t, s_phase - 1, acc2.x + acc2.y);
         l_run = l_run * alpha + (acc2.x + acc2.y);
-        if (tr) trace_ev(p, 3 + 5 * t, s_phase - 1, l_run);
         if (j > 0) {
           // PV_t(j-1) must be done before P_t is overwritten and O_t rescaled
           if constexpr (k2)

@@ -6,16 +6,17 @@
 // destination row (one head_size vector) is fetched from an affine source
 // row index over four loop dimensions.
 //
-// Bulk path (every permutation the engine issues at a native head size: the
-// innermost dimension is contiguous in source and destination, so a copy is
-// a list of contiguous runs — (t, head range) blocks of heads/U * hs * 2
-// bytes): the TMA bulk-copy engine moves the runs, global -> shared ->
-// global (cp.async.bulk with mbarrier completion, then cp.async.bulk stores
-// in bulk groups), from one issuing lane per warp with a ring of shared
-// memory slots — no per-element instructions, and ONE launch for several
-// tensors (Q, K and V packed together; every peer part of the direct
-// exchange). Vector path (fallback): 32-bit index arithmetic, 16-byte
-// loads with kUnroll in flight per thread. Head sizes that are not a
+// TMA path (every permutation the engine issues at a native head size):
+// source and destination are two strided views of the same logical
+// (i0, i1, i2, i3, element) space, so a permutation is a TMA tensor copy —
+// each box (all hs elements x up to 256 i3 rows x b2 i2 rows) is loaded with
+// cp.async.bulk.tensor from the source map and stored with
+// cp.async.bulk.tensor to the destination map at the SAME coordinates; the
+// strides in the two tensor maps do the transpose. One issuing lane per CTA
+// keeps a ring of shared-memory boxes in flight; no per-element instructions,
+// and ONE launch for several tensors (Q, K and V together; every peer part of
+// the direct exchange). Vector path (fallback): 32-bit index arithmetic,
+// 16-byte loads with kUnroll in flight per thread. Head sizes that are not a
 // multiple of 8 (or padding to a larger destination row) take the scalar
 // path (small test shapes only).
 #include <cuda_bf16.h>
@@ -25,6 +26,8 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
+#include <cuda.h>
 
 #include "ptx_sm100.cuh"
 #include "reshard.hpp"
@@ -101,136 +104,6 @@ __global__ void __launch_bounds__(256) row_permute_scalar(RowPermute p) {
   }
 }
 
-// ----------------------------------------------------------------- bulk path
-constexpr int kBulkWarps = 2;         // independent issuing lanes per CTA
-constexpr int kBulkSlots = 16;        // shared-memory slots per warp
-constexpr int kBulkSlot = 4096;       // bytes per slot
-constexpr int kBulkAhead = 8;         // loads in flight ahead of the stores
-constexpr int kMaxBulkJobs = 48;
-
-struct BulkJob {
-  const uint8_t* src;
-  uint8_t* dst;
-  uint64_t s0, s1, s2, t0, t1, t2;  // byte strides of the three outer dims
-  uint32_t d1, d2;                  // run r = (i0 * d1 + i1) * d2 + i2
-  uint32_t run_bytes;               // contiguous bytes per run (16-byte multiple)
-  uint32_t group;                   // runs per item (run_bytes <= slot) ...
-  uint32_t pieces;                  // ... or slot-sized pieces per run (run_bytes > slot)
-  uint64_t runs;
-  uint64_t first_item;              // prefix of items over the jobs
-};
-struct BulkParams {
-  BulkJob job[kMaxBulkJobs];
-  int njobs;
-  uint64_t total_items;
-};
-
-__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src_smem, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(reinterpret_cast<uint64_t>(dst)),
-               "r"(src_smem), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s_u32(uint32_t dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   dst_smem),
-               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(ptx::smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-
-// Item i of the flattened job list -> (job, run range or piece).
-struct Item {
-  const BulkJob* j;
-  uint64_t run;      // first run
-  uint32_t nruns;    // runs in the item (group mode)
-  uint32_t off, bytes;  // piece mode: byte offset inside the run, piece size
-};
-__device__ __forceinline__ Item locate_item(const BulkParams& p, uint64_t i) {
-  int k = 0;
-  while (k + 1 < p.njobs && p.job[k + 1].first_item <= i) ++k;
-  const BulkJob& j = p.job[k];
-  const uint64_t li = i - j.first_item;
-  Item it;
-  it.j = &j;
-  if (j.pieces > 1) {
-    it.run = li / j.pieces;
-    const uint32_t pc = static_cast<uint32_t>(li % j.pieces);
-    it.nruns = 1;
-    it.off = pc * kBulkSlot;
-    it.bytes = min(static_cast<uint32_t>(kBulkSlot), j.run_bytes - it.off);
-  } else {
-    it.run = li * j.group;
-    const uint64_t left = j.runs - it.run;
-    it.nruns = static_cast<uint32_t>(left < j.group ? left : j.group);
-    it.off = 0;
-    it.bytes = it.nruns * j.run_bytes;
-  }
-  return it;
-}
-__device__ __forceinline__ void run_addr(const BulkJob& j, uint64_t r, const uint8_t*& s, uint8_t*& d) {
-  const uint64_t i2 = r % j.d2;
-  const uint64_t q = r / j.d2;
-  const uint64_t i1 = q % j.d1;
-  const uint64_t i0 = q / j.d1;
-  s = j.src + i0 * j.s0 + i1 * j.s1 + i2 * j.s2;
-  d = j.dst + i0 * j.t0 + i1 * j.t1 + i2 * j.t2;
-}
-
-__global__ void __launch_bounds__(32 * kBulkWarps, 1) row_permute_bulk(const __grid_constant__ BulkParams p) {
-  extern __shared__ __align__(128) uint8_t bulk_smem[];
-  __shared__ __align__(8) uint64_t bars[kBulkWarps][kBulkSlots];
-  const int warp = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) != 0) return;  // one issuing lane per warp
-  uint64_t* bar = bars[warp];
-  for (int s = 0; s < kBulkSlots; ++s) ptx::mbar_init(&bar[s], 1);
-  ptx::fence_barrier_init();
-  const uint32_t base = ptx::smem_u32(bulk_smem) + warp * kBulkSlots * kBulkSlot;
-  const uint64_t lane_id = uint64_t(blockIdx.x) * kBulkWarps + warp;
-  const uint64_t lanes = uint64_t(gridDim.x) * kBulkWarps;
-  const uint64_t cnt = p.total_items > lane_id ? (p.total_items - lane_id + lanes - 1) / lanes : 0;
-  for (uint64_t k = 0; k < cnt + kBulkAhead; ++k) {
-    if (k < cnt) {  // load item k into slot k % S
-      const uint32_t slot = static_cast<uint32_t>(k % kBulkSlots);
-      // the slot's previous item (k - S) must have been read by its store;
-      // stores issued so far: items < k - A, so at most S - A - 1 newer ones
-      if (k >= kBulkSlots) bulk_wait_read<kBulkSlots - kBulkAhead - 1>();
-      const Item it = locate_item(p, lane_id + k * lanes);
-      ptx::mbar_arrive_expect_tx(&bar[slot], it.bytes);
-      uint32_t dst = base + slot * kBulkSlot;
-      for (uint32_t r = 0; r < it.nruns; ++r) {
-        const uint8_t* s;
-        uint8_t* d;
-        run_addr(*it.j, it.run + r, s, d);
-        const uint32_t b = it.j->pieces > 1 ? it.bytes : it.j->run_bytes;
-        bulk_g2s_u32(dst, s + it.off, b, &bar[slot]);
-        dst += b;
-      }
-    }
-    if (k >= kBulkAhead && k - kBulkAhead < cnt) {  // store item k - A
-      const uint64_t m = k - kBulkAhead;
-      const uint32_t slot = static_cast<uint32_t>(m % kBulkSlots);
-      ptx::mbar_wait(&bar[slot], static_cast<uint32_t>((m / kBulkSlots) & 1));
-      const Item it = locate_item(p, lane_id + m * lanes);
-      uint32_t src = base + slot * kBulkSlot;
-      for (uint32_t r = 0; r < it.nruns; ++r) {
-        const uint8_t* s;
-        uint8_t* d;
-        run_addr(*it.j, it.run + r, s, d);
-        const uint32_t b = it.j->pieces > 1 ? it.bytes : it.j->run_bytes;
-        bulk_s2g(d + it.off, src, b);
-        src += b;
-      }
-      bulk_commit();
-    }
-  }
-  bulk_wait_all();
-}
-
 int64_t max_row(const RowPermute& p, const int64_t* stride) {
   int64_t m = 0;
   for (int i = 0; i < 4; ++i) m += (p.dims[i] - 1) * stride[i];
@@ -238,88 +111,206 @@ int64_t max_row(const RowPermute& p, const int64_t* stride) {
 }
 
 
-// RowPermute -> bulk job: the innermost dim must be contiguous in both
-// tensors (then it and any further contiguous dims form one run).
-bool to_bulk_job(const RowPermute& p, BulkJob& j) {
-  if (p.hs_src != p.hs_dst || (p.hs_src * 2) % 16 != 0) return false;
+}  // namespace
+
+// ------------------------------------------------------------------ TMA path
+namespace {
+constexpr int kTmaSlots = 6;
+constexpr int kTmaAhead = 4;          // loads in flight ahead of the stores
+constexpr int kTmaBoxBytes = 32768;
+constexpr int kMaxTmaJobs = 48;
+
+struct alignas(64) TmaJob {
+  CUtensorMap src, dst;                // 5-D (hs, d3, d2, d1, d0) views
+  int n3, n2, n1;                      // boxes along d3, d2, d1 (d0: the rest)
+  int b3, b2;                          // box extent along d3, d2
+  int bytes;                           // full-box bytes (TMA zero-fills / clips the edges)
+  int first;                           // prefix of boxes over the jobs
+  // map dims 2..4 <- logical outer coordinate (0: d2, 1: d1, 2: d0), per map:
+  // each map orders its outer dims by stride (box-1 dims do not change the
+  // box's shared-memory layout, so the two maps may order them differently)
+  unsigned char ps[3], pd[3];
+};
+struct TmaParams {
+  TmaJob job[kMaxTmaJobs];
+  int njobs, total;
+};
+
+__device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(ptx::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap* m, uint32_t src, int c0, int c1, int c2, int c3,
+                                             int c4) {
+  asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+               : "memory");
+}
+
+__device__ __forceinline__ void box_coords(const TmaParams& p, int i, const TmaJob*& j, int& c1, int& c2, int& c3,
+                                           int& c4) {
+  int k = 0;
+  while (k + 1 < p.njobs && p.job[k + 1].first <= i) ++k;
+  j = &p.job[k];
+  int r = i - j->first;
+  const int i3 = r % j->n3;
+  r /= j->n3;
+  const int i2 = r % j->n2;
+  r /= j->n2;
+  const int i1 = r % j->n1;
+  c4 = r / j->n1;
+  c1 = i3 * j->b3;
+  c2 = i2 * j->b2;
+  c3 = i1;
+}
+
+__global__ void __launch_bounds__(32, 1) reshard_tma_kernel(const __grid_constant__ TmaParams p) {
+  extern __shared__ __align__(1024) uint8_t tma_smem[];
+  __shared__ __align__(8) uint64_t bar[kTmaSlots];
+  if (threadIdx.x != 0) return;  // one issuing lane
+  for (int s = 0; s < kTmaSlots; ++s) ptx::mbar_init(&bar[s], 1);
+  ptx::fence_barrier_init();
+  const uint32_t base = (ptx::smem_u32(tma_smem) + 1023u) & ~1023u;
+  const int cnt = p.total > int(blockIdx.x) ? (p.total - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x) : 0;
+  for (int k = 0; k < cnt + kTmaAhead; ++k) {
+    if (k < cnt) {  // load box k into slot k % S
+      const int slot = k % kTmaSlots;
+      // stores issued so far: boxes < k - A; the slot's previous box k - S
+      // must have been read: at most S - A - 1 newer stores may be pending
+      if (k >= kTmaSlots) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kTmaSlots - kTmaAhead - 1) : "memory");
+      const TmaJob* j;
+      int c1, c2, c3, c4;
+      box_coords(p, int(blockIdx.x) + k * int(gridDim.x), j, c1, c2, c3, c4);
+      ptx::mbar_arrive_expect_tx(&bar[slot], static_cast<uint32_t>(j->bytes));
+      const int L[3] = {c2, c3, c4};
+      tma_load_5d(base + slot * kTmaBoxBytes, &j->src, &bar[slot], 0, c1, L[j->ps[0]], L[j->ps[1]], L[j->ps[2]]);
+    }
+    if (k >= kTmaAhead && k - kTmaAhead < cnt) {  // store box k - A
+      const int m = k - kTmaAhead;
+      const int slot = m % kTmaSlots;
+      ptx::mbar_wait(&bar[slot], static_cast<uint32_t>((m / kTmaSlots) & 1));
+      const TmaJob* j;
+      int c1, c2, c3, c4;
+      box_coords(p, int(blockIdx.x) + m * int(gridDim.x), j, c1, c2, c3, c4);
+      const int L[3] = {c2, c3, c4};
+      tma_store_5d(&j->dst, base + slot * kTmaBoxBytes, 0, c1, L[j->pd[0]], L[j->pd[1]], L[j->pd[2]]);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeTiledFn>(nullptr);
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+// RowPermute -> TMA job; false when the shape does not fit the TMA path.
+bool to_tma_job(const RowPermute& p, TmaJob& j) {
+  const EncodeTiledFn enc = encode_tiled();
+  if (!enc || p.hs_src != p.hs_dst || p.hs_src > 256 || (p.hs_src * 2) % 16) return false;
   if (p.src_stride[3] != 1 || p.dst_stride[3] != 1) return false;
   const int64_t row = p.hs_src * 2;
-  int64_t run_rows = p.dims[3];
-  int outer = 2;  // dims[0..outer] are loops
-  while (outer >= 0 && p.src_stride[outer] == run_rows && p.dst_stride[outer] == run_rows) {
-    run_rows *= p.dims[outer];
-    --outer;
-  }
-  int64_t d[3] = {1, 1, 1}, ss[3] = {0, 0, 0}, ts[3] = {0, 0, 0};
-  for (int k = 0; k <= outer; ++k) {  // right-align the remaining loop dims into d[0..2]
-    const int slot = 2 - (outer - k);
-    d[slot] = p.dims[k];
-    ss[slot] = p.src_stride[k] * row;
-    ts[slot] = p.dst_stride[k] * row;
-  }
-  const int64_t run_bytes = run_rows * row;
-  if (run_bytes <= 0 || run_bytes > (int64_t(1) << 30)) return false;
-  for (int k = 0; k < 3; ++k)
-    if (ss[k] % 16 || ts[k] % 16) return false;
+  for (int k = 0; k < 4; ++k)
+    if (p.dims[k] < 1 || p.dims[k] > (int64_t(1) << 31)) return false;
   if (reinterpret_cast<uintptr_t>(p.src) % 16 || reinterpret_cast<uintptr_t>(p.dst) % 16) return false;
-  j.src = static_cast<const uint8_t*>(p.src);
-  j.dst = static_cast<uint8_t*>(p.dst);
-  j.s0 = ss[0], j.s1 = ss[1], j.s2 = ss[2];
-  j.t0 = ts[0], j.t1 = ts[1], j.t2 = ts[2];
-  j.d1 = static_cast<uint32_t>(d[1]);
-  j.d2 = static_cast<uint32_t>(d[2]);
-  j.run_bytes = static_cast<uint32_t>(run_bytes);
-  j.runs = static_cast<uint64_t>(d[0] * d[1] * d[2]);
-  if (run_bytes <= kBulkSlot) {
-    j.group = static_cast<uint32_t>(kBulkSlot / run_bytes);
-    j.pieces = 1;
-  } else {
-    j.group = 1;
-    j.pieces = static_cast<uint32_t>((run_bytes + kBulkSlot - 1) / kBulkSlot);
-  }
+  const int b3 = static_cast<int>(std::min<int64_t>(p.dims[3], 256));
+  const int64_t box_row_bytes = int64_t(b3) * row;
+  if (box_row_bytes > kTmaBoxBytes) return false;
+  const int b2 = static_cast<int>(std::min<int64_t>({p.dims[2], 256, kTmaBoxBytes / box_row_bytes}));
+  // logical outer dims: 0 = d2 (box b2), 1 = d1, 2 = d0 (box 1)
+  const int64_t ext[3] = {p.dims[2], p.dims[1], p.dims[0]};
+  const cuuint32_t bx[3] = {cuuint32_t(b2), 1, 1};
+  auto encode = [&](CUtensorMap* m, const void* ptr, const int64_t* stride, unsigned char* perm) {
+    int64_t st[3] = {stride[2] * row, stride[1] * row, stride[0] * row};
+    int64_t big = row * p.dims[3];
+    for (int k = 0; k < 3; ++k)
+      if (ext[k] > 1) big = std::max(big, st[k]);
+    for (int k = 0; k < 3; ++k)
+      if (ext[k] == 1) st[k] = big;  // any stride; keep the order monotonic
+    int ord[3] = {0, 1, 2};
+    std::stable_sort(ord, ord + 3, [&](int a, int b) { return st[a] < st[b]; });
+    const cuuint64_t dims[5] = {cuuint64_t(p.hs_src), cuuint64_t(p.dims[3]), cuuint64_t(ext[ord[0]]),
+                                cuuint64_t(ext[ord[1]]), cuuint64_t(ext[ord[2]])};
+    const cuuint64_t str[4] = {cuuint64_t(row), cuuint64_t(st[ord[0]]), cuuint64_t(st[ord[1]]),
+                               cuuint64_t(st[ord[2]])};
+    for (int k = 0; k < 4; ++k)
+      if (str[k] % 16 || str[k] >= (cuuint64_t(1) << 40) || str[k] == 0) return false;
+    const cuuint32_t box[5] = {cuuint32_t(p.hs_src), cuuint32_t(b3), bx[ord[0]], bx[ord[1]], bx[ord[2]]};
+    const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    for (int k = 0; k < 3; ++k) perm[k] = static_cast<unsigned char>(ord[k]);
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(ptr), dims, str, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+  if (!encode(&j.src, p.src, p.src_stride, j.ps) || !encode(&j.dst, p.dst, p.dst_stride, j.pd)) return false;
+  j.b3 = b3;
+  j.b2 = b2;
+  j.n3 = static_cast<int>((p.dims[3] + b3 - 1) / b3);
+  j.n2 = static_cast<int>((p.dims[2] + b2 - 1) / b2);
+  j.n1 = static_cast<int>(p.dims[1]);
+  j.bytes = static_cast<int>(box_row_bytes * b2);
+  const int64_t boxes = int64_t(j.n3) * j.n2 * j.n1 * p.dims[0];
+  if (boxes >= (int64_t(1) << 30)) return false;
+  j.first = static_cast<int>(boxes);  // temporarily: this job's box count
   return true;
 }
 
-cudaError_t launch_bulk(const BulkJob* jobs, int n, int num_sms, cudaStream_t stream) {
-  BulkParams bp{};
-  uint64_t items = 0;
+cudaError_t launch_tma(TmaParams& tp, int n, int num_sms, cudaStream_t stream) {
+  int total = 0;
   for (int k = 0; k < n; ++k) {
-    bp.job[k] = jobs[k];
-    bp.job[k].first_item = items;
-    items += jobs[k].pieces > 1 ? jobs[k].runs * jobs[k].pieces : (jobs[k].runs + jobs[k].group - 1) / jobs[k].group;
+    const int boxes = tp.job[k].first;
+    tp.job[k].first = total;
+    total += boxes;
   }
-  bp.njobs = n;
-  bp.total_items = items;
-  if (!items) return cudaSuccess;
-  constexpr int smem = kBulkWarps * kBulkSlots * kBulkSlot;
+  tp.njobs = n;
+  tp.total = total;
+  if (!total) return cudaSuccess;
+  constexpr int smem = kTmaSlots * kTmaBoxBytes + 1024;
   static std::atomic<uint64_t> attr_done{0};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (!(attr_done.load() & (uint64_t(1) << (dev & 63)))) {
-    e = cudaFuncSetAttribute(row_permute_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    e = cudaFuncSetAttribute(reshard_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_done.fetch_or(uint64_t(1) << (dev & 63));
   }
-  const uint64_t lanes_needed = (items + 3) / 4;  // >= 4 items per issuing lane
-  const int grid = static_cast<int>(std::min<uint64_t>(num_sms, (lanes_needed + kBulkWarps - 1) / kBulkWarps));
-  row_permute_bulk<<<grid > 0 ? grid : 1, 32 * kBulkWarps, smem, stream>>>(bp);
+  const int grid = std::max(1, std::min(num_sms, (total + 3) / 4));
+  reshard_tma_kernel<<<grid, 32, smem, stream>>>(tp);
   return cudaGetLastError();
 }
-
 }  // namespace
 
-// Several permutations in one launch: the bulk kernel when every one
-// qualifies (contiguous innermost dim, 16-byte runs, native head size),
-// else one launch each.
+// Several permutations in one launch: the TMA kernel when every one fits it
+// (contiguous innermost dim, native head size), else one launch each.
 cudaError_t launch_row_permute_multi(const RowPermute* ps, int n, int num_sms, cudaStream_t stream,
                                      int* launches) {
-  BulkJob jobs[kMaxBulkJobs];
-  bool bulk = n <= kMaxBulkJobs && !std::getenv("USPB_NO_BULK");
-  for (int k = 0; bulk && k < n; ++k) bulk = to_bulk_job(ps[k], jobs[k]);
-  if (bulk) {
-    if (launches) *launches = 1;
-    return launch_bulk(jobs, n, num_sms, stream);
+  static TmaParams tp;  // host staging (large); launches are issued from one thread per engine
+  static std::mutex mu;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    bool tma = n <= kMaxTmaJobs && !std::getenv("USPB_NO_TMA_RESHARD");
+    for (int k = 0; tma && k < n; ++k) tma = to_tma_job(ps[k], tp.job[k]);
+    if (tma) {
+      if (launches) *launches = 1;
+      return launch_tma(tp, n, num_sms, stream);
+    }
   }
   for (int k = 0; k < n; ++k) {
     const cudaError_t e = launch_row_permute(ps[k], num_sms, stream);

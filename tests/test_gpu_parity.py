@@ -35,6 +35,10 @@ def _check_case(c: UspCase, device):
     assert eo["max_abs"] <= O_TOL and eo["rel_l2"] <= O_REL_L2, msg
     assert el["max_abs"] <= LSE_TOL, msg
     assert all(e.last_launches() >= 1 for e in engines), "native kernels did not launch"
+    if c.ulysses > 1 and c.bs == 1 and c.hs in (64, 128):
+        # the Q/K/V pack is ONE TMA reshard launch, then R attention steps
+        # and the O unpack (a fallback to per-tensor vector copies would add 2)
+        assert all(e.last_launches() == c.ring + 2 for e in engines), [e.last_launches() for e in engines]
     # the collectives each rank actually issued == the planned ledger, which
     # tests/test_ledger.py pins to the reference World's ledger
     from paper_2405_07719_b200.usp import forward_ledger
