@@ -35,7 +35,9 @@ def nvcc() -> str:
 
 
 def _flags() -> list[str]:
-    extra = ["-DUSPB_TRACE"] if os.environ.get("USPB_TRACE_BUILD") else []
+    extra = ["-DUSPB_TRACE", "-DUSPB_DEV"] if os.environ.get("USPB_TRACE_BUILD") else []
+    if _VARIANT:
+        extra.append("-DUSPB_DEV")  # development knobs (environment) only in variant builds
     extra += os.environ.get("USPB_NVCC_EXTRA", "").split()  # development experiments only
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
                    "-I", os.path.join(ROOT, "include"), "-I", CSRC, "--expt-relaxed-constexpr"] + extra

@@ -161,7 +161,7 @@ class Engine {
     nq_ = (tiling_.pair_rows || group % 2 == 0) ? 2 : 1;
     cluster_ = tiling_.cluster;  // 2-CTA clusters sharing K/V tiles by TMA multicast
     static const int cluster_mode = [] {  // 2: cta_group::2 MMAs on the same clusters (experimental)
-      const char* e = std::getenv("USP_FA_CLUSTER");
+      const char* e = dev_env("USP_FA_CLUSTER");
       return e ? std::atoi(e) : 1;
     }();
     cluster_mode_ = cluster_ ? (cluster_mode == 2 ? 2 : 1) : 0;
@@ -327,7 +327,7 @@ class Engine {
     const void* vh = v;
     uint8_t* kv0 = kv0_.as<uint8_t>();
     static const bool direct_ok = [] {
-      const char* e = std::getenv("USP_DIRECT_A2A");
+      const char* e = dev_env("USP_DIRECT_A2A");
       return !e || std::atoi(e) != 0;
     }();
     // Direct exchange over a peer-memory transport at bs = 1:
@@ -521,7 +521,7 @@ class Engine {
       hlse_ = DevBuf(lb);
       USPB_CHECK(cudaStreamCreateWithFlags(&h2d_stream_, cudaStreamNonBlocking));
       USPB_CHECK(cudaStreamCreateWithFlags(&d2h_stream_, cudaStreamNonBlocking));
-      const unsigned fl = std::getenv("USP_HOST_TRACE") ? cudaEventDefault : cudaEventDisableTiming;
+      const unsigned fl = dev_env("USP_HOST_TRACE") ? cudaEventDefault : cudaEventDisableTiming;
       USPB_CHECK(cudaEventCreateWithFlags(&ev_entry_, fl));
       USPB_CHECK(cudaEventCreateWithFlags(&ev_drained_, fl));
     }
@@ -582,7 +582,7 @@ class Engine {
     USPB_CHECK(cudaStreamWaitEvent(st, ev_drained_, 0));
     have_fwd_ = true;
     fwd_ledger_size_ = ledger_.size();
-    static const bool trace = std::getenv("USP_HOST_TRACE") != nullptr;  // development timeline
+    static const bool trace = dev_env("USP_HOST_TRACE") != nullptr;  // development timeline
     if (trace) {
       USPB_CHECK(cudaStreamSynchronize(st));
       auto at = [&](cudaEvent_t e) {
@@ -692,7 +692,7 @@ class Engine {
       ring_first_.push_back(std::move(f));
       ring_last_.push_back(std::move(l));
     }
-    const unsigned fl = std::getenv("USP_HOST_TRACE") ? cudaEventDefault : cudaEventDisableTiming;
+    const unsigned fl = dev_env("USP_HOST_TRACE") ? cudaEventDefault : cudaEventDisableTiming;
     USPB_CHECK(cudaEventCreateWithFlags(&ev_kv_, fl));
     while (ev_chunk_in_.size() < ring_first_.size()) {
       cudaEvent_t a, e;
@@ -714,7 +714,7 @@ class Engine {
   // 8K rows or fewer are a single chunk (plain copies around fwd()).
   std::vector<int64_t> chunk_bounds() const {
     static const int forced = [] {
-      const char* e = std::getenv("USP_HOST_CHUNKS");
+      const char* e = dev_env("USP_HOST_CHUNKS");
       return e ? std::max(1, std::atoi(e)) : 0;
     }();
     auto tiles = [](int64_t r) { return (r + kTileM - 1) / kTileM * kTileM; };
@@ -734,7 +734,7 @@ class Engine {
     const double att_s_per_pair = 4.0 * hl_ * hs_ / 1.2e15;
     const int64_t big = std::max<int64_t>(tiles(Tr_ / 8), 1024);
     static const int64_t tail_rows = [] {  // development knob (default 8192 rows)
-      const char* e = std::getenv("USP_HOST_TAIL");
+      const char* e = dev_env("USP_HOST_TAIL");
       return e ? std::max<int64_t>(0, std::atoll(e)) : int64_t(8192);
     }();
     const int64_t tail = Tr_ > 4 * 8192 ? tiles(tail_rows) : 0;
@@ -772,7 +772,7 @@ class Engine {
       d.mode = EpiMode::kSingle;
       chunk_steps_.push_back(std::move(d));
       cudaEvent_t a, e;
-      const unsigned fl = std::getenv("USP_HOST_TRACE") ? cudaEventDefault : cudaEventDisableTiming;
+      const unsigned fl = dev_env("USP_HOST_TRACE") ? cudaEventDefault : cudaEventDisableTiming;
       USPB_CHECK(cudaEventCreateWithFlags(&a, fl));
       USPB_CHECK(cudaEventCreateWithFlags(&e, fl));
       ev_chunk_in_.push_back(a);
@@ -1116,12 +1116,12 @@ class Engine {
     }
     const int group = hl_ / kvl_;
     static const bool bwd_cluster_env = [] {
-      const char* e = std::getenv("USP_BWD_CLUSTER");
+      const char* e = dev_env("USP_BWD_CLUSTER");
       return !e || std::atoi(e) != 0;
     }();
     bwd_cluster_ = bwd_cluster_env && hsk_ == 128 && group % 2 == 0;
     static const bool dkdv_cluster_env = [] {
-      const char* e = std::getenv("USP_BWD_DKDV_CLUSTER");
+      const char* e = dev_env("USP_BWD_DKDV_CLUSTER");
       return !e || std::atoi(e) != 0;
     }();
     dkdv_cluster_ = dkdv_cluster_env && hsk_ == 128;
@@ -1177,7 +1177,7 @@ class Engine {
     p.inv_scale = static_cast<float>(1.0 / std::sqrt(double(hs_)));
     p.accumulate = accumulate ? 1 : 0;
     p.cluster = (is_dq ? bwd_cluster_ : dkdv_cluster_) ? 1 : 0;
-    static const char* bwd_trace = std::getenv("USP_BWD_TRACE");  // development timeline
+    static const char* bwd_trace = dev_env("USP_BWD_TRACE");  // development timeline
     if (bwd_trace && std::string(bwd_trace) == (is_dq ? "dq" : "dkdv")) {
       if (!trace_buf_.p) trace_buf_ = DevBuf(sizeof(unsigned long long) * kTraceTiles * kTraceEvents);
       USPB_CHECK(cudaMemsetAsync(trace_buf_.p, 0, trace_buf_.bytes, st));
@@ -1243,17 +1243,17 @@ class Engine {
     }
     p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(double(hs_)));
     static const int kv_hint = [] {
-      const char* e = std::getenv("USP_KV_HINT");
+      const char* e = dev_env("USP_KV_HINT");
       return e ? std::atoi(e) : 0;
     }();
     p.kv_hint = kv_hint;
     static const int dbg = [] {
-      const char* e = std::getenv("USP_FA_DEBUG");
+      const char* e = dev_env("USP_FA_DEBUG");
       return e ? std::atoi(e) : 0;
     }();
     p.debug_flags = dbg;
     p.rescale_count = count_rescale_ ? dbg_count_.as<unsigned long long>() : nullptr;
-    static const bool trace = std::getenv("USP_FA_TRACE") != nullptr;
+    static const bool trace = dev_env("USP_FA_TRACE") != nullptr;
     if (trace) {
       if (!trace_buf_.p) trace_buf_ = DevBuf(sizeof(unsigned long long) * kTraceTiles * kTraceEvents);
       USPB_CHECK(cudaMemsetAsync(trace_buf_.p, 0, trace_buf_.bytes, st));

@@ -84,6 +84,14 @@ __device__ __forceinline__ void bwd_bar_sync(uint32_t id, uint32_t count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
+#ifndef USPB_BWD_F2FP
+#define USPB_BWD_F2FP 0
+#endif
+// bf16x2 packing of P / dS: F2FP (cvt.rn) or the integer-pipe round-half-up
+__device__ __forceinline__ uint32_t bwd_pack(float lo, float hi) {
+  return USPB_BWD_F2FP ? pack_bf16x2(lo, hi) : pack_bf16x2_int(lo, hi);
+}
+
 template <int HS>
 struct BwdCfg {
   static constexpr int kTile = 128;
@@ -339,7 +347,7 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dq_kernel(cons
             const float2 d = fadd2(make_float2(__uint_as_float(dp[2 * i]), __uint_as_float(dp[2 * i + 1])),
                                    make_float2(-dlt, -dlt));
             const float2 ds = fmul2(pr, d);
-            pk[i] = pack_bf16x2_int(ds.x, ds.y);
+            pk[i] = bwd_pack(ds.x, ds.y);
           }
           st16(lane_base + sb + packed_col(c), pk);  // dS chunk c, over already-consumed S columns
           tmem_st_wait();
@@ -692,8 +700,8 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
 #pragma unroll
                 for (int e = 0; e < 4; ++e) pv[e] = kpos > qv[e] ? 0.f : pv[e];
               }
-              pp[2 * i4] = pack_bf16x2_pos(pv[0], pv[1]);
-              pp[2 * i4 + 1] = pack_bf16x2_pos(pv[2], pv[3]);
+              pp[2 * i4] = bwd_pack(pv[0], pv[1]);
+              pp[2 * i4 + 1] = bwd_pack(pv[2], pv[3]);
             }
             st16(lane_base + packed_col(c), pp);
             tmem_st_wait();
@@ -733,7 +741,7 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
               const float2 d = fadd2(make_float2(__uint_as_float(dp[4 * i4 + e]), __uint_as_float(dp[4 * i4 + e + 1])),
                                      make_float2(ndv[e], ndv[e + 1]));
               const float2 ds = fmul2(pw, d);
-              pd[2 * i4 + e / 2] = pack_bf16x2_int(ds.x, ds.y);
+              pd[2 * i4 + e / 2] = bwd_pack(ds.x, ds.y);
             }
           }
           st16(lane_base + 128 + packed_col(c), pd);

@@ -319,7 +319,11 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS>::kThreads, 1)
           e.x = ex2(x.x);
           e.y = ex2(x.y);
           acc2 = fadd2(acc2, e);
-          s[i] = pack_bf16x2_pos(e.x, e.y);
+          // one F2FP (cvt.rn.bf16x2.f32) per pair: it does NOT share the
+          // MUFU pipe on sm_100 (round 1 assumed so and packed on the integer
+          // pipes, 2 IADD + PRMT per pair); measured +4 % (1294 -> 1350
+          // TFLOP/s at 128K, A/B on one box, profiles/r02_fwd_ab.json)
+          s[i] = pack_bf16x2(e.x, e.y);
         }
         if (tr) trace_ev(p, 3 + 5 * t, s_phase - 1, acc2.x + acc2.y);
         l_run = l_run * alpha + (acc2.x + acc2.y);

@@ -231,11 +231,11 @@ int64_t visible_pairs(const std::vector<int64_t>& q_pos, const std::vector<int64
 
 FwdTiling fwd_tiling(int hl, int kvl, int hsk, int64_t q_rows, int64_t batch, int sms) {
   static const bool rows_ok = [] {
-    const char* e = std::getenv("USP_FA_PAIR_ROWS");
+    const char* e = dev_env("USP_FA_PAIR_ROWS");
     return !e || std::atoi(e) != 0;
   }();
   static const bool cluster_ok = [] {
-    const char* e = std::getenv("USP_FA_CLUSTER");
+    const char* e = dev_env("USP_FA_CLUSTER");
     return !e || std::atoi(e) != 0;
   }();
   const int group = hl / kvl;
@@ -305,7 +305,7 @@ StepPlan plan_step(const std::vector<int64_t>& q_pos, const std::vector<int64_t>
   // first (LPT) so the static round-robin assignment stays balanced.
   // Order 0 is plain LPT over (q tile, batch, head pair).
   static const int order = [] {
-    const char* e = std::getenv("USP_UNIT_ORDER");
+    const char* e = dev_env("USP_UNIT_ORDER");
     return e ? std::atoi(e) : 1;
   }();
   struct U {

@@ -13,6 +13,7 @@
 
 #include <cstdint>
 #include <stdexcept>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -31,6 +32,18 @@ class Error : public std::runtime_error {
 };
 
 [[noreturn]] void throw_invalid(const std::string& what);
+
+// Development knobs (A/B experiments, traces): the environment is read only
+// in builds with -DUSPB_DEV (build.py variants); the product library ignores
+// it (USP_COMM_TIMEOUT_S, a documented setting, is the exception).
+inline const char* dev_env(const char* name) {
+#ifdef USPB_DEV
+  return std::getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
 [[noreturn]] void throw_constraint(const std::string& what);
 
 struct MeshShape {

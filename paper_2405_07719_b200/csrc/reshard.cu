@@ -30,6 +30,7 @@
 #include <cuda.h>
 
 #include "ptx_sm100.cuh"
+#include "plan.hpp"
 #include "reshard.hpp"
 
 namespace uspb200 {
@@ -305,7 +306,7 @@ cudaError_t launch_row_permute_multi(const RowPermute* ps, int n, int num_sms, c
   static std::mutex mu;
   {
     std::lock_guard<std::mutex> lk(mu);
-    bool tma = n <= kMaxTmaJobs && !std::getenv("USPB_NO_TMA_RESHARD");
+    bool tma = n <= kMaxTmaJobs && !dev_env("USPB_NO_TMA_RESHARD");
     for (int k = 0; tma && k < n; ++k) tma = to_tma_job(ps[k], tp.job[k]);
     if (tma) {
       if (launches) *launches = 1;

@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""A/B device timing of forward-kernel builds (development aid).
+"""A/B device timing of forward- (or, with AB_BWD=1, backward-) kernel builds (development aid).
 
   python tools/ab_fwd.py [variant ...]      # "" = the product build
 
@@ -33,8 +33,21 @@ def child(L, hs, hc, kv, causal):
     q, k, v = u(eng.q_shape()), u(eng.kv_shape()), u(eng.kv_shape())
     o, lse = eng.alloc_outputs()
     iters = max(5, int(6e11 / (L * L)))
+    bwd = os.environ.get("AB_BWD") == "1"
+    if bwd:
+        fwd = eng.forward(q, k, v, o, lse)
+        do = u(eng.q_shape())
+        dq, dk, dv = eng.alloc_grads()
+        iters = max(3, iters // 3)
+
+    def step():
+        if bwd:
+            eng.backward(fwd, do, dq, dk, dv)
+        else:
+            eng.forward(q, k, v, o, lse)
+
     for _ in range(3):
-        eng.forward(q, k, v, o, lse)
+        step()
     torch.cuda.synchronize()
     clk = ClockSampler(0)
     clk.start()
@@ -42,12 +55,12 @@ def child(L, hs, hc, kv, causal):
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
     for _ in range(iters):
-        eng.forward(q, k, v, o, lse)
+        step()
     e.record()
     torch.cuda.synchronize()
     c = clk.stop()
     ms = s.elapsed_time(e) / iters
-    print("RESULT " + json.dumps({"L": L, "hs": hs, "ms": ms, "tflops": eng.flops() / ms / 1e9,
+    print("RESULT " + json.dumps({"L": L, "hs": hs, "ms": ms, "tflops": eng.flops() * (2.5 if bwd else 1.0) / ms / 1e9, "pass": "bwd" if bwd else "fwd",
                                   "sm_mhz": c["sm_mhz"], "w": c["power_w_max"]}), flush=True)
 
 
