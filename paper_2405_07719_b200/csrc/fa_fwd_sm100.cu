@@ -642,6 +642,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS>::kThreads, 1)
           for (int j = 0; j < n; ++j) {
             const uint32_t ki = kv_it + 2 * j;
             wait_full(ki);
+            if (lane == 0) trace_ev(p, 14, s_count / NQ);  // K_j landed (S warp)
 #pragma unroll
             for (int t = 0; t < NQ; ++t) {
               if (s_count > 0) {
@@ -651,6 +652,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS>::kThreads, 1)
                   mbar_wait(s_free, f_phase & 1);
                 ++f_phase;
               }
+              if (t == 0 && lane == 0) trace_ev(p, 15, s_count / NQ);  // S buffer free for S_A(j)
               tc_fence_after();
               issue_qk(t, ki % NS);
               commit(&s_full[t]);

@@ -20,12 +20,15 @@ buf = np.zeros(16 * 256, np.uint64)
 assert lib().usp_engine_trace_copy(eng._h, buf.ctypes.data_as(ctypes.c_void_p)) == 1
 t = buf.reshape(16, 256).astype(np.int64)
 base = t[0, 1]
-names = ["A:S", "A:ld", "A:max", "A:exp", "A:P", "B:S", "B:ld", "B:max", "B:exp", "B:P", "M:PA", "M:issA", "M:PB", "M:issB"]
+names = ["A:S", "A:ld", "A:max", "A:exp", "A:P", "B:S", "B:ld", "B:max", "B:exp", "B:P", "M:PA", "M:issA", "M:PB", "M:issB", "S:K", "S:free"]
 print("tile " + " ".join(f"{n:>7}" for n in names))
 for i in range(2, 40):
-    print(f"{i:4d} " + " ".join(f"{(t[e, i] - base) if t[e, i] else -1:7d}" for e in range(14)))
+    print(f"{i:4d} " + " ".join(f"{(t[e, i] - base) if t[e, i] else -1:7d}" for e in range(16)))
 d = lambda a, b: np.median((t[b, 4:200] - t[a, 4:200]))
 print("median A: S->ld %.0f ld->max %.0f max->exp %.0f exp->P %.0f | period A %.0f" % (d(0, 1), d(1, 2), d(2, 3), d(3, 4), np.median(np.diff(t[0, 4:200]))))
 print("median B: S->ld %.0f ld->max %.0f max->exp %.0f exp->P %.0f" % (d(5, 6), d(6, 7), d(7, 8), d(8, 9)))
 print("median P_A arrive->MMA sees %.0f ; MMA sees->issued %.0f ; issued->next S_A seen %.0f" % (
     np.median(t[10, 4:200] - t[4, 4:200]), np.median(t[11, 4:200] - t[10, 4:200]), np.median(t[0, 5:201] - t[11, 4:200])))
+print("median S warp: K_j landed -> S_A(j) buffer free %.0f ; S_A(j) seen by softmax - buffer free %.0f ; "
+      "A:P(j-1) stored -> K_j landed %.0f" % (np.median(t[15, 4:200] - t[14, 4:200]), np.median(t[0, 4:200] - t[15, 4:200]),
+                                            np.median(t[14, 4:200] - t[4, 3:199])))
