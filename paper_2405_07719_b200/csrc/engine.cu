@@ -93,6 +93,27 @@ static CUtensorMap make_tmap(const void* base, int64_t hs, int64_t heads, int64_
   return m;
 }
 
+// fp32 (hs, heads, seq, batch) map for the fused backward's TMA reductions:
+// box (32 columns, 1, 32 rows, 1) = 128-byte rows, 128B-swizzled in shared memory.
+static CUtensorMap make_tmap_f32(void* base, int64_t hs, int64_t heads, int64_t seq, int64_t batch) {
+  CUtensorMap m;
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(hs), static_cast<cuuint64_t>(heads),
+                              static_cast<cuuint64_t>(seq), static_cast<cuuint64_t>(batch)};
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(hs * 4), static_cast<cuuint64_t>(heads * hs * 4),
+                                 static_cast<cuuint64_t>(seq * heads * hs * 4)};
+  const cuuint32_t box[4] = {32, 1, 32, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    std::ostringstream os;
+    os << "cuTensorMapEncodeTiled (fp32) failed (" << int(r) << ")";
+    throw Error(ErrorCode::kInternal, os.str());
+  }
+  return m;
+}
+
 // ------------------------------------------------------------ device memory
 struct DevBuf {
   void* p = nullptr;
@@ -261,6 +282,7 @@ class Engine {
   }
   // SMs the attention grid leaves free for a concurrent communication kernel
   // (default: the sizing above).
+  void set_deterministic(bool on) { deterministic_ = on; }  // plans follow at the next backward
   void set_reserved_sms(int n) {
     if (n < 0 || n >= num_sms_) throw_invalid("reserved SMs must be in [0, #SMs)");
     reserved_sms_ = n;
@@ -823,8 +845,11 @@ class Engine {
     }
     record_a2a(4, q_part_);
     // delta = rowsum(dO * O) (output_dot_rows, attention.cpp:266-280)
+    const bool fused = use_fused_bwd();
+    const float inv_scale = static_cast<float>(1.0 / std::sqrt(double(hs_)));
     USPB_CHECK(launch_bwd_delta(oh, doh, delta_.as<float>(), B_, Tr_, hl_, hsk_, lse,
-                                bwd_steps_[0].dkdv.q_pos.as<int32_t>(), qvec_.as<float>(), st));
+                                (fused ? bwd_steps_[0].fused : bwd_steps_[0].dkdv).q_pos.as<int32_t>(),
+                                qvec_.as<float>(), fused ? inv_scale : 1.f, st));
     ++launches_;
 
     // -- 2. ring backward
@@ -837,6 +862,9 @@ class Engine {
     const size_t gkv = size_t(B_) * Tr_ * kvl_ * hsk_;  // fp32 elements of one of dK / dV
     float* own = own_dkv_.as<float>();
     int cur = 0;  // acc_dkv_[cur] holds the circulating partial
+    if (fused) {
+      ring_bwd_fused(tm_q, tm_do, kbuf, vbuf, lse, gkv, cur, st);
+    } else {
     for (int t = 0; t < R_; ++t) {
       if (t + 1 < R_) {
         USPB_CHECK(cudaEventRecord(ev_pre_[t], st));
@@ -851,7 +879,7 @@ class Engine {
       if (t > 0) USPB_CHECK(cudaStreamWaitEvent(st, ev_recv_[t - 1], 0));  // K/V(t) (and acc) landed
       const BwdStep& bs = bwd_steps_[t];
       float* tgt = t == 0 ? own : acc_dkv_[cur].as<float>();
-      launch_bwd_kernel(false, bs.dkdv, tm_q, tm_do, kbuf(t), vbuf(t), lse, nullptr, tgt, tgt + gkv,
+      launch_bwd_kernel(0, bs.dkdv, tm_q, tm_do, kbuf(t), vbuf(t), lse, nullptr, tgt, tgt + gkv,
                         t >= 2, st);
       if (t >= 1) {
         // ship the partial to the next ring rank (overlaps the dQ kernel)
@@ -870,10 +898,11 @@ class Engine {
           USPB_CHECK(cudaEventRecord(ev_acc_[0], comm_stream_));
         }
       }
-      launch_bwd_kernel(true, bs.dq, tm_q, tm_do, kbuf(t), vbuf(t), lse, dq_acc_.as<float>(), nullptr,
+      launch_bwd_kernel(1, bs.dq, tm_q, tm_do, kbuf(t), vbuf(t), lse, dq_acc_.as<float>(), nullptr,
                         nullptr, t > 0, st);
     }
     if (R_ > 1) USPB_CHECK(cudaStreamWaitEvent(st, ev_acc_[0], 0));
+    }
 
     // -- 3. casts (+ dK = acc + own) and the dQ, dK, dV all-to-alls out
     const float* acc = R_ > 1 ? acc_dkv_[cur].as<float>() : nullptr;
@@ -1079,9 +1108,65 @@ class Engine {
     ++launches_;
   }
 
+  // Ring backward with the fused kernel (ring_attention.cpp:79-155): step t
+  // runs ONE kernel on K/V block src = (r - t) mod R that writes this step's
+  // dK/dV block and reduces its dQ contribution into dq_acc_ (zeroed first).
+  // The circulating partial is formed as in the reference: t = 0 keeps the
+  // own block, t = 1 starts the partial, t >= 2 adds the block into the
+  // received partial (add_into, :129-134) — the kernel writes the block to a
+  // scratch buffer so it does not wait for the partial's shift, only the
+  // small fp32 add does. Shifts: K/V ahead of the kernel (as the forward),
+  // the partial after the add; both on comm_stream_, overlapping the next
+  // step's kernel.
+  template <class KB, class VB>
+  void ring_bwd_fused(const CUtensorMap& tm_q, const CUtensorMap& tm_do, KB kbuf, VB vbuf, const float* lse,
+                      size_t gkv, int& cur, cudaStream_t st) {
+    USPB_CHECK(cudaMemsetAsync(dq_acc_.p, 0, dq_acc_.bytes, st));
+    float* own = own_dkv_.as<float>();
+    for (int t = 0; t < R_; ++t) {
+      if (t + 1 < R_) {
+        USPB_CHECK(cudaEventRecord(ev_pre_[t], st));  // kernel t-1 done with buf(t+1)
+        USPB_CHECK(cudaStreamWaitEvent(comm_stream_, ev_pre_[t], 0));
+        record_shift(1);
+        record_shift(2);
+        tr_->ring_shift(*groups_, {kbuf(t), vbuf(t)},
+                        {const_cast<void*>(kbuf(t + 1)), const_cast<void*>(vbuf(t + 1))},
+                        {kv_bytes_, kv_bytes_}, comm_stream_);
+        USPB_CHECK(cudaEventRecord(ev_recv_[t], comm_stream_));
+      }
+      if (t > 0) USPB_CHECK(cudaStreamWaitEvent(st, ev_recv_[t - 1], 0));  // K/V(t) landed
+      float* tgt = t == 0 ? own : (t == 1 ? acc_dkv_[cur].as<float>() : blk_dkv_.as<float>());
+      launch_bwd_kernel(2, bwd_steps_[t].fused, tm_q, tm_do, kbuf(t), vbuf(t), lse, dq_acc_.as<float>(), tgt,
+                        tgt + gkv, false, st);
+      if (t >= 1) {
+        float* a = acc_dkv_[cur].as<float>();
+        if (t >= 2) {  // the partial shifted after step t-1 has landed: partial = block + partial
+          USPB_CHECK(cudaStreamWaitEvent(st, ev_acc_[0], 0));
+          USPB_CHECK(launch_add_f32(blk_dkv_.as<float>(), a, static_cast<int64_t>(2 * gkv), st));
+          ++launches_;
+        }
+        USPB_CHECK(cudaEventRecord(ev_acc_[t], st));
+        USPB_CHECK(cudaStreamWaitEvent(comm_stream_, ev_acc_[t], 0));
+        record_shift(6, 4);
+        record_shift(7, 4);
+        float* b = acc_dkv_[cur ^ 1].as<float>();
+        tr_->ring_shift(*groups_, {a, a + gkv}, {b, b + gkv}, {gkv * 4, gkv * 4}, comm_stream_);
+        cur ^= 1;
+        USPB_CHECK(cudaEventRecord(ev_acc_[0], comm_stream_));
+      }
+    }
+    if (R_ > 1) USPB_CHECK(cudaStreamWaitEvent(st, ev_acc_[0], 0));
+  }
+
   struct BwdStep {
-    DevStep dq, dkdv;
+    DevStep dq, dkdv;  // two-kernel (deterministic) backward
+    DevStep fused;     // one-kernel backward: dK/dV units over single key tiles
   };
+  // The fused backward (one kernel per ring step, dQ reduced with fp32
+  // atomics) is the default at head size 128; usp_engine_set_deterministic
+  // selects the two-kernel path, whose dQ is accumulated in a fixed order and
+  // is bitwise reproducible.
+  bool use_fused_bwd() const { return hsk_ == 128 && !deterministic_; }
   static void upload_plan(DevStep& d, StepPlan&& h) {
     d.host = std::move(h);
     d.q_pos = upload(d.host.q_pos);
@@ -1092,7 +1177,15 @@ class Engine {
   }
 
   void ensure_bwd_buffers() {
-    if (!bwd_steps_.empty()) return;
+    const bool fused = use_fused_bwd();
+    if (!bwd_steps_.empty() && bwd_fused_built_ == fused) return;
+    const size_t kv_elems = size_t(B_) * Tr_ * kvl_ * hsk_;
+    if (fused && R_ > 2 && !blk_dkv_.p) blk_dkv_ = DevBuf(2 * kv_elems * sizeof(float));
+    if (!bwd_steps_.empty()) {  // mode switch: rebuild the plans only
+      bwd_steps_.clear();
+      build_bwd_plans(fused);
+      return;
+    }
     const bool reshape = U_ > 1 || hs_ != hsk_;
     const size_t q_heads = size_t(B_) * Tr_ * hl_ * hsk_;
     const size_t kv_heads = size_t(B_) * Tr_ * kvl_ * hsk_;
@@ -1114,6 +1207,11 @@ class Engine {
       grad_h_ = DevBuf(U_ * (q_part_ + 2 * kv_part_));
       grad_recv_ = DevBuf(U_ * (q_part_ + 2 * kv_part_));
     }
+    build_bwd_plans(fused);
+  }
+
+  void build_bwd_plans(bool fused) {
+    bwd_fused_built_ = fused;
     const int group = hl_ / kvl_;
     static const bool bwd_cluster_env = [] {
       const char* e = dev_env("USP_BWD_CLUSTER");
@@ -1132,6 +1230,11 @@ class Engine {
       BwdStep bs;
       // dQ: t = 0 writes every row (empties included), later steps accumulate
       StepPlan fq = plan_step(my_pos, k_pos, shape_.causal, B_, hl_, t == 0, group);
+      if (fused) {  // dK/dV units write every key row at every step (fresh block each time)
+        upload_plan(bs.fused, transpose_plan(fq, B_, kvl_, true));
+        bwd_steps_.push_back(std::move(bs));
+        continue;
+      }
       // dK/dV: t = 0 (own) and t = 1 (new partial) write every key row
       // (over key-tile pairs when 2-CTA clusters share the Q / dO tiles)
       upload_plan(bs.dkdv, dkdv_cluster_ ? transpose_plan_pairs(fq, B_, kvl_, t <= 1)
@@ -1144,7 +1247,8 @@ class Engine {
     }
   }
 
-  void launch_bwd_kernel(bool is_dq, const DevStep& s, const CUtensorMap& tm_q, const CUtensorMap& tm_do,
+  // kind: 0 dK/dV kernel, 1 dQ kernel, 2 fused kernel
+  void launch_bwd_kernel(int kind, const DevStep& s, const CUtensorMap& tm_q, const CUtensorMap& tm_do,
                          const void* kb, const void* vb, const float* lse, float* dq, float* dk, float* dv,
                          bool accumulate, cudaStream_t st) {
     if (s.host.units.empty()) return;
@@ -1161,12 +1265,13 @@ class Engine {
     p.dq = dq;
     p.dk = dk;
     p.dv = dv;
+    if (kind == 2) p.tm_dq = make_tmap_f32(dq, hsk_, hl_, Tr_, B_);
     p.units = s.units.as<uint32_t>();
     p.tile_off = s.tile_off.as<int32_t>();
     p.tile_list = s.tile_list.as<int32_t>();
     p.q_pos = s.q_pos.as<int32_t>();
     p.k_pos = s.k_pos.as<int32_t>();
-    p.sched = sched_.as<int>() + (is_dq ? 4 : 8);
+    p.sched = sched_.as<int>() + 4 * (kind + 1);
     p.num_units = static_cast<int>(s.host.units.size());
     p.batch = static_cast<int>(B_);
     p.q_len = static_cast<int>(Tr_);
@@ -1176,9 +1281,9 @@ class Engine {
     p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(double(hs_)));
     p.inv_scale = static_cast<float>(1.0 / std::sqrt(double(hs_)));
     p.accumulate = accumulate ? 1 : 0;
-    p.cluster = (is_dq ? bwd_cluster_ : dkdv_cluster_) ? 1 : 0;
+    p.cluster = kind == 2 ? 0 : ((kind == 1 ? bwd_cluster_ : dkdv_cluster_) ? 1 : 0);
     static const char* bwd_trace = dev_env("USP_BWD_TRACE");  // development timeline
-    if (bwd_trace && std::string(bwd_trace) == (is_dq ? "dq" : "dkdv")) {
+    if (bwd_trace && std::string(bwd_trace) == (kind == 2 ? "fused" : kind == 1 ? "dq" : "dkdv")) {
       if (!trace_buf_.p) trace_buf_ = DevBuf(sizeof(unsigned long long) * kTraceTiles * kTraceEvents);
       USPB_CHECK(cudaMemsetAsync(trace_buf_.p, 0, trace_buf_.bytes, st));
       p.trace = trace_buf_.as<unsigned long long>();
@@ -1192,7 +1297,9 @@ class Engine {
       e1 = timing_event(2 * timed_.size() + 1);
       USPB_CHECK(cudaEventRecord(e0, st));
     }
-    USPB_CHECK(is_dq ? launch_bwd_dq(p, hsk_, grid, st) : launch_bwd_dkdv(p, hsk_, grid, st));
+    USPB_CHECK(kind == 2   ? launch_bwd_fused(p, hsk_, grid, st)
+               : kind == 1 ? launch_bwd_dq(p, hsk_, grid, st)
+                           : launch_bwd_dkdv(p, hsk_, grid, st));
     ++launches_;
     if (timing_) {
       USPB_CHECK(cudaEventRecord(e1, st));
@@ -1418,6 +1525,9 @@ class Engine {
   bool cluster_ = false;
   bool bwd_cluster_ = false;
   bool dkdv_cluster_ = false;
+  bool deterministic_ = false;
+  bool bwd_fused_built_ = false;
+  DevBuf blk_dkv_;  // fused backward, R > 2: this step's dK/dV block before it joins the partial
   int cluster_mode_ = 0;
   int64_t B_ = 1, T_ = 0, Tr_ = 0;
   int num_sms_ = 148;
@@ -1795,6 +1905,11 @@ usp_status usp_engine_get_info(const usp_engine* engine, usp_engine_info* out) {
     out->ring_step_ms_est = i.step_ms_est;
     out->required_gbs = i.required_gbs;
   });
+}
+
+usp_status usp_engine_set_deterministic(usp_engine* engine, int32_t on) {
+  if (!engine) return USP_INVALID_INPUT;
+  return guarded([&] { engine->impl->set_deterministic(on != 0); });
 }
 
 usp_status usp_engine_set_reserved_sms(usp_engine* engine, int32_t n) {

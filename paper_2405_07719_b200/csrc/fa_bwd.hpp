@@ -17,6 +17,9 @@ namespace uspb200 {
 
 struct BwdParams {
   CUtensorMap tm_q, tm_k, tm_v, tm_do;  // (hs, heads, len, batch) bf16, box (64,1,128,1), SW128
+  // fused kernel: the fp32 dQ accumulator (hs, heads, q_len, batch), box
+  // (32, 1, 32, 1), 128B swizzle — target of the TMA reductions
+  CUtensorMap tm_dq;
   const float* lse;    // natural-log LSE (batch, q_len, heads)
   const float* delta;  // rowsum(dO * O) (batch, q_len, heads)
   float* dq;           // fp32 (batch, q_len, heads, hs)      [dq kernel]
@@ -49,13 +52,22 @@ struct BwdParams {
 
 cudaError_t launch_bwd_dq(const BwdParams& p, int hs, int grid, cudaStream_t stream);
 cudaError_t launch_bwd_dkdv(const BwdParams& p, int hs, int grid, cudaStream_t stream);
+// Both in one kernel (head size 128): units / CSR as for the dK/dV kernel
+// (transpose_plan, single key tiles); dK / dV written like the dK/dV kernel,
+// dQ (scaled) REDUCED into p.dq with fp32 atomics (caller zeroes it first).
+cudaError_t launch_bwd_fused(const BwdParams& p, int hs, int grid, cudaStream_t stream);
 // delta[row] = sum_s o[row][s] * dout[row][s]  (output_dot_rows, attention.cpp:266-280)
 // over rows (b, t, h) of a (batch, q_len, heads, hs) tensor; with qvec also
 // the dK/dV kernel's per-q-tile vectors (see BwdParams::qvec) from lse and
-// the effective q positions (padded to whole tiles).
+// the effective q positions (padded to whole tiles), the -delta entries
+// multiplied by qvec_delta_scale (1 for the dK/dV kernel; 1/sqrt(hs) for the
+// fused kernel, whose dS carries the softmax scale).
 cudaError_t launch_bwd_delta(const void* o, const void* dout, float* delta, int64_t batch, int64_t q_len,
                              int heads, int hs, const float* lse, const int32_t* q_pos, float* qvec,
-                             cudaStream_t stream);
+                             float qvec_delta_scale, cudaStream_t stream);
+// acc = blk + acc, n fp32 elements (n % 4 == 0): the ring's circulating
+// dK/dV partial plus this step's block (add_into, ring_attention.cpp:129-134).
+cudaError_t launch_add_f32(const float* blk, float* acc, int64_t n, cudaStream_t stream);
 // dst = bf16(src [+ src2]), rows of hs_src -> hs_dst (drops padding);
 // the sum is (src + src2) in that order (ring_attention.cpp:145-150).
 cudaError_t launch_cast_rows(const float* src, const float* src2, void* dst, int64_t rows, int hs_src,

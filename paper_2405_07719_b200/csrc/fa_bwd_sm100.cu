@@ -44,6 +44,9 @@
 #ifndef USPB_DKDV_SWAP
 #define USPB_DKDV_SWAP 1  // Q / dO slot roles alternate per ring round (qd_slot)
 #endif
+#ifndef USPB_FUSED_NORED
+#define USPB_FUSED_NORED 0  // development A/B: the fused kernel's drain skips the dQ reductions
+#endif
 #ifndef USPB_DKDV_STAGES
 #define USPB_DKDV_STAGES 6
 #endif
@@ -948,9 +951,489 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
   if (warp == C::kMmaWarp) tmem_dealloc(tmem, 512);
 }
 
+// ============================================================ fused kernel
+// One kernel for the whole block backward (attention_block_backward,
+// attention.cpp:282-324): unit = (batch, kv head, 128-row key tile), loop
+// over the visible q tiles (descending, see below) x the GQA group's q heads.
+// Five GEMMs per (key tile, q tile) instead of the two-kernel path's seven:
+//   S^T  = K Q^T            SS -> TMEM [0,128)
+//   dP^T = V dO^T           SS -> TMEM [128,256)
+//   dV  += P^T dO           TS (P^T bf16 over consumed S^T columns) -> [256,384)
+//   dQ   = dS K             SS, both MN-major -> TMEM [128,256) (dP^T consumed)
+//   dK  += dS^T Q           SS (dS^T K-major from shared memory) -> [384,512)
+// The compute warps store dS^T (bf16) once, into a 128B-swizzled shared tile
+// — the slot of the tile's dO, dead once the dV MMAs completed — that serves
+// as dK's K-major A and dQ's MN-major A. dQ(i) is a per-tile partial: four
+// drain warps (one per TMEM lane quarter, thread = q row) read all of it into
+// registers and release the dP region for dP^T(i+1), then stage it 32
+// head-dim columns at a time (4 KB per warp, 128B-swizzled, double-buffered)
+// in shared memory, from where TMA reduces it into the fp32 dQ rows
+// (cp.reduce.async.bulk.tensor .add). Per-thread red.global.add from four
+// warps sustains only ~14 B/clk/SM of the ~24 the L2 reduction path takes
+// (tools/microbench/red_rate.cu) and set a 5.6k-clk tile period.
+// q tiles are walked in descending order with the group's heads innermost, so
+// the resident CTAs (consecutive key tiles of one kv head, longest first)
+// work on the same q tile together (ascending, and heads rotated per key
+// tile, measured the same at 32K and 128K). dQ accumulation order across key
+// tiles is not fixed: the result is not bitwise reproducible run to run (the
+// two-kernel path is). What bounds it (tools/trace_fused.py, round 2): the
+// 64 KB of fp32 reductions per tile (~24 B/clk/SM through L2, measured) and
+// the TMA unit they share with the Q / dO loads, whose 2-slot rings free a
+// slot only when the tile's last MMA (dK) completes.
+template <int HS>
+struct FusedCfg {
+  static_assert(HS == 128, "the fused backward is built for head size 128");
+  static constexpr int kTileBytes = 128 * HS * 2;
+  static constexpr int kSubBytes = 128 * 128;
+  static constexpr int kSub = HS / 64;
+  static constexpr int kCompute = 8, kDrain = 4;
+  // 16 warps: 0-7 compute, 8-11 dQ drain (lane quarter = warp & 3), 12 TMA,
+  // 13 MMA, 14-15 idle (complete the warpgroup for setmaxnreg). The drain
+  // holds a whole 128-column share of dQ^T in registers.
+  static constexpr int kThreads = 512;
+  static constexpr int kTmaWarp = 12, kMmaWarp = 13;
+  static constexpr int kComputeRegs = 168, kDrainRegs = 144, kProducerRegs = 32;
+  static_assert(2 * kComputeRegs + kDrainRegs + kProducerRegs <= 512, "register split (pool = 512 x 128)");
+  static constexpr int kVecBytes = 2 * 128 * 4;  // -lse2 | -delta of one q tile
+  static constexpr int kStageBytes = 32 * 32 * 4;  // fp32 dQ staging box: 32 rows x 32 columns, SW128
+  static constexpr int kOffK = 0, kOffV = kTileBytes, kOffQ = 2 * kTileBytes, kOffDO = 4 * kTileBytes;
+  static constexpr int kOffStage = 6 * kTileBytes, kOffVec = kOffStage + 4 * 2 * kStageBytes;  // [warp][2]
+  static constexpr int kOffBar = kOffVec + 2 * kVecBytes;
+  static constexpr int kSmemBytes = kOffBar + 256;
+  static_assert(kSmemBytes <= 232448, "fused smem");
+  static constexpr uint32_t kIdescSS = idesc_bf16_f32(128, 128, 0, 0);  // S^T / dP^T
+  static constexpr uint32_t kIdescTS = idesc_bf16_f32(128, HS, 0, 1);   // dV += P^T dO
+  static constexpr uint32_t kIdescDK = idesc_bf16_f32(128, HS, 0, 1);   // dK += dS^T Q
+  static constexpr uint32_t kIdescDQ = idesc_bf16_f32(128, HS, 1, 1);   // dQ = dS K
+};
+
+template <int HS>
+__global__ void __launch_bounds__(FusedCfg<HS>::kThreads, 1) fa_bwd_fused_kernel(const __grid_constant__ BwdParams p) {
+  using C = FusedCfg<HS>;
+  constexpr uint32_t kS = 0, kDP = 128, kDV = 256, kDK = 256 + HS;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((smem_u32(smem) & 1023u) != 0) __trap();  // the swizzled tiles need 1 KB alignment (no padding room)
+  uint8_t* sK = smem + C::kOffK;
+  uint8_t* sV = smem + C::kOffV;
+  uint8_t* sQ = smem + C::kOffQ;    // [2]
+  uint8_t* sDO = smem + C::kOffDO;  // [2]; dS^T of tile g over dO(g) once dV(g) completed
+  uint8_t* stage = smem + C::kOffStage;  // [drain warp][2] fp32 dQ boxes for the TMA reductions
+  uint8_t* vec = smem + C::kOffVec;  // [2][-lse2 128 | -delta 128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
+  uint64_t* kv_full = bars + 0;
+  uint64_t* kv_empty = bars + 1;
+  uint64_t* q_full = bars + 2;    // [2] Q tile + its vector landed
+  uint64_t* q_empty = bars + 4;   // [2] dK MMA of that tile done
+  uint64_t* do_full = bars + 6;   // [2]
+  uint64_t* do_empty = bars + 8;  // [2] dQ^T / dK MMAs (the last readers of the slot's dS^T) done
+  uint64_t* s_full = bars + 10;
+  uint64_t* p_ready = bars + 11;  // [2] P^T chunk pair in TMEM (256 arrivals)
+  uint64_t* dp_full = bars + 13;
+  uint64_t* ds_full = bars + 14;  // dS^T tile in shared memory (256 arrivals)
+  uint64_t* dv_done = bars + 15;  // dV MMAs of the tile done: its dO slot may take dS^T
+  uint64_t* dq_full = bars + 16;  // dQ in TMEM
+  uint64_t* dq_free = bars + 17;  // dQ read by the drain warps
+  uint64_t* acc_full = bars + 18;
+  uint64_t* u_full = bars + 19;
+  uint64_t* u_empty = bars + 20;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 21);
+  int* unit_slot = reinterpret_cast<int*>(tmem_slot + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(kv_full, 1);
+    mbar_init(kv_empty, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&q_full[s], 1);
+      mbar_init(&q_empty[s], 1);
+      mbar_init(&do_full[s], 1);
+      mbar_init(&do_empty[s], 1);
+      mbar_init(&p_ready[s], 256);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(dp_full, 1);
+    mbar_init(ds_full, 256);
+    mbar_init(dv_done, 1);
+    mbar_init(dq_full, 1);
+    mbar_init(dq_free, C::kDrain);
+    mbar_init(acc_full, 1);
+    mbar_init(u_full, 1);
+    mbar_init(u_empty, C::kCompute + C::kDrain + 1);  // compute + drain + MMA warps
+    fence_barrier_init();
+  }
+  if (warp == C::kMmaWarp) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (tmem != 0) __trap();
+  const int group = p.heads / p.kv_heads;
+
+  auto get_unit = [&](uint32_t it) {
+    mbar_wait(u_full, it & 1);
+    const int u = *reinterpret_cast<volatile int*>(unit_slot);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(u_empty);
+    return u;
+  };
+  // tile i of a unit with n q tiles: q tiles descending, heads innermost
+  auto tile_entry = [&](int beg, int n, int i) { return p.tile_list[beg + (n - 1 - i / group)]; };
+  auto tile_head = [&](int kvh, int i) { return kvh * group + i % group; };
+
+  if (warp >= C::kCompute + C::kDrain) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(C::kProducerRegs));
+  } else if (warp >= C::kCompute) {
+    static_assert(C::kDrainRegs >= 128, "drain warps grow from the launch's 128");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::kDrainRegs));
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::kComputeRegs));
+  }
+
+  if (warp < C::kCompute) {
+    // ---------------------------------------------------- compute warps (thread = key row)
+    const int q4 = warp & 3, hf = warp >> 2;
+    const int key_in_tile = q4 * 32 + lane;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
+    const float sl2 = p.scale_log2;
+    const uint32_t vec_s = smem_u32(vec);
+    // this thread's row of the dS^T tile: 64-column block hf, 128-byte row
+    // key_in_tile, 16-byte units XOR-swizzled by the row (SWIZZLE_128B)
+    const float isc = p.inv_scale;
+    const uint32_t ds_row0 = smem_u32(sDO) + hf * C::kSubBytes + key_in_tile * 128;
+    const uint32_t swz = static_cast<uint32_t>(key_in_tile & 7);
+    uint32_t g = 0, a_phase = 0;
+    for (uint32_t it = 0;; ++it) {
+      const int u = get_unit(it);
+      if (u >= p.num_units) break;
+      const uint32_t unit = p.units[u];
+      const int kt = unit & 0xFFFF, kvh = (unit >> 16) & 0xFF, b = unit >> 24;
+      const int beg = p.tile_off[kt], n = p.tile_off[kt + 1] - beg;
+      const int k_row = kt * 128 + key_in_tile;
+      const int kpos = p.k_pos[k_row];
+      const int total = group * n;
+      for (int i = 0; i < total; ++i, ++g) {
+        const int entry = tile_entry(beg, n, i);
+        const int qt = entry & 0x7FFFFFFF;
+        const uint32_t s = g & 1u;
+        mbar_wait(&q_full[s], (g >> 1) & 1);  // this q tile's -lse2 / -delta came with its Q tile
+        const uint32_t vb = vec_s + s * C::kVecBytes;
+        // phase 1: P^T = exp2(S^T * scale - lse2), packed over consumed S^T columns
+        const bool tr = q4 == 0 && lane == 0;
+        mbar_wait(s_full, g & 1);
+        if (tr && hf == 0) bwd_trace(p, 0, g);
+        tc_fence_after();
+        uint32_t pp2[2][16];
+        uint32_t sv2[64];
+        tmem_ld32(lane_base + kS + (2 * hf) * 32, sv2);
+        tmem_ld32(lane_base + kS + (2 * hf + 1) * 32, sv2 + 32);
+        tmem_ld_wait(sv2);
+        tmem_ld_wait(sv2 + 32);
+        auto p_chunks = [&](auto masked) {
+          constexpr bool kMasked = decltype(masked)::value;
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            const int c = 2 * hf + cc;
+            const uint32_t* sv = sv2 + 32 * cc;
+            uint32_t* pp = pp2[cc];
+#pragma unroll
+            for (int i4 = 0; i4 < 8; ++i4) {
+              const uint32_t col = (c * 32 + 4 * i4) * 4;
+              const float4 L4 = lds_f4(vb + col);
+              const float2 x01 = ffma2(make_float2(__uint_as_float(sv[4 * i4]), __uint_as_float(sv[4 * i4 + 1])),
+                                       make_float2(sl2, sl2), make_float2(L4.x, L4.y));
+              const float2 x23 = ffma2(make_float2(__uint_as_float(sv[4 * i4 + 2]), __uint_as_float(sv[4 * i4 + 3])),
+                                       make_float2(sl2, sl2), make_float2(L4.z, L4.w));
+              float pv[4] = {ex2(x01.x), ex2(x01.y), ex2(x23.x), ex2(x23.y)};
+              if constexpr (kMasked) {
+                const int4 qv = __ldg(reinterpret_cast<const int4*>(p.q_pos + qt * 128 + c * 32) + i4);
+                pv[0] = kpos > qv.x ? 0.f : pv[0];
+                pv[1] = kpos > qv.y ? 0.f : pv[1];
+                pv[2] = kpos > qv.z ? 0.f : pv[2];
+                pv[3] = kpos > qv.w ? 0.f : pv[3];
+              }
+              pp[2 * i4] = bwd_pack(pv[0], pv[1]);
+              pp[2 * i4 + 1] = bwd_pack(pv[2], pv[3]);
+            }
+            st16(lane_base + kS + packed_col(c), pp);
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&p_ready[cc]);
+          }
+        };
+        if (entry < 0)
+          p_chunks(std::true_type{});
+        else
+          p_chunks(std::false_type{});
+        if (tr) bwd_trace(p, 4 * hf + 1, g);
+        // phase 2: dS^T = P^T (dP^T - delta) -> the shared dS^T tile
+        mbar_wait(dp_full, g & 1);
+        if (tr) bwd_trace(p, 4 * hf + 2, g);
+        tc_fence_after();
+        uint32_t dp2[64];
+        tmem_ld32(lane_base + kDP + (2 * hf) * 32, dp2);
+        tmem_ld32(lane_base + kDP + (2 * hf + 1) * 32, dp2 + 32);
+        tmem_ld_wait(dp2);
+        tmem_ld_wait(dp2 + 32);
+        uint32_t pd2[2][16];
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          const int c = 2 * hf + cc;
+          const uint32_t* dp = dp2 + 32 * cc;
+          uint32_t* pd = pd2[cc];
+#pragma unroll
+          for (int i4 = 0; i4 < 8; ++i4) {
+            const float4 D4 = lds_f4(vb + 512 + (c * 32 + 4 * i4) * 4);  // -delta / sqrt(hs) of 4 q rows
+            const float ndv[4] = {D4.x, D4.y, D4.z, D4.w};
+#pragma unroll
+            for (int e = 0; e < 4; e += 2) {
+              const uint32_t w = pp2[cc][2 * i4 + e / 2];
+              const float2 pw = make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+              // (dP - delta) / sqrt(hs): ds carries the scale (attention.cpp's
+              // ds = p (dp - delta) / sqrt(hs)), so neither dQ nor dK is rescaled
+              const float2 d = ffma2(make_float2(__uint_as_float(dp[4 * i4 + e]), __uint_as_float(dp[4 * i4 + e + 1])),
+                                     make_float2(isc, isc), make_float2(ndv[e], ndv[e + 1]));
+              const float2 ds = fmul2(pw, d);
+              pd[2 * i4 + e / 2] = bwd_pack(ds.x, ds.y);
+            }
+          }
+        }
+        if (tr && hf == 0) bwd_trace(p, 12, g);
+        // dS^T(g) goes over dO(g): wait until the dV MMAs have read it
+        mbar_wait(dv_done, g & 1);
+        if (tr && hf == 0) bwd_trace(p, 4, g);
+        const uint32_t ds_row = ds_row0 + s * C::kTileBytes;
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t unit16 = static_cast<uint32_t>(cc * 4 + k) ^ swz;
+            sts_v4(ds_row + unit16 * 16, pd2[cc][4 * k], pd2[cc][4 * k + 1], pd2[cc][4 * k + 2], pd2[cc][4 * k + 3]);
+          }
+        fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core
+        tc_fence_before();
+        mbar_arrive(ds_full);
+        if (tr) bwd_trace(p, 4 * hf + 3, g);
+      }
+      // epilogue: warp half 0 stores dv (+)= dV, half 1 dk (+)= dK / sqrt(hs)
+      const bool any = n > 0;
+      if (any) {
+        mbar_wait(acc_full, a_phase & 1);
+        ++a_phase;
+        tc_fence_after();
+      }
+      const bool valid = k_row < p.k_len;
+      const size_t krow = (static_cast<size_t>(b) * p.k_len + (valid ? k_row : 0)) * p.kv_heads + kvh;
+      if (hf == 0)
+        store_rows<HS>(lane_base, kDV, any, valid, p.dv + krow * HS, 1.f, p.accumulate != 0);
+      else
+        store_rows<HS>(lane_base, kDK, any, valid, p.dk + krow * HS, 1.f, p.accumulate != 0);
+    }
+  } else if (warp < C::kCompute + C::kDrain) {
+    // ---------------------------------------------------- dQ drain (thread = q row)
+    const int q4 = warp & 3;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + kDP;
+    // this warp's two 4 KB staging boxes; this thread's 128-byte row in them
+    const uint32_t st_row = smem_u32(stage) + q4 * 2 * C::kStageBytes + lane * 128;
+    const uint32_t swz = static_cast<uint32_t>(lane & 7);
+    uint32_t g = 0, chunk = 0;
+    for (uint32_t it = 0;; ++it) {
+      const int u = get_unit(it);
+      if (u >= p.num_units) break;
+      const uint32_t unit = p.units[u];
+      const int kt = unit & 0xFFFF, kvh = (unit >> 16) & 0xFF, b = unit >> 24;
+      const int beg = p.tile_off[kt], n = p.tile_off[kt + 1] - beg;
+      const int total = group * n;
+      for (int i = 0; i < total; ++i, ++g) {
+        const int qt = tile_entry(beg, n, i) & 0x7FFFFFFF;
+        const int h = tile_head(kvh, i);
+        mbar_wait(dq_full, g & 1);
+        if (q4 == 0 && lane == 0) bwd_trace(p, 14, g);
+        tc_fence_after();
+        // this q row's whole dQ partial into registers, then release the dP
+        // region: staging and reduction run behind dP^T(i+1)
+        uint32_t r[128];
+        tmem_ld32(lane_base, r);
+        tmem_ld32(lane_base + 32, r + 32);
+        tmem_ld32(lane_base + 64, r + 64);
+        tmem_ld32(lane_base + 96, r + 96);
+        tmem_ld_wait(r);
+        tmem_ld_wait(r + 32);
+        tmem_ld_wait(r + 64);
+        tmem_ld_wait(r + 96);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(dq_free);  // the dP region may take dP^T(i+1)
+#pragma unroll
+        for (int cb = 0; cb < HS / 32; ++cb, ++chunk) {
+          const uint32_t buf = chunk & 1u;
+          // the box was last read by the reduction issued two chunks ago
+          if (lane == 0) bulk_wait_group_read<1>();
+          __syncwarp();
+          const uint32_t row = st_row + buf * C::kStageBytes;
+#pragma unroll
+          for (int k = 0; k < 8; ++k)  // 16-byte units XOR-swizzled by the row (SWIZZLE_128B)
+            sts_v4(row + ((static_cast<uint32_t>(k) ^ swz) << 4), r[32 * cb + 4 * k], r[32 * cb + 4 * k + 1],
+                   r[32 * cb + 4 * k + 2], r[32 * cb + 4 * k + 3]);
+          fence_proxy_async_smem();  // generic-proxy stores -> visible to the TMA unit
+          __syncwarp();
+          if (lane == 0) {
+            // dq[b][32 rows of this warp][h][32 cb ..] += the box (rows past
+            // q_len are dropped by the tensor map bounds)
+            if (!USPB_FUSED_NORED)
+              tma_reduce_add_4d(&p.tm_dq, stage + (q4 * 2 + buf) * C::kStageBytes, 32 * cb, h,
+                                qt * 128 + 32 * q4, b);
+            bulk_commit_group();
+          }
+        }
+        if (q4 == 0 && lane == 0) bwd_trace(p, 15, g);  // all chunks handed to TMA
+      }
+    }
+    if (lane == 0) bulk_wait_group<0>();  // every reduction has landed before the CTA exits
+  } else if (warp == C::kTmaWarp) {
+    // ---------------------------------------------------- producer
+    if (lane == 0) {
+      uint32_t g = 0, kv_it = 0;
+      for (uint32_t it = 0;; ++it) {
+        const int u = atomicAdd(&p.sched[0], 1);
+        mbar_wait(u_empty, (it & 1) ^ 1);
+        *reinterpret_cast<volatile int*>(unit_slot) = u;
+        mbar_arrive(u_full);
+        if (u >= p.num_units) break;
+        const uint32_t unit = p.units[u];
+        const int kt = unit & 0xFFFF, kvh = (unit >> 16) & 0xFF, b = unit >> 24;
+        const int beg = p.tile_off[kt], n = p.tile_off[kt + 1] - beg;
+        if (n == 0) continue;
+        mbar_wait(kv_empty, (kv_it & 1) ^ 1);
+        ++kv_it;
+        mbar_arrive_expect_tx(kv_full, 2 * C::kTileBytes);
+        for (int sb = 0; sb < C::kSub; ++sb) {
+          tma_load_4d(sK + sb * C::kSubBytes, &p.tm_k, kv_full, sb * 64, kvh, kt * 128, b);
+          tma_load_4d(sV + sb * C::kSubBytes, &p.tm_v, kv_full, sb * 64, kvh, kt * 128, b);
+        }
+        const int total = group * n;
+        for (int i = 0; i < total; ++i, ++g) {
+          const int qt = tile_entry(beg, n, i) & 0x7FFFFFFF;
+          const int h = tile_head(kvh, i);
+          const uint32_t s = g & 1u, ph = ((g >> 1) & 1) ^ 1;
+          mbar_wait(&q_empty[s], ph);
+          mbar_arrive_expect_tx(&q_full[s], C::kTileBytes + C::kVecBytes);
+          bulk_g2s(vec + s * C::kVecBytes, p.qvec + ((static_cast<size_t>(b) * p.heads + h) * p.n_q_tiles + qt) * 384,
+                   C::kVecBytes, &q_full[s]);
+          for (int sb = 0; sb < C::kSub; ++sb)
+            tma_load_4d(sQ + s * C::kTileBytes + sb * C::kSubBytes, &p.tm_q, &q_full[s], sb * 64, h, qt * 128, b);
+          mbar_wait(&do_empty[s], ph);
+          mbar_arrive_expect_tx(&do_full[s], C::kTileBytes);
+          for (int sb = 0; sb < C::kSub; ++sb)
+            tma_load_4d(sDO + s * C::kTileBytes + sb * C::kSubBytes, &p.tm_do, &do_full[s], sb * 64, h, qt * 128, b);
+        }
+      }
+      if (atomicAdd(&p.sched[1], 1) == static_cast<int>(gridDim.x) - 1) {
+        p.sched[0] = 0;
+        p.sched[1] = 0;
+        __threadfence();
+      }
+    }
+  } else if (warp == C::kMmaWarp) {
+    // ---------------------------------------------------- MMA issue
+    const uint64_t k_desc = smem_desc_sw128(smem_u32(sK), 16, 1024);
+    const uint64_t v_desc = smem_desc_sw128(smem_u32(sV), 16, 1024);
+    const uint64_t q_desc0 = smem_desc_sw128(smem_u32(sQ), 16, 1024);
+    const uint64_t do_desc0 = smem_desc_sw128(smem_u32(sDO), 16, 1024);
+    const uint64_t q_mn0 = smem_desc_sw128(smem_u32(sQ), C::kSubBytes, 1024);
+    const uint64_t do_mn0 = smem_desc_sw128(smem_u32(sDO), C::kSubBytes, 1024);
+    const uint64_t k_mn = smem_desc_sw128(smem_u32(sK), C::kSubBytes, 1024);
+    constexpr uint64_t kSlot = C::kTileBytes >> 4;  // descriptor units per ring slot
+    uint32_t g = 0, kv_phase = 0;
+    for (uint32_t it = 0;; ++it) {
+      const int u = get_unit(it);
+      if (u >= p.num_units) break;
+      const int kt = p.units[u] & 0xFFFF;
+      const int n = p.tile_off[kt + 1] - p.tile_off[kt];
+      if (n == 0) continue;
+      const int total = group * n;
+      mbar_wait(kv_full, kv_phase & 1);
+      ++kv_phase;
+      tc_fence_after();
+      // prologue: S^T, dP^T of the unit's first tile
+      {
+        const uint32_t s = g & 1u;
+        mbar_wait(&q_full[s], (g >> 1) & 1);
+        tc_fence_after();
+        if (elect_one()) mma_qk_hs128(kS, k_desc, q_desc0 + s * kSlot, C::kIdescSS, 0u);
+        __syncwarp();
+        bwd_commit(s_full);
+        if (g > 0) mbar_wait(dq_free, (g - 1) & 1);  // the previous tile's dQ^T left the dP region
+        mbar_wait(&do_full[s], (g >> 1) & 1);
+        tc_fence_after();
+        if (elect_one()) mma_qk_hs128(kDP, v_desc, do_desc0 + s * kSlot, C::kIdescSS, 0u);
+        __syncwarp();
+        bwd_commit(dp_full);
+      }
+      for (int i = 0; i < total; ++i, ++g) {
+        const uint32_t s = g & 1u, s1 = s ^ 1u, ph1 = ((g + 1) >> 1) & 1;
+        // dV += P^T dO(g), per chunk pair as P^T lands
+        const uint64_t dob = do_mn0 + s * kSlot;
+#pragma unroll
+        for (int n4 = 0; n4 < 4; ++n4) {
+          const int c = chunk_at(n4);
+          if ((n4 & 1) == 0) {
+            mbar_wait(&p_ready[n4 >> 1], g & 1);
+            if (n4 == 2 && lane == 0) bwd_trace(p, 8, g);
+            tc_fence_after();
+          }
+          if (elect_one())
+            mma_ts_k2(kDV, kS + packed_col(c), dob + static_cast<uint64_t>(c * 256), C::kIdescTS,
+                      (i > 0 || n4 > 0) ? 1u : 0u);
+          __syncwarp();
+        }
+        bwd_commit(dv_done);  // dO(g) consumed: the compute warps may write dS^T(g) over it
+        // S^T(g+1) over the S region (P^T(g) is read by the dV MMAs above)
+        if (i + 1 < total) {
+          mbar_wait(&q_full[s1], ph1);
+          tc_fence_after();
+          if (elect_one()) mma_qk_hs128(kS, k_desc, q_desc0 + s1 * kSlot, C::kIdescSS, 0u);
+          __syncwarp();
+          bwd_commit(s_full);
+          if (lane == 0) bwd_trace(p, 9, g);
+        }
+        // dQ^T(g) = K^T dS^T into the dP region, then dK += dS^T Q(g)
+        mbar_wait(ds_full, g & 1);
+        if (lane == 0) bwd_trace(p, 10, g);
+        tc_fence_after();
+        if (elect_one()) mma_mn_mn_chain(kDP, do_mn0 + s * kSlot, k_mn, C::kIdescDQ, 0u);  // A = dS, B = K
+        __syncwarp();
+        bwd_commit(dq_full);
+        if (elect_one())
+          mma_kmaj_mn_chain(kDK, do_desc0 + s * kSlot, q_mn0 + s * kSlot, C::kIdescDK, i > 0 ? 1u : 0u);
+        __syncwarp();
+        bwd_commit(&q_empty[s]);
+        bwd_commit(&do_empty[s]);  // the slot's dS^T has been read
+        if (lane == 0) bwd_trace(p, 11, g);
+        // dP^T(g+1) once the drain warps have read dQ^T(g)
+        if (i + 1 < total) {
+          mbar_wait(dq_free, g & 1);
+          mbar_wait(&do_full[s1], ph1);
+          tc_fence_after();
+          if (elect_one()) mma_qk_hs128(kDP, v_desc, do_desc0 + s1 * kSlot, C::kIdescSS, 0u);
+          __syncwarp();
+          bwd_commit(dp_full);
+          if (lane == 0) bwd_trace(p, 13, g);
+        }
+      }
+      bwd_commit(acc_full);
+      bwd_commit(kv_empty);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == C::kMmaWarp) tmem_dealloc(tmem, 512);
+}
+
 // ============================================================ small kernels
 __global__ void delta_kernel(const uint16_t* o, const uint16_t* dout, float* delta, int64_t batch, int64_t q_len,
-                             int heads, int hs, int64_t n_qt, const float* lse, const int32_t* q_pos, float* qvec) {
+                             int heads, int hs, int64_t n_qt, const float* lse, const int32_t* q_pos, float* qvec,
+                             float delta_scale) {
   // one warp per row (b, t, h) over the padded rows t < n_qt * 128: 16-byte
   // loads, fp32 dot, shuffle reduction
   const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
@@ -979,7 +1462,7 @@ __global__ void delta_kernel(const uint16_t* o, const uint16_t* dout, float* del
       float* v = qvec + ((b * heads + h) * n_qt + t / 128) * 384 + (t % 128);
       // negated, for the dK/dV kernel's packed FFMA2 / FADD2
       v[0] = valid ? -(lse[r] * 1.4426950408889634f) : -INFINITY;  // padding rows: p = 0
-      v[128] = valid ? -acc : -0.f;
+      v[128] = valid ? -acc * delta_scale : -0.f;
       v[256] = __int_as_float(q_pos[t]);
     }
   }
@@ -1067,16 +1550,49 @@ cudaError_t launch_bwd_dkdv(const BwdParams& p, int hs, int grid, cudaStream_t s
   return cudaErrorInvalidValue;
 }
 
+cudaError_t launch_bwd_fused(const BwdParams& p, int hs, int grid, cudaStream_t stream) {
+  if (hs != 128) return cudaErrorInvalidValue;
+  using C = FusedCfg<128>;
+  auto kern = fa_bwd_fused_kernel<128>;
+  static std::atomic<uint64_t> done{0};
+  const cudaError_t once = ensure_smem_attr(kern, C::kSmemBytes, done);
+  if (once != cudaSuccess) return once;
+  kern<<<grid, C::kThreads, C::kSmemBytes, stream>>>(p);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_bwd_delta(const void* o, const void* dout, float* delta, int64_t batch, int64_t q_len,
                              int heads, int hs, const float* lse, const int32_t* q_pos, float* qvec,
-                             cudaStream_t stream) {
+                             float qvec_delta_scale, cudaStream_t stream) {
   const int64_t n_qt = (q_len + 127) / 128;
   const int64_t rows = batch * n_qt * 128 * heads;
   if (rows == 0) return cudaSuccess;
   const int64_t threads = rows * 32;
   const int grid = static_cast<int>((threads + 255) / 256);
   delta_kernel<<<grid, 256, 0, stream>>>(static_cast<const uint16_t*>(o), static_cast<const uint16_t*>(dout), delta,
-                                         batch, q_len, heads, hs, n_qt, lse, q_pos, qvec);
+                                         batch, q_len, heads, hs, n_qt, lse, q_pos, qvec, qvec_delta_scale);
+  return cudaGetLastError();
+}
+
+__global__ void add_f32_kernel(const float4* a, float4* acc, int64_t n4) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4; i += int64_t(gridDim.x) * blockDim.x) {
+    const float4 x = a[i];
+    float4 y = acc[i];
+    y.x = x.x + y.x;
+    y.y = x.y + y.y;
+    y.z = x.z + y.z;
+    y.w = x.w + y.w;
+    acc[i] = y;
+  }
+}
+
+cudaError_t launch_add_f32(const float* blk, float* acc, int64_t n, cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  if (n % 4 != 0) return cudaErrorInvalidValue;
+  const int64_t n4 = n / 4;
+  const int64_t blocks = (n4 + 255) / 256;
+  add_f32_kernel<<<static_cast<int>(blocks < 148 * 8 ? blocks : 148 * 8), 256, 0, stream>>>(
+      reinterpret_cast<const float4*>(blk), reinterpret_cast<float4*>(acc), n4);
   return cudaGetLastError();
 }
 

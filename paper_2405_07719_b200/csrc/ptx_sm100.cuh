@@ -93,6 +93,9 @@ __device__ __forceinline__ float4 lds_f4(uint32_t addr) {
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
   return v;
 }
+__device__ __forceinline__ void sts_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
 __device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
@@ -150,6 +153,26 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const void* tmap, uint64_
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2),
       "r"(c3)
       : "memory");
+}
+// TMA reduction shared -> global: the box at {c0..c3} of the fp32 tensor
+// behind `tmap` += the dense box in shared memory (bulk_group completion).
+__device__ __forceinline__ void tma_reduce_add_4d(const void* tmap, const void* src, int c0, int c1, int c2,
+                                                  int c3) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.4d.global.shared::cta.add.tile.bulk_group"
+      " [%0, {%2, %3, %4, %5}], [%1];" ::"l"(reinterpret_cast<uint64_t>(tmap)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// Waits until at most N committed bulk groups still READ their shared source.
+template <int N>
+__device__ __forceinline__ void bulk_wait_group_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_group() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
 // Plain bulk copy global -> shared (16-byte multiple), completion on `bar`.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -399,6 +422,64 @@ __device__ __forceinline__ void mma_ts_k2(uint32_t d_tmem, uint32_t a_tmem, uint
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], rb, %3, p1;\n\t"
       "}"
       ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// D[128 x N] (+)= A[128 x 128] B[128 x N], both from shared memory, 8
+// k-steps of 16: A K-major (32 B per step inside a 128-byte swizzle row,
+// 16 KB to the next 64-column block), B MN-major (16 rows = 2 KB per step).
+// The fused backward's dK += dS^T Q (A = dS^T as the compute warps stored it).
+__device__ __forceinline__ void mma_kmaj_mn_chain(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                                  uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p0, p1;\n\t.reg .b64 ra, rb;\n\t"
+      "setp.ne.b32 p0, %4, 0;\n\t"
+      "setp.eq.u32 p1, 1, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p0;\n\t"
+      "add.s64 ra, %1, 2;\n\tadd.s64 rb, %2, 128;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 4;\n\tadd.s64 rb, %2, 256;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 6;\n\tadd.s64 rb, %2, 384;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 1024;\n\tadd.s64 rb, %2, 512;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 1026;\n\tadd.s64 rb, %2, 640;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 1028;\n\tadd.s64 rb, %2, 768;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 1030;\n\tadd.s64 rb, %2, 896;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "}"
+      ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// D[128 x N] (+)= A[128 x 128] B[128 x N] with BOTH operands MN-major in
+// shared memory (16 rows = 2 KB per k-step each): the fused backward's
+// dQ^T = K^T dS^T (A = the K tile, B = dS^T, both stored key-row-major).
+__device__ __forceinline__ void mma_mn_mn_chain(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                                uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p0, p1;\n\t.reg .b64 ra, rb;\n\t"
+      "setp.ne.b32 p0, %4, 0;\n\t"
+      "setp.eq.u32 p1, 1, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p0;\n\t"
+      "add.s64 ra, %1, 128;\n\tadd.s64 rb, %2, 128;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 256;\n\tadd.s64 rb, %2, 256;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 384;\n\tadd.s64 rb, %2, 384;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 512;\n\tadd.s64 rb, %2, 512;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 640;\n\tadd.s64 rb, %2, 640;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 768;\n\tadd.s64 rb, %2, 768;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "add.s64 ra, %1, 896;\n\tadd.s64 rb, %2, 896;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ra, rb, %3, p1;\n\t"
+      "}"
+      ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
 

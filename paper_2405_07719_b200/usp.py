@@ -390,6 +390,12 @@ class UspAttention:
         check(lib().usp_engine_get_info(self._h, ctypes.byref(i)))
         return {f: getattr(i, f) for f, _ in i._fields_}
 
+    def set_deterministic(self, on: bool = True) -> None:
+        """Backward algorithm: fused one-kernel (default at head size 128; dQ
+        reduced with fp32 atomics, last bits may vary run to run) or the
+        bitwise-reproducible two-kernel path (``on=True``)."""
+        check(lib().usp_engine_set_deterministic(self._h, 1 if on else 0))
+
     def set_reserved_sms(self, n: int) -> None:
         check(lib().usp_engine_set_reserved_sms(self._h, int(n)))
 

@@ -105,14 +105,18 @@ def run_usp_gpu(c: UspCase, q, k, v, device, setup=None):
     return out, [l_ for l_ in lses], engines, comm
 
 
-def run_usp_gpu_fwd_bwd(c: UspCase, q, k, v, dout, device):
+def run_usp_gpu_fwd_bwd(c: UspCase, q, k, v, dout, device, deterministic: bool = False):
     """Forward then backward on every rank of a local world. Returns
-    (out, dq, dk, dv) global in original token order, and the engines."""
+    (out, dq, dk, dv) global in original token order, and the engines.
+    ``deterministic`` selects the two-kernel backward (default: the fused
+    kernel wherever the head size allows it)."""
     import torch
 
     from paper_2405_07719_b200 import local_world_backward
 
     out, lses, engines, comm = run_usp_gpu(c, q, k, v, device)
+    for e in engines:
+        e.set_deterministic(deterministic)
     pos = [torch.tensor(e.positions(), dtype=torch.long, device=device) for e in engines]
     fwds = []
     from paper_2405_07719_b200 import UspForward

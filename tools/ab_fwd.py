@@ -73,6 +73,8 @@ def main():
     shapes = [(131072, 128, 32, 8, 1), (32768, 128, 32, 8, 1), (32768, 64, 8, 8, 1), (32768, 128, 32, 8, 0)]
     if os.environ.get("AB_SHAPES") == "long":
         shapes = shapes[:1]
+    elif os.environ.get("AB_SHAPES") == "bwd":
+        shapes = shapes[:2]
     for rnd in range(int(os.environ.get("AB_ROUNDS", "2"))):
         for sh in shapes:
             for var in variants:

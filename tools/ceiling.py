@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""Practical ceiling for the forward kernel: library attention kernels on the
+"""Practical ceiling for the forward (and, with --bwd, the backward) kernels: library attention kernels on the
 same box at the bench shape (verdict r1 item 6).
 
 Causal attention, hc 32 / kv 8 (GQA) / hs 128, bf16, bs 1, at L = 128K (and
@@ -47,7 +47,7 @@ def bench(fn, reps=5, warm=2):
     return sorted(ts)[len(ts) // 2]
 
 
-def run(backend, L):
+def run(backend, L, bwd=False):
     import torch
 
     dev = torch.device("cuda", 0)
@@ -70,10 +70,22 @@ def run(backend, L):
             kt = kt.repeat_interleave(hc // kv, dim=1)
             vt = vt.repeat_interleave(hc // kv, dim=1)
 
-        def fn():
+        if bwd:
+            qt, kt, vt = (x.contiguous().requires_grad_(True) for x in (qt, kt, vt))
             with sdpa_kernel(SDPBackend.CUDNN_ATTENTION):
-                torch.nn.functional.scaled_dot_product_attention(qt, kt, vt, is_causal=True, enable_gqa=gqa)
+                out = torch.nn.functional.scaled_dot_product_attention(qt, kt, vt, is_causal=True, enable_gqa=gqa)
+            do = torch.rand_like(out) * 2 - 1
+
+            def fn():
+                with sdpa_kernel(SDPBackend.CUDNN_ATTENTION):
+                    torch.autograd.grad(out, (qt, kt, vt), do, retain_graph=True)
+        else:
+            def fn():
+                with sdpa_kernel(SDPBackend.CUDNN_ATTENTION):
+                    torch.nn.functional.scaled_dot_product_attention(qt, kt, vt, is_causal=True, enable_gqa=gqa)
     elif backend == "trtllm":
+        if bwd:
+            raise SystemExit("trtllm: forward only")
         from flashinfer.prefill import trtllm_batch_context_with_kv_cache
 
         page = 64
@@ -93,32 +105,51 @@ def run(backend, L):
         from flash_attn import flash_attn_func
 
         qb, kb, vb = q.unsqueeze(0), k.unsqueeze(0), v.unsqueeze(0)
+        if bwd:
+            qb, kb, vb = (x.contiguous().requires_grad_(True) for x in (qb, kb, vb))
+            out = flash_attn_func(qb, kb, vb, causal=True)
+            do = torch.rand_like(out) * 2 - 1
 
-        def fn():
-            flash_attn_func(qb, kb, vb, causal=True)
+            def fn():
+                torch.autograd.grad(out, (qb, kb, vb), do, retain_graph=True)
+        else:
+            def fn():
+                flash_attn_func(qb, kb, vb, causal=True)
     elif backend == "ours":
         from paper_2405_07719_b200 import ProcessMesh, UspAttention
 
         eng = UspAttention(ProcessMesh(1, 1), rank=0, seq_len=L, heads=hc, kv_heads=kv, head_size=hs, causal=True)
         qo, ko, vo = q.unsqueeze(0), k.unsqueeze(0), v.unsqueeze(0)
         o, lse = eng.alloc_outputs()
+        if bwd:
+            fwd = eng.forward(qo, ko, vo)
+            do = u(L, hc, hs).unsqueeze(0)
+            dq, dk, dv = eng.alloc_grads()
 
-        def fn():
-            eng.forward(qo, ko, vo, o, lse)
+            def fn():
+                eng.backward(fwd, do, dq, dk, dv)
+        else:
+            def fn():
+                eng.forward(qo, ko, vo, o, lse)
     else:
         raise SystemExit(f"unknown backend {backend}")
     ms = bench(fn)
-    return {"backend": backend, "L": L, "ms": ms, "tflops": flops(L) / ms / 1e9, "note": note}
+    # backward: algorithmic FLOPs = 2.5x the forward's (five GEMMs per visible pair)
+    f = flops(L) * (2.5 if bwd else 1.0)
+    return {"backend": backend, "pass": "bwd" if bwd else "fwd", "L": L, "ms": ms, "tflops": f / ms / 1e9,
+            "note": note}
 
 
 def main():
-    if len(sys.argv) > 2 and sys.argv[1] == "--one":
-        print("RESULT " + json.dumps(run(sys.argv[2], int(sys.argv[3]))), flush=True)
+    bwd = "--bwd" in sys.argv
+    args = [a for a in sys.argv[1:] if a != "--bwd"]
+    if len(args) > 1 and args[0] == "--one":
+        print("RESULT " + json.dumps(run(args[1], int(args[2]), bwd)), flush=True)
         return
     for L in (131072, 32768):
-        for b in ("ours", "cudnn", "trtllm", "fa2"):
+        for b in ("ours", "cudnn", "fa2") if bwd else ("ours", "cudnn", "trtllm", "fa2"):
             try:
-                r = subprocess.run([sys.executable, os.path.abspath(__file__), "--one", b, str(L)],
+                r = subprocess.run([sys.executable, os.path.abspath(__file__), "--one", b, str(L)] + (["--bwd"] if bwd else []),
                                    capture_output=True, text=True, timeout=600)
                 line = [x for x in r.stdout.splitlines() if x.startswith("RESULT ")]
                 if line:
