@@ -223,6 +223,16 @@ typedef struct usp_engine_info {
   double kv_shift_bytes, ring_step_ms_est, required_gbs;
 } usp_engine_info;
 USP_API usp_status usp_engine_get_info(const usp_engine* engine, usp_engine_info* out);
+/* Ulysses all-to-all pipelining: every member's T rows are
+ * exchanged in `chunks` row chunks; ring step 0 computes chunk c as soon as it
+ * has landed (the exchange of chunk c+1 overlaps it) and the last step's
+ * chunk c sends its O rows while chunk c+1 computes. Default 2 when U > 1,
+ * bs = 1, T divides into whole query tiles and the transport is not the
+ * peer-memory one (whose exchange is already fused into the kernels);
+ * 1 = one exchange each way. USP_INVALID_INPUT when the rows do not divide.
+ * Results are bitwise identical for every chunk count. */
+USP_API usp_status usp_engine_set_a2a_chunks(usp_engine* engine, int32_t chunks);
+USP_API int32_t usp_engine_a2a_chunks(const usp_engine* engine);
 /* Backward algorithm. Default (off): at head size 128 one fused kernel per
  * ring step computes dK, dV and dQ (five GEMMs per tile pair; dQ partials are
  * reduced into fp32 with atomics, so dQ's summation order — and its last

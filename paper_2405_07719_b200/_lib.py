@@ -90,7 +90,7 @@ EXPORTS = [
     "usp_comm_create_nccl", "usp_comm_create_local", "usp_comm_destroy", "usp_engine_create",
     "usp_attn_fwd", "usp_engine_last_launches", "usp_engine_destroy", "usp_engine_enable_timing",
     "usp_engine_kernel_times", "usp_engine_debug_counters", "usp_engine_rescale_count",
-    "usp_engine_stage_times", "usp_engine_get_info", "usp_engine_set_reserved_sms", "usp_engine_set_deterministic", "usp_comm_set_timeout", "usp_comm_status", "usp_comm_debug_rendezvous", "usp_local_world_fwd", "usp_attn_bwd", "usp_local_world_bwd",
+    "usp_engine_stage_times", "usp_engine_get_info", "usp_engine_set_reserved_sms", "usp_engine_set_deterministic", "usp_engine_set_a2a_chunks", "usp_engine_a2a_chunks", "usp_comm_set_timeout", "usp_comm_status", "usp_comm_debug_rendezvous", "usp_local_world_fwd", "usp_attn_bwd", "usp_local_world_bwd",
     "usp_backward_ledger", "usp_attn_fwd_host", "usp_comm_create_p2p",
     "usp_last_error", "usp_version",
 ]
@@ -146,6 +146,8 @@ def _declare(lib):
         "usp_engine_get_info": (st, [vp, P(UspEngineInfo)]),
         "usp_engine_set_reserved_sms": (st, [vp, ctypes.c_int32]),
         "usp_engine_set_deterministic": (st, [vp, ctypes.c_int32]),
+        "usp_engine_set_a2a_chunks": (st, [vp, ctypes.c_int32]),
+        "usp_engine_a2a_chunks": (ctypes.c_int32, [vp]),
         "usp_engine_rescale_count": (st, [vp, i64p]),
         "usp_local_world_fwd": (st, [P(vp), ctypes.c_int32, P(vp), P(vp), P(vp), P(vp), P(vp), P(vp)]),
         "usp_last_error": (ctypes.c_char_p, []),

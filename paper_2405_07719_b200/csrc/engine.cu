@@ -268,8 +268,78 @@ class Engine {
       ring_ctas_ = std::min(16, std::max(1, static_cast<int>(std::ceil(2.0 * required_gbs_ / kCtaGBs))));
       reserved_sms_ = (tr_ && tr_->comm_uses_sms()) ? ring_ctas_ : 0;
     }
+    // Ulysses exchanges pipelined in row chunks: default two
+    // chunks wherever the exchange goes through a transport collective (not
+    // the peer-memory direct exchange) at bs = 1. On NCCL the chunk exchanges
+    // that overlap the attention run on a second Ulysses communicator capped
+    // at a2a_ctas CTAs, and the attention grid leaves that many SMs: sized
+    // like the ring (2x the bandwidth an overlapped chunk of Q / O needs to
+    // land within one chunk of attention, at a conservative 20 GB/s per CTA),
+    // from the shape alone so every rank computes the same values.
+    const int rows_unit = tiling_.rows_per_unit;
+    const bool chunkable = U_ > 1 && B_ == 1 && tr_ && !tr_->peer_memory() && T_ % (2 * rows_unit) == 0;
+    if (chunkable) {
+      constexpr double kFwdTflops = 1300.0, kCtaGBs = 20.0;
+      const double L = double(shape_.seq_len);
+      const double pairs = shape_.causal ? L * (L + 1) / 2 : L * L;
+      const double f_rank = 4.0 * double(B_) * double(H_) * hs_ * pairs / double(U_ * R_);
+      const int C = 2;
+      const double t_chunk = f_rank / R_ / C / (kFwdTflops * 1e12);
+      const double bytes = double(U_ - 1) * double(q_part_) / C;
+      const double gbs = t_chunk > 0 ? bytes / t_chunk / 1e9 : 0.0;
+      if (tr_->comm_uses_sms()) {
+        a2a_ctas_ = std::min(16, std::max(1, static_cast<int>(std::ceil(2.0 * gbs / kCtaGBs))));
+        reserved_sms_ = std::max(reserved_sms_, a2a_ctas_);
+      }
+      configure_chunks(C);
+    }
     if (tr_) groups_ = tr_->make_groups(c.rank, shape_.mesh.ulysses_group(c.rank),
-                                        shape_.mesh.ring_group(c.rank), ring_ctas_);
+                                        shape_.mesh.ring_group(c.rank), ring_ctas_, a2a_ctas_);
+  }
+
+  // Row-chunk plans of the ring steps whose attention overlaps a Ulysses
+  // exchange: step 0 (a2a in) and step R-1 (a2a out). Chunk c of every
+  // member's T rows = rows [c T/C, (c+1) T/C): unit u belongs to chunk
+  // ((first row of u) mod T) / (T / C).
+  void configure_chunks(int C) {
+    if (C < 1 || (C > 1 && (U_ < 2 || B_ != 1 || T_ % (int64_t(C) * tiling_.rows_per_unit) != 0)))
+      throw_invalid("a2a chunks must divide every member's rows into whole query tiles (U > 1, bs = 1)");
+    a2a_steps_.clear();
+    a2a_chunks_ = C;
+    if (C == 1) return;
+    if (!comm_stream_) USPB_CHECK(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking));
+    while (static_cast<int>(ev_in_.size()) < C) {
+      cudaEvent_t a, b;
+      USPB_CHECK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+      USPB_CHECK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+      ev_in_.push_back(a);
+      ev_attn_.push_back(b);
+    }
+    if (!ev_chunk_misc_[0])
+      for (auto& e : ev_chunk_misc_) USPB_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    const int64_t rows = T_ / C, per = tiling_.rows_per_unit;
+    for (int si : {0, R_ - 1}) {
+      if (si == R_ - 1 && si == 0 && !a2a_steps_.empty()) break;  // R = 1: one split step
+      std::vector<DevStep> cs(C);
+      const StepPlan& h = steps_[si].host;
+      for (int c = 0; c < C; ++c) {
+        cs[c].host = h;
+        cs[c].host.units.clear();
+        cs[c].mode = steps_[si].mode;
+      }
+      for (uint32_t u : h.units) {
+        const int64_t row0 = int64_t(u & 0xFFFF) * per;
+        cs[static_cast<size_t>((row0 % T_) / rows)].host.units.push_back(u);
+      }
+      for (auto& d : cs) {
+        d.q_pos = upload(d.host.q_pos);
+        d.k_pos = upload(d.host.k_pos);
+        d.tile_off = upload(d.host.tile_off);
+        d.tile_list = upload(d.host.tile_list);
+        d.units = upload(d.host.units);
+      }
+      a2a_steps_.push_back(std::move(cs));
+    }
   }
 
  public:
@@ -283,13 +353,20 @@ class Engine {
   // SMs the attention grid leaves free for a concurrent communication kernel
   // (default: the sizing above).
   void set_deterministic(bool on) { deterministic_ = on; }  // plans follow at the next backward
+  void set_a2a_chunks(int n) { configure_chunks(n); }
+  int a2a_chunks() const { return a2a_chunks_; }
   void set_reserved_sms(int n) {
     if (n < 0 || n >= num_sms_) throw_invalid("reserved SMs must be in [0, #SMs)");
     reserved_sms_ = n;
   }
 
  private:
-  int ring_ctas_ = 1, reserved_sms_ = 0;
+  int ring_ctas_ = 1, reserved_sms_ = 0, a2a_ctas_ = 0, a2a_chunks_ = 1;
+  // a2a_steps_[0]: step 0 split in row chunks (a2a in overlap);
+  // a2a_steps_[1] (R > 1): step R-1 (a2a out overlap)
+  std::vector<std::vector<DevStep>> a2a_steps_;
+  std::vector<cudaEvent_t> ev_in_, ev_attn_;
+  cudaEvent_t ev_chunk_misc_[2] = {nullptr, nullptr};  // packed, last a2a out done
   double kv_shift_bytes_ = 0, step_ms_est_ = 0, required_gbs_ = 0;
 
  public:
@@ -307,6 +384,10 @@ class Engine {
     for (auto e : stage_pool_) cudaEventDestroy(e);
     for (auto e : ev_pre_) cudaEventDestroy(e);
     for (auto e : ev_recv_) cudaEventDestroy(e);
+    for (auto e : ev_in_) cudaEventDestroy(e);
+    for (auto e : ev_attn_) cudaEventDestroy(e);
+    for (auto e : ev_chunk_misc_)
+      if (e) cudaEventDestroy(e);
     for (auto e : ev_acc_) cudaEventDestroy(e);
     if (comm_stream_) cudaStreamDestroy(comm_stream_);
     for (auto e : ev_chunk_in_) cudaEventDestroy(e);
@@ -357,6 +438,7 @@ class Engine {
     // head-sharded buffers (no staging, no copy), and the last attention
     // step stores O rows straight into the owners' receive buffers.
     const bool direct = direct_ok && U_ > 1 && B_ == 1 && U_ <= 16 && tr_ && tr_->peer_memory();
+    const bool chunked = !direct && a2a_chunks_ > 1;
     if (direct) {
       // -- 1. Ulysses in, fused with the pack: part m of my Q/K/V rows ->
       //    member m's rows [u*T, (u+1)*T) of its head-sharded Q / K / V
@@ -376,6 +458,48 @@ class Engine {
       batch_flush(st);
       tr_->ulysses_done(*groups_, st);  // every member's parts for me have landed
       stage(st, "pack_a2a_in");
+      record_a2a(0, q_part_);
+      record_a2a(1, kv_part_);
+      record_a2a(2, kv_part_);
+      qh = q_h_.p;
+      kh = kv0;
+      vh = kv0 + kv_bytes_;
+    } else if (chunked) {
+      // -- 1. Ulysses in, pipelined: pack once, then C
+      //    exchanges on comm_stream_, chunk c = rows [c T/C, (c+1) T/C) of
+      //    every member's part (K / V whole in chunk 0: every q row needs
+      //    every key); ring step 0 runs chunk c as soon as it has landed, so
+      //    the exchange of chunk c+1 overlaps the attention of chunk c.
+      //    Received in place (bs = 1), no unpack.
+      uint8_t* sq = send_.as<uint8_t>();
+      uint8_t* sk = sq + U_ * q_part_;
+      uint8_t* sv = sk + U_ * kv_part_;
+      batch_begin();
+      pack_heads(q, sq, H_, hl_, st);
+      pack_heads(k, sk, KV_, kvl_, st);
+      pack_heads(v, sv, KV_, kvl_, st);
+      batch_flush(st);
+      stage(st, "pack");
+      USPB_CHECK(cudaEventRecord(ev_chunk_misc_[0], st));
+      USPB_CHECK(cudaStreamWaitEvent(comm_stream_, ev_chunk_misc_[0], 0));
+      const size_t qs = q_part_ / a2a_chunks_;
+      for (int c = 0; c < a2a_chunks_; ++c) {
+        std::vector<std::vector<A2APart>> parts(c == 0 ? 3 : 1, std::vector<A2APart>(U_));
+        for (int p = 0; p < U_; ++p) {
+          parts[0][p] = {sq + p * q_part_ + c * qs, q_h_.as<uint8_t>() + p * q_part_ + c * qs};
+          if (c == 0) {
+            parts[1][p] = {sk + p * kv_part_, kv0 + p * kv_part_};
+            parts[2][p] = {sv + p * kv_part_, kv0 + kv_bytes_ + p * kv_part_};
+          }
+        }
+        cudaEvent_t s0 = side_event(comm_stream_);
+        if (c == 0)
+          tr_->all_to_all(*groups_, parts, {qs, kv_part_, kv_part_}, comm_stream_);
+        else
+          tr_->all_to_all(*groups_, parts, {qs}, comm_stream_, /*overlapped=*/true);
+        side_span("a2a_in." + std::to_string(c), s0, side_event(comm_stream_));
+        USPB_CHECK(cudaEventRecord(ev_in_[c], comm_stream_));
+      }
       record_a2a(0, q_part_);
       record_a2a(1, kv_part_);
       record_a2a(2, kv_part_);
@@ -474,12 +598,44 @@ class Engine {
       }
       const bool last = t == R_ - 1;
       if (direct_o && last) tr_->ulysses_ready(*groups_, st);  // every member's o_recv_ is free
+      if (chunked && (t == 0 || last)) {
+        // row chunks: wait for chunk c's Q (step 0); after the last step's
+        // chunk c, its O rows go out while chunk c+1 computes
+        const std::vector<DevStep>& cs = a2a_steps_[t == 0 ? 0 : 1];
+        const size_t qs = q_part_ / a2a_chunks_;
+        for (int c = 0; c < a2a_chunks_; ++c) {
+          if (t == 0) {
+            USPB_CHECK(cudaStreamWaitEvent(st, ev_in_[c], 0));
+            stage(st, "wait_in." + std::to_string(c));  // exposed part of chunk c's exchange
+          }
+          launch_plan(cs[c], tm_q, kbuf(t), vbuf(t), o_heads, lse, Tr_, Tr_, st);
+          stage(st, "attn" + std::to_string(t) + "." + std::to_string(c));
+          if (!last) continue;
+          USPB_CHECK(cudaEventRecord(ev_attn_[c], st));
+          USPB_CHECK(cudaStreamWaitEvent(comm_stream_, ev_attn_[c], 0));
+          std::vector<std::vector<A2APart>> parts(1, std::vector<A2APart>(U_));
+          uint8_t* osend = static_cast<uint8_t*>(o_heads);
+          for (int p = 0; p < U_; ++p)
+            parts[0][p] = {osend + p * q_part_ + c * qs, o_recv_.as<uint8_t>() + p * q_part_ + c * qs};
+          cudaEvent_t s0 = side_event(comm_stream_);
+          tr_->all_to_all(*groups_, parts, {qs}, comm_stream_, /*overlapped=*/c + 1 < a2a_chunks_);
+          side_span("a2a_out." + std::to_string(c), s0, side_event(comm_stream_));
+        }
+        continue;
+      }
       launch_step(t, tm_q, kbuf(t), vbuf(t), o_heads, lse, st, direct_o && last ? o_peer : nullptr);
       stage(st, "attn" + std::to_string(t));
     }
 
     // -- 3. Ulysses out: [peer][b][T][H/U] -> (b, T, H, hs)
-    if (direct_o) {
+    if (chunked) {
+      USPB_CHECK(cudaEventRecord(ev_chunk_misc_[1], comm_stream_));
+      USPB_CHECK(cudaStreamWaitEvent(st, ev_chunk_misc_[1], 0));
+      stage(st, "a2a_out");  // exposed part: the last chunk's exchange
+      record_a2a(3, q_part_);
+      unpack_heads(o_recv_.p, o, st);
+      stage(st, "unpack");
+    } else if (direct_o) {
       tr_->ulysses_done(*groups_, st);  // every member's rows for me have landed
       stage(st, "a2a_out");
       record_a2a(3, q_part_);
@@ -1906,6 +2062,13 @@ usp_status usp_engine_get_info(const usp_engine* engine, usp_engine_info* out) {
     out->required_gbs = i.required_gbs;
   });
 }
+
+usp_status usp_engine_set_a2a_chunks(usp_engine* engine, int32_t chunks) {
+  if (!engine) return USP_INVALID_INPUT;
+  return guarded([&] { engine->impl->set_a2a_chunks(chunks); });
+}
+
+int32_t usp_engine_a2a_chunks(const usp_engine* engine) { return engine ? engine->impl->a2a_chunks() : -1; }
 
 usp_status usp_engine_set_deterministic(usp_engine* engine, int32_t on) {
   if (!engine) return USP_INVALID_INPUT;

@@ -82,7 +82,7 @@ class LocalTransport final : public Transport {
     rendezvous(members, rank, sig);
   }
 
-  std::shared_ptr<Groups> make_groups(int rank, const std::vector<int>& ug, const std::vector<int>& rg,
+  std::shared_ptr<Groups> make_groups(int rank, const std::vector<int>& ug, const std::vector<int>& rg, int,
                                       int) override {
     auto g = std::make_shared<Groups>();
     g->rank = rank;
@@ -97,7 +97,7 @@ class LocalTransport final : public Transport {
   }
 
   void all_to_all(const Groups& g, const std::vector<std::vector<A2APart>>& parts,
-                  const std::vector<size_t>& bytes, cudaStream_t stream) override {
+                  const std::vector<size_t>& bytes, cudaStream_t stream, bool) override {
     std::ostringstream sig;
     sig << "all_to_all<bf16>(tensors=" << parts.size() << ",part_bytes=";
     for (size_t t = 0; t < bytes.size(); ++t) sig << (t ? "/" : "") << bytes[t];
@@ -324,9 +324,9 @@ class NcclTransport final : public Transport {
   // are collective over the world and every rank creates its engines in the
   // same order, so every rank hits (or misses) this cache together.
   std::shared_ptr<Groups> make_groups(int rank, const std::vector<int>& ug, const std::vector<int>& rg,
-                                      int ring_ctas) override {
+                                      int ring_ctas, int a2a_ctas) override {
     check_healthy();
-    const auto key = std::make_tuple(ug, rg, ring_ctas);
+    const auto key = std::make_tuple(ug, rg, ring_ctas, a2a_ctas);
     auto hit = groups_.find(key);
     if (hit != groups_.end()) return hit->second;
     auto g = std::make_shared<Groups>();
@@ -351,15 +351,27 @@ class NcclTransport final : public Transport {
     owned_.push_back(rc);
     g->ulysses_comm = uc;
     g->ring_comm = rc;
+    if (a2a_ctas > 0 && ug.size() > 1) {
+      // the Ulysses chunk exchanges that overlap the attention kernel
+      ncclConfig_t ocfg = NCCL_CONFIG_INITIALIZER;
+      ocfg.blocking = 0;
+      ocfg.maxCTAs = a2a_ctas;
+      ocfg.minCTAs = 1;
+      ncclComm_t oc = nullptr;
+      split(/*color=*/r, /*key=*/u, &oc, &ocfg, "ncclCommSplit(ulysses overlap group [" + group_key(ug) + "])");
+      owned_.push_back(oc);
+      g->ulysses_overlap_comm = oc;
+    }
     groups_.emplace(key, g);
     return g;
   }
 
   void all_to_all(const Groups& g, const std::vector<std::vector<A2APart>>& parts,
-                  const std::vector<size_t>& bytes, cudaStream_t stream) override {
+                  const std::vector<size_t>& bytes, cudaStream_t stream, bool overlapped) override {
     check_healthy();
     const NcclApi& api = nccl();
-    auto comm = static_cast<ncclComm_t>(g.ulysses_comm);
+    auto comm = static_cast<ncclComm_t>(overlapped && g.ulysses_overlap_comm ? g.ulysses_overlap_comm
+                                                                              : g.ulysses_comm);
     const int me = index_of(g.ulysses, g.rank);
     // Self part: a device copy (NCCL would also copy it).
     for (size_t t = 0; t < parts.size(); ++t)
@@ -528,7 +540,7 @@ class NcclTransport final : public Transport {
   int n_, rank_, device_;
   ncclComm_t world_ = nullptr;
   std::vector<ncclComm_t> owned_;
-  std::map<std::tuple<std::vector<int>, std::vector<int>, int>, std::shared_ptr<Groups>> groups_;
+  std::map<std::tuple<std::vector<int>, std::vector<int>, int, int>, std::shared_ptr<Groups>> groups_;
   int64_t a2a_seq_ = 0, shift_seq_ = 0;
   std::mutex mu_;
   std::condition_variable cv_;

@@ -32,21 +32,30 @@ struct Groups {
   std::vector<int> ulysses, ring;
   void* ulysses_comm = nullptr;  // transport-private (ncclComm_t for NCCL)
   void* ring_comm = nullptr;
+  // NCCL: a second Ulysses communicator capped at a2a_ctas CTAs, for the
+  // chunk exchanges that run while the attention kernel holds the other SMs
+  void* ulysses_overlap_comm = nullptr;
 };
 
 class Transport {
  public:
   virtual ~Transport() = default;
   virtual int world_size() const = 0;
-  // Collective over the world: builds this rank's sub-groups. ring_ctas:
-  // how many CTAs (SMs) the ring exchange may use while the attention
-  // kernel runs (NCCL maxCTAs of the ring communicator; Engine sizes it).
+  // Collective over the world: builds this rank's sub-groups. ring_ctas /
+  // a2a_ctas: how many CTAs (SMs) the ring exchange / an overlapped Ulysses
+  // chunk exchange may use while the attention kernel runs (NCCL maxCTAs of
+  // the ring communicator and of the capped Ulysses communicator; 0 = no
+  // overlapped Ulysses exchanges). Engine sizes both from the shape alone,
+  // so every rank passes the same values.
   virtual std::shared_ptr<Groups> make_groups(int rank, const std::vector<int>& ulysses_group,
-                                              const std::vector<int>& ring_group, int ring_ctas) = 0;
+                                              const std::vector<int>& ring_group, int ring_ctas,
+                                              int a2a_ctas = 0) = 0;
   // Several tensors exchanged in one collective over the Ulysses group:
   // parts[t][p] for tensor t and member index p, bytes[t] per part.
+  // overlapped: the exchange runs concurrently with the attention kernel
+  // (NCCL uses the capped communicator).
   virtual void all_to_all(const Groups& g, const std::vector<std::vector<A2APart>>& parts,
-                          const std::vector<size_t>& bytes, cudaStream_t stream) = 0;
+                          const std::vector<size_t>& bytes, cudaStream_t stream, bool overlapped = false) = 0;
   // Ring shift of several buffers at once (K and V) over the ring group.
   virtual void ring_shift(const Groups& g, const std::vector<const void*>& send,
                           const std::vector<void*>& recv, const std::vector<size_t>& bytes,

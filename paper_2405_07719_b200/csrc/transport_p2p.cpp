@@ -126,7 +126,7 @@ class P2PTransport final : public Transport {
   int world_size() const override { return n_; }
   bool comm_uses_sms() const override { return false; }  // copy engines + stream memops only
 
-  std::shared_ptr<Groups> make_groups(int rank, const std::vector<int>& ug, const std::vector<int>& rg,
+  std::shared_ptr<Groups> make_groups(int rank, const std::vector<int>& ug, const std::vector<int>& rg, int,
                                       int) override {
     if (rank != rank_) throw_invalid("p2p transport: engine rank differs from the transport's rank");
     auto g = std::make_shared<Groups>();
@@ -151,7 +151,7 @@ class P2PTransport final : public Transport {
   }
 
   void all_to_all(const Groups& g, const std::vector<std::vector<A2APart>>& parts,
-                  const std::vector<size_t>& bytes, cudaStream_t stream) override {
+                  const std::vector<size_t>& bytes, cudaStream_t stream, bool) override {
     const int me = index_in(g.ulysses, g.rank);
     const uint64_t e = ++epoch_[0];
     // destinations in every peer: where MY part lands in peer p's buffer is

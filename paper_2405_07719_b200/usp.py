@@ -390,6 +390,15 @@ class UspAttention:
         check(lib().usp_engine_get_info(self._h, ctypes.byref(i)))
         return {f: getattr(i, f) for f, _ in i._fields_}
 
+    def set_a2a_chunks(self, chunks: int) -> None:
+        """Row chunks of the pipelined Ulysses all-to-alls (1 = one exchange
+        each way; default 2 where it applies, see usp_engine_set_a2a_chunks)."""
+        check(lib().usp_engine_set_a2a_chunks(self._h, int(chunks)))
+
+    @property
+    def a2a_chunks(self) -> int:
+        return int(lib().usp_engine_a2a_chunks(self._h))
+
     def set_deterministic(self, on: bool = True) -> None:
         """Backward algorithm: fused one-kernel (default at head size 128; dQ
         reduced with fp32 atomics, last bits may vary run to run) or the
