@@ -44,6 +44,12 @@
 #ifndef USPB_DKDV_SWAP
 #define USPB_DKDV_SWAP 1  // Q / dO slot roles alternate per ring round (qd_slot)
 #endif
+#ifndef USPB_FUSED_RDEPTH
+#define USPB_FUSED_RDEPTH 1
+#endif
+#ifndef USPB_FUSED_DYN
+#define USPB_FUSED_DYN 1  // the fused kernel's MMA warp issues S^T(g+1) / dQ(g)+dK(g) in readiness order
+#endif
 #ifndef USPB_FUSED_NORED
 #define USPB_FUSED_NORED 0  // development A/B: the fused kernel's drain skips the dQ reductions
 #endif
@@ -1267,7 +1273,9 @@ __global__ void __launch_bounds__(FusedCfg<HS>::kThreads, 1) fa_bwd_fused_kernel
         for (int cb = 0; cb < HS / 32; ++cb, ++chunk) {
           const uint32_t buf = chunk & 1u;
           // the box was last read by the reduction issued two chunks ago
-          if (lane == 0) bulk_wait_group_read<1>();
+          // (USPB_FUSED_RDEPTH = reductions a warp keeps queued on the TMA
+          // unit, which the Q / dO loads queue behind)
+          if (lane == 0) bulk_wait_group_read<USPB_FUSED_RDEPTH>();
           __syncwarp();
           const uint32_t row = st_row + buf * C::kStageBytes;
 #pragma unroll
@@ -1387,28 +1395,53 @@ __global__ void __launch_bounds__(FusedCfg<HS>::kThreads, 1) fa_bwd_fused_kernel
           __syncwarp();
         }
         bwd_commit(dv_done);  // dO(g) consumed: the compute warps may write dS^T(g) over it
-        // S^T(g+1) over the S region (P^T(g) is read by the dV MMAs above)
-        if (i + 1 < total) {
-          mbar_wait(&q_full[s1], ph1);
+        // S^T(g+1) over the S region (P^T(g) is read by the dV MMAs above),
+        // and dQ(g) into the dP region then dK(g) once dS^T(g) is in shared
+        // memory: whichever is ready first is issued first. Q(g+1) is
+        // loaded only once dK(g-1) completed (two Q slots), so waiting for it
+        // before dQ(g) / dK(g) would also delay dK(g) and with it Q(g+2).
+        auto issue_s_next = [&] {
           tc_fence_after();
           if (elect_one()) mma_qk_hs128(kS, k_desc, q_desc0 + s1 * kSlot, C::kIdescSS, 0u);
           __syncwarp();
           bwd_commit(s_full);
           if (lane == 0) bwd_trace(p, 9, g);
+        };
+        auto issue_dq_dk = [&] {
+          if (lane == 0) bwd_trace(p, 10, g);
+          tc_fence_after();
+          if (elect_one()) mma_mn_mn_chain(kDP, do_mn0 + s * kSlot, k_mn, C::kIdescDQ, 0u);  // A = dS, B = K
+          __syncwarp();
+          bwd_commit(dq_full);
+          if (elect_one())
+            mma_kmaj_mn_chain(kDK, do_desc0 + s * kSlot, q_mn0 + s * kSlot, C::kIdescDK, i > 0 ? 1u : 0u);
+          __syncwarp();
+          bwd_commit(&q_empty[s]);
+          bwd_commit(&do_empty[s]);  // the slot's dS^T has been read
+          if (lane == 0) bwd_trace(p, 11, g);
+        };
+        if (!USPB_FUSED_DYN || i + 1 >= total) {
+          if (i + 1 < total) {
+            mbar_wait(&q_full[s1], ph1);
+            issue_s_next();
+          }
+          mbar_wait(ds_full, g & 1);
+          issue_dq_dk();
+        } else {
+          bool s_done = false, d_done = false;
+          uint32_t spins = 0;
+          while (!(s_done && d_done)) {
+            if (!s_done && mbar_test(&q_full[s1], ph1)) {
+              issue_s_next();
+              s_done = true;
+            } else if (!d_done && mbar_test(ds_full, g & 1)) {
+              issue_dq_dk();
+              d_done = true;
+            } else if (++spins == (1u << 28)) {
+              __trap();  // a pipeline deadlock fails the launch instead of hanging
+            }
+          }
         }
-        // dQ^T(g) = K^T dS^T into the dP region, then dK += dS^T Q(g)
-        mbar_wait(ds_full, g & 1);
-        if (lane == 0) bwd_trace(p, 10, g);
-        tc_fence_after();
-        if (elect_one()) mma_mn_mn_chain(kDP, do_mn0 + s * kSlot, k_mn, C::kIdescDQ, 0u);  // A = dS, B = K
-        __syncwarp();
-        bwd_commit(dq_full);
-        if (elect_one())
-          mma_kmaj_mn_chain(kDK, do_desc0 + s * kSlot, q_mn0 + s * kSlot, C::kIdescDK, i > 0 ? 1u : 0u);
-        __syncwarp();
-        bwd_commit(&q_empty[s]);
-        bwd_commit(&do_empty[s]);  // the slot's dS^T has been read
-        if (lane == 0) bwd_trace(p, 11, g);
         // dP^T(g+1) once the drain warps have read dQ^T(g)
         if (i + 1 < total) {
           mbar_wait(dq_free, g & 1);
