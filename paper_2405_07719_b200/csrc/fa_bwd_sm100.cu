@@ -1125,6 +1125,13 @@ __global__ void __launch_bounds__(FusedCfg<HS>::kThreads, 1) fa_bwd_fused_kernel
         const uint32_t vb = vec_s + s * C::kVecBytes;
         // phase 1: P^T = exp2(S^T * scale - lse2), packed over consumed S^T columns
         const bool tr = q4 == 0 && lane == 0;
+        // the first chunk's -lse2 values (32 q columns, broadcast reads)
+        // issued before the S^T wait so their latency hides behind it: the
+        // compute warps stalled on these loads (ncu short-scoreboard);
+        // +5.5 % (981 -> 1035 TFLOP/s at 128K, A/B). All 64 columns spill.
+        float4 lv[8];
+#pragma unroll
+        for (int x = 0; x < 8; ++x) lv[x] = lds_f4(vb + (hf * 64 + 4 * x) * 4);
         mbar_wait(s_full, g & 1);
         if (tr && hf == 0) bwd_trace(p, 0, g);
         tc_fence_after();
@@ -1143,8 +1150,7 @@ __global__ void __launch_bounds__(FusedCfg<HS>::kThreads, 1) fa_bwd_fused_kernel
             uint32_t* pp = pp2[cc];
 #pragma unroll
             for (int i4 = 0; i4 < 8; ++i4) {
-              const uint32_t col = (c * 32 + 4 * i4) * 4;
-              const float4 L4 = lds_f4(vb + col);
+              const float4 L4 = cc == 0 ? lv[i4] : lds_f4(vb + (c * 32 + 4 * i4) * 4);
               const float2 x01 = ffma2(make_float2(__uint_as_float(sv[4 * i4]), __uint_as_float(sv[4 * i4 + 1])),
                                        make_float2(sl2, sl2), make_float2(L4.x, L4.y));
               const float2 x23 = ffma2(make_float2(__uint_as_float(sv[4 * i4 + 2]), __uint_as_float(sv[4 * i4 + 3])),
@@ -1172,6 +1178,9 @@ __global__ void __launch_bounds__(FusedCfg<HS>::kThreads, 1) fa_bwd_fused_kernel
           p_chunks(std::false_type{});
         if (tr) bwd_trace(p, 4 * hf + 1, g);
         // phase 2: dS^T = P^T (dP^T - delta) -> the shared dS^T tile
+        float4 dv4[8];  // -delta / sqrt(hs) of the first chunk's 32 q columns, before the dP^T wait
+#pragma unroll
+        for (int x = 0; x < 8; ++x) dv4[x] = lds_f4(vb + 512 + (hf * 64 + 4 * x) * 4);
         mbar_wait(dp_full, g & 1);
         if (tr) bwd_trace(p, 4 * hf + 2, g);
         tc_fence_after();
@@ -1188,7 +1197,7 @@ __global__ void __launch_bounds__(FusedCfg<HS>::kThreads, 1) fa_bwd_fused_kernel
           uint32_t* pd = pd2[cc];
 #pragma unroll
           for (int i4 = 0; i4 < 8; ++i4) {
-            const float4 D4 = lds_f4(vb + 512 + (c * 32 + 4 * i4) * 4);  // -delta / sqrt(hs) of 4 q rows
+            const float4 D4 = cc == 0 ? dv4[i4] : lds_f4(vb + 512 + (c * 32 + 4 * i4) * 4);  // -delta / sqrt(hs)
             const float ndv[4] = {D4.x, D4.y, D4.z, D4.w};
 #pragma unroll
             for (int e = 0; e < 4; e += 2) {
