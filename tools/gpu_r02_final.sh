@@ -20,3 +20,6 @@ tail -1 gpurun_out/${TAG}_ncu_fa.log
 timeout 900 python tools/time_bwd.py > gpurun_out/${TAG}_bwd.txt 2>&1
 BWD_DET=1 timeout 900 python tools/time_bwd.py 131072 >> gpurun_out/${TAG}_bwd.txt 2>&1
 tail -4 gpurun_out/${TAG}_bwd.txt
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fused -s 1 -c 1 \
+   -o gpurun_out/${TAG}_bwd_fused python tools/profile_bwd.py 32768 2 > gpurun_out/${TAG}_ncu_bwd.log 2>&1
+tail -1 gpurun_out/${TAG}_ncu_bwd.log
