@@ -1143,6 +1143,7 @@ __global__ void __launch_bounds__(FusedCfg<HS>::kThreads, 1) fa_bwd_fused_kernel
         tmem_ld_wait(sv2 + 32);
         auto p_chunks = [&](auto masked) {
           constexpr bool kMasked = decltype(masked)::value;
+          float4 lv1[8];
 #pragma unroll
           for (int cc = 0; cc < 2; ++cc) {
             const int c = 2 * hf + cc;
@@ -1150,7 +1151,7 @@ __global__ void __launch_bounds__(FusedCfg<HS>::kThreads, 1) fa_bwd_fused_kernel
             uint32_t* pp = pp2[cc];
 #pragma unroll
             for (int i4 = 0; i4 < 8; ++i4) {
-              const float4 L4 = cc == 0 ? lv[i4] : lds_f4(vb + (c * 32 + 4 * i4) * 4);
+              const float4 L4 = cc == 0 ? lv[i4] : lv1[i4];
               const float2 x01 = ffma2(make_float2(__uint_as_float(sv[4 * i4]), __uint_as_float(sv[4 * i4 + 1])),
                                        make_float2(sl2, sl2), make_float2(L4.x, L4.y));
               const float2 x23 = ffma2(make_float2(__uint_as_float(sv[4 * i4 + 2]), __uint_as_float(sv[4 * i4 + 3])),
@@ -1165,6 +1166,10 @@ __global__ void __launch_bounds__(FusedCfg<HS>::kThreads, 1) fa_bwd_fused_kernel
               }
               pp[2 * i4] = bwd_pack(pv[0], pv[1]);
               pp[2 * i4 + 1] = bwd_pack(pv[2], pv[3]);
+            }
+            if (cc == 0) {  // the second chunk's -lse2 while the first chunk's P^T is stored
+#pragma unroll
+              for (int x = 0; x < 8; ++x) lv1[x] = lds_f4(vb + (hf * 64 + 32 + 4 * x) * 4);
             }
             st16(lane_base + kS + packed_col(c), pp);
             tmem_st_wait();
@@ -1190,6 +1195,7 @@ __global__ void __launch_bounds__(FusedCfg<HS>::kThreads, 1) fa_bwd_fused_kernel
         tmem_ld_wait(dp2);
         tmem_ld_wait(dp2 + 32);
         uint32_t pd2[2][16];
+        float4 dv1[8];
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
           const int c = 2 * hf + cc;
@@ -1197,7 +1203,7 @@ __global__ void __launch_bounds__(FusedCfg<HS>::kThreads, 1) fa_bwd_fused_kernel
           uint32_t* pd = pd2[cc];
 #pragma unroll
           for (int i4 = 0; i4 < 8; ++i4) {
-            const float4 D4 = cc == 0 ? dv4[i4] : lds_f4(vb + 512 + (c * 32 + 4 * i4) * 4);  // -delta / sqrt(hs)
+            const float4 D4 = cc == 0 ? dv4[i4] : dv1[i4];  // -delta / sqrt(hs)
             const float ndv[4] = {D4.x, D4.y, D4.z, D4.w};
 #pragma unroll
             for (int e = 0; e < 4; e += 2) {
@@ -1210,6 +1216,10 @@ __global__ void __launch_bounds__(FusedCfg<HS>::kThreads, 1) fa_bwd_fused_kernel
               const float2 ds = fmul2(pw, d);
               pd[2 * i4 + e / 2] = bwd_pack(ds.x, ds.y);
             }
+          }
+          if (cc == 0) {
+#pragma unroll
+            for (int x = 0; x < 8; ++x) dv1[x] = lds_f4(vb + 512 + (hf * 64 + 32 + 4 * x) * 4);
           }
         }
         if (tr && hf == 0) bwd_trace(p, 12, g);
