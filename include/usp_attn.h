@@ -233,14 +233,12 @@ USP_API usp_status usp_engine_get_info(const usp_engine* engine, usp_engine_info
  * Results are bitwise identical for every chunk count. */
 USP_API usp_status usp_engine_set_a2a_chunks(usp_engine* engine, int32_t chunks);
 USP_API int32_t usp_engine_a2a_chunks(const usp_engine* engine);
-/* Backward algorithm. Default (off): at head sizes 65..128 (run at the
- * kernel head size 128) one fused kernel per ring step computes dK, dV and
- * dQ (five GEMMs per tile pair; dQ partials are reduced into fp32 by TMA in
- * arrival order, so dQ's summation order — and its last bits — may differ
- * run to run). On: two kernels per step (dK/dV, then dQ, which recomputes S
- * and dP) with every sum in a fixed order — bitwise reproducible backward.
- * Head sizes <= 64 always use the two-kernel path. Takes effect at the next
- * usp_attn_bwd. */
+/* Backward algorithm. Default (off): one fused kernel per ring step computes
+ * dK, dV and dQ (five GEMMs per tile pair; dQ partials are reduced into fp32
+ * by TMA in arrival order, so dQ's summation order — and its last bits — may
+ * differ run to run). On: two kernels per step (dK/dV, then dQ, which
+ * recomputes S and dP) with every sum in a fixed order — bitwise
+ * reproducible backward. Takes effect at the next usp_attn_bwd. */
 USP_API usp_status usp_engine_set_deterministic(usp_engine* engine, int32_t on);
 /* Overrides the SMs the attention grid leaves free for a concurrent
  * communication kernel (0 .. #SMs-1). */

@@ -1318,11 +1318,11 @@ class Engine {
     DevStep dq, dkdv;  // two-kernel (deterministic) backward
     DevStep fused;     // one-kernel backward: dK/dV units over single key tiles
   };
-  // The fused backward (one kernel per ring step, dQ reduced with fp32
-  // atomics) is the default at head size 128; usp_engine_set_deterministic
+  // The fused backward (one kernel per ring step, dQ reduced in fp32 by
+  // TMA) is the default; usp_engine_set_deterministic
   // selects the two-kernel path, whose dQ is accumulated in a fixed order and
   // is bitwise reproducible.
-  bool use_fused_bwd() const { return hsk_ == 128 && !deterministic_; }
+  bool use_fused_bwd() const { return !deterministic_; }  // kernel head sizes 64 and 128
   static void upload_plan(DevStep& d, StepPlan&& h) {
     d.host = std::move(h);
     d.q_pos = upload(d.host.q_pos);

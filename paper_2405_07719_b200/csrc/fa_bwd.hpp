@@ -52,7 +52,7 @@ struct BwdParams {
 
 cudaError_t launch_bwd_dq(const BwdParams& p, int hs, int grid, cudaStream_t stream);
 cudaError_t launch_bwd_dkdv(const BwdParams& p, int hs, int grid, cudaStream_t stream);
-// Both in one kernel (head size 128): units / CSR as for the dK/dV kernel
+// Both in one kernel (kernel head size 64 or 128): units / CSR as for the dK/dV kernel
 // (transpose_plan, single key tiles); dK / dV written like the dK/dV kernel,
 // dQ (scaled) REDUCED into p.dq with fp32 atomics (caller zeroes it first).
 cudaError_t launch_bwd_fused(const BwdParams& p, int hs, int grid, cudaStream_t stream);

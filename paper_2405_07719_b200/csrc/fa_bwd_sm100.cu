@@ -988,14 +988,18 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
 // slot only when the tile's last MMA (dK) completes.
 template <int HS>
 struct FusedCfg {
-  static_assert(HS == 128, "the fused backward is built for head size 128");
+  static_assert(HS == 128 || HS == 64, "the fused backward runs at kernel head size 64 or 128");
   static constexpr int kTileBytes = 128 * HS * 2;
+  // dS^T (128 keys x 128 q, bf16 = 32 KB) fits over the tile's dO slot only
+  // at head size 128; at 64 it gets its own buffer (released after dQ / dK)
+  static constexpr bool kDsInDo = HS == 128;
+  static constexpr int kDsBytes = 128 * 128 * 2;
   static constexpr int kSubBytes = 128 * 128;
   static constexpr int kSub = HS / 64;
   static constexpr int kCompute = 8, kDrain = 4;
   // 16 warps: 0-7 compute, 8-11 dQ drain (lane quarter = warp & 3), 12 TMA,
   // 13 MMA, 14-15 idle (complete the warpgroup for setmaxnreg). The drain
-  // holds a whole 128-column share of dQ^T in registers.
+  // holds its q row's whole HS-column dQ partial in registers.
   static constexpr int kThreads = 512;
   static constexpr int kTmaWarp = 12, kMmaWarp = 13;
   static constexpr int kComputeRegs = 168, kDrainRegs = 144, kProducerRegs = 32;
@@ -1003,7 +1007,9 @@ struct FusedCfg {
   static constexpr int kVecBytes = 2 * 128 * 4;  // -lse2 | -delta of one q tile
   static constexpr int kStageBytes = 32 * 32 * 4;  // fp32 dQ staging box: 32 rows x 32 columns, SW128
   static constexpr int kOffK = 0, kOffV = kTileBytes, kOffQ = 2 * kTileBytes, kOffDO = 4 * kTileBytes;
-  static constexpr int kOffStage = 6 * kTileBytes, kOffVec = kOffStage + 4 * 2 * kStageBytes;  // [warp][2]
+  static constexpr int kOffDS = 6 * kTileBytes;  // (HS = 64 only)
+  static constexpr int kOffStage = kOffDS + (kDsInDo ? 0 : kDsBytes);
+  static constexpr int kOffVec = kOffStage + 4 * 2 * kStageBytes;  // [warp][2]
   static constexpr int kOffBar = kOffVec + 2 * kVecBytes;
   static constexpr int kSmemBytes = kOffBar + 256;
   static_assert(kSmemBytes <= 232448, "fused smem");
@@ -1022,7 +1028,11 @@ __global__ void __launch_bounds__(FusedCfg<HS>::kThreads, 1) fa_bwd_fused_kernel
   uint8_t* sK = smem + C::kOffK;
   uint8_t* sV = smem + C::kOffV;
   uint8_t* sQ = smem + C::kOffQ;    // [2]
-  uint8_t* sDO = smem + C::kOffDO;  // [2]; dS^T of tile g over dO(g) once dV(g) completed
+  uint8_t* sDO = smem + C::kOffDO;  // [2]; HS 128: dS^T of tile g over dO(g) once dV(g) completed
+  // the dS^T tile of the current q tile: dO's slot (HS 128) or its own buffer
+  auto ds_base = [&](uint32_t slot) -> uint8_t* {
+    return C::kDsInDo ? sDO + slot * C::kTileBytes : smem + C::kOffDS;
+  };
   uint8_t* stage = smem + C::kOffStage;  // [drain warp][2] fp32 dQ boxes for the TMA reductions
   uint8_t* vec = smem + C::kOffVec;  // [2][-lse2 128 | -delta 128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
@@ -1036,7 +1046,7 @@ __global__ void __launch_bounds__(FusedCfg<HS>::kThreads, 1) fa_bwd_fused_kernel
   uint64_t* p_ready = bars + 11;  // [2] P^T chunk pair in TMEM (256 arrivals)
   uint64_t* dp_full = bars + 13;
   uint64_t* ds_full = bars + 14;  // dS^T tile in shared memory (256 arrivals)
-  uint64_t* dv_done = bars + 15;  // dV MMAs of the tile done: its dO slot may take dS^T
+  uint64_t* dv_done = bars + 15;  // HS 128: dV MMAs done, the dO slot may take dS^T; HS 64: the dS^T buffer is free
   uint64_t* dq_full = bars + 16;  // dQ in TMEM
   uint64_t* dq_free = bars + 17;  // dQ read by the drain warps
   uint64_t* acc_full = bars + 18;
@@ -1105,7 +1115,7 @@ __global__ void __launch_bounds__(FusedCfg<HS>::kThreads, 1) fa_bwd_fused_kernel
     // this thread's row of the dS^T tile: 64-column block hf, 128-byte row
     // key_in_tile, 16-byte units XOR-swizzled by the row (SWIZZLE_128B)
     const float isc = p.inv_scale;
-    const uint32_t ds_row0 = smem_u32(sDO) + hf * C::kSubBytes + key_in_tile * 128;
+    const uint32_t ds_row0 = smem_u32(ds_base(0)) + hf * C::kSubBytes + key_in_tile * 128;
     const uint32_t swz = static_cast<uint32_t>(key_in_tile & 7);
     uint32_t g = 0, a_phase = 0;
     for (uint32_t it = 0;; ++it) {
@@ -1223,10 +1233,14 @@ __global__ void __launch_bounds__(FusedCfg<HS>::kThreads, 1) fa_bwd_fused_kernel
           }
         }
         if (tr && hf == 0) bwd_trace(p, 12, g);
-        // dS^T(g) goes over dO(g): wait until the dV MMAs have read it
-        mbar_wait(dv_done, g & 1);
+        // HS 128: dS^T(g) goes over dO(g), once the dV MMAs have read it;
+        // HS 64: into the dS^T buffer, once the previous tile's dQ / dK read it
+        if (C::kDsInDo)
+          mbar_wait(dv_done, g & 1);
+        else if (g > 0)
+          mbar_wait(dv_done, (g - 1) & 1);
         if (tr && hf == 0) bwd_trace(p, 4, g);
-        const uint32_t ds_row = ds_row0 + s * C::kTileBytes;
+        const uint32_t ds_row = ds_row0 + (C::kDsInDo ? s * C::kTileBytes : 0u);
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
@@ -1276,15 +1290,11 @@ __global__ void __launch_bounds__(FusedCfg<HS>::kThreads, 1) fa_bwd_fused_kernel
         tc_fence_after();
         // this q row's whole dQ partial into registers, then release the dP
         // region: staging and reduction run behind dP^T(i+1)
-        uint32_t r[128];
-        tmem_ld32(lane_base, r);
-        tmem_ld32(lane_base + 32, r + 32);
-        tmem_ld32(lane_base + 64, r + 64);
-        tmem_ld32(lane_base + 96, r + 96);
-        tmem_ld_wait(r);
-        tmem_ld_wait(r + 32);
-        tmem_ld_wait(r + 64);
-        tmem_ld_wait(r + 96);
+        uint32_t r[HS];
+#pragma unroll
+        for (int c = 0; c < HS / 32; ++c) tmem_ld32(lane_base + 32 * c, r + 32 * c);
+#pragma unroll
+        for (int c = 0; c < HS / 32; ++c) tmem_ld_wait(r + 32 * c);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(dq_free);  // the dP region may take dP^T(i+1)
@@ -1370,6 +1380,19 @@ __global__ void __launch_bounds__(FusedCfg<HS>::kThreads, 1) fa_bwd_fused_kernel
     const uint64_t do_mn0 = smem_desc_sw128(smem_u32(sDO), C::kSubBytes, 1024);
     const uint64_t k_mn = smem_desc_sw128(smem_u32(sK), C::kSubBytes, 1024);
     constexpr uint64_t kSlot = C::kTileBytes >> 4;  // descriptor units per ring slot
+    // the dS^T tile as dQ's MN-major A and dK's K-major A (HS 64: its own buffer)
+    const uint64_t ds_mn0 = C::kDsInDo ? do_mn0 : smem_desc_sw128(smem_u32(smem + C::kOffDS), C::kSubBytes, 1024);
+    const uint64_t ds_k0 = C::kDsInDo ? do_desc0 : smem_desc_sw128(smem_u32(smem + C::kOffDS), 16, 1024);
+    constexpr uint64_t kDsSlot = C::kDsInDo ? kSlot : 0;
+    auto qk = [&](uint32_t d, uint64_t ad, uint64_t bd) {  // D = A B^T over the head dimension
+      if (elect_one()) {
+        if constexpr (HS == 128)
+          mma_qk_hs128(d, ad, bd, C::kIdescSS, 0u);
+        else
+          mma_qk_hs64(d, ad, bd, C::kIdescSS, 0u);
+      }
+      __syncwarp();
+    };
     uint32_t g = 0, kv_phase = 0;
     for (uint32_t it = 0;; ++it) {
       const int u = get_unit(it);
@@ -1386,14 +1409,12 @@ __global__ void __launch_bounds__(FusedCfg<HS>::kThreads, 1) fa_bwd_fused_kernel
         const uint32_t s = g & 1u;
         mbar_wait(&q_full[s], (g >> 1) & 1);
         tc_fence_after();
-        if (elect_one()) mma_qk_hs128(kS, k_desc, q_desc0 + s * kSlot, C::kIdescSS, 0u);
-        __syncwarp();
+        qk(kS, k_desc, q_desc0 + s * kSlot);
         bwd_commit(s_full);
         if (g > 0) mbar_wait(dq_free, (g - 1) & 1);  // the previous tile's dQ^T left the dP region
         mbar_wait(&do_full[s], (g >> 1) & 1);
         tc_fence_after();
-        if (elect_one()) mma_qk_hs128(kDP, v_desc, do_desc0 + s * kSlot, C::kIdescSS, 0u);
-        __syncwarp();
+        qk(kDP, v_desc, do_desc0 + s * kSlot);
         bwd_commit(dp_full);
       }
       for (int i = 0; i < total; ++i, ++g) {
@@ -1413,7 +1434,11 @@ __global__ void __launch_bounds__(FusedCfg<HS>::kThreads, 1) fa_bwd_fused_kernel
                       (i > 0 || n4 > 0) ? 1u : 0u);
           __syncwarp();
         }
-        bwd_commit(dv_done);  // dO(g) consumed: the compute warps may write dS^T(g) over it
+        if constexpr (C::kDsInDo) {
+          bwd_commit(dv_done);  // dO(g) consumed: the compute warps may write dS^T(g) over it
+        } else {
+          bwd_commit(&do_empty[s]);  // dO(g) consumed (dS^T has its own buffer)
+        }
         // S^T(g+1) over the S region (P^T(g) is read by the dV MMAs above),
         // and dQ(g) into the dP region then dK(g) once dS^T(g) is in shared
         // memory: whichever is ready first is issued first. Q(g+1) is
@@ -1421,22 +1446,24 @@ __global__ void __launch_bounds__(FusedCfg<HS>::kThreads, 1) fa_bwd_fused_kernel
         // before dQ(g) / dK(g) would also delay dK(g) and with it Q(g+2).
         auto issue_s_next = [&] {
           tc_fence_after();
-          if (elect_one()) mma_qk_hs128(kS, k_desc, q_desc0 + s1 * kSlot, C::kIdescSS, 0u);
-          __syncwarp();
+          qk(kS, k_desc, q_desc0 + s1 * kSlot);
           bwd_commit(s_full);
           if (lane == 0) bwd_trace(p, 9, g);
         };
         auto issue_dq_dk = [&] {
           if (lane == 0) bwd_trace(p, 10, g);
           tc_fence_after();
-          if (elect_one()) mma_mn_mn_chain(kDP, do_mn0 + s * kSlot, k_mn, C::kIdescDQ, 0u);  // A = dS, B = K
+          if (elect_one()) mma_mn_mn_chain(kDP, ds_mn0 + s * kDsSlot, k_mn, C::kIdescDQ, 0u);  // A = dS, B = K
           __syncwarp();
           bwd_commit(dq_full);
           if (elect_one())
-            mma_kmaj_mn_chain(kDK, do_desc0 + s * kSlot, q_mn0 + s * kSlot, C::kIdescDK, i > 0 ? 1u : 0u);
+            mma_kmaj_mn_chain(kDK, ds_k0 + s * kDsSlot, q_mn0 + s * kSlot, C::kIdescDK, i > 0 ? 1u : 0u);
           __syncwarp();
           bwd_commit(&q_empty[s]);
-          bwd_commit(&do_empty[s]);  // the slot's dS^T has been read
+          if constexpr (C::kDsInDo)
+            bwd_commit(&do_empty[s]);  // the slot's dS^T has been read
+          else
+            bwd_commit(dv_done);  // the dS^T buffer has been read
           if (lane == 0) bwd_trace(p, 11, g);
         };
         if (!USPB_FUSED_DYN || i + 1 >= total) {
@@ -1466,8 +1493,7 @@ __global__ void __launch_bounds__(FusedCfg<HS>::kThreads, 1) fa_bwd_fused_kernel
           mbar_wait(dq_free, g & 1);
           mbar_wait(&do_full[s1], ph1);
           tc_fence_after();
-          if (elect_one()) mma_qk_hs128(kDP, v_desc, do_desc0 + s1 * kSlot, C::kIdescSS, 0u);
-          __syncwarp();
+          qk(kDP, v_desc, do_desc0 + s1 * kSlot);
           bwd_commit(dp_full);
           if (lane == 0) bwd_trace(p, 13, g);
         }
@@ -1602,15 +1628,21 @@ cudaError_t launch_bwd_dkdv(const BwdParams& p, int hs, int grid, cudaStream_t s
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_bwd_fused(const BwdParams& p, int hs, int grid, cudaStream_t stream) {
-  if (hs != 128) return cudaErrorInvalidValue;
-  using C = FusedCfg<128>;
-  auto kern = fa_bwd_fused_kernel<128>;
+template <int HS>
+static cudaError_t launch_fused_impl(const BwdParams& p, int grid, cudaStream_t stream) {
+  using C = FusedCfg<HS>;
+  auto kern = fa_bwd_fused_kernel<HS>;
   static std::atomic<uint64_t> done{0};
   const cudaError_t once = ensure_smem_attr(kern, C::kSmemBytes, done);
   if (once != cudaSuccess) return once;
   kern<<<grid, C::kThreads, C::kSmemBytes, stream>>>(p);
   return cudaGetLastError();
+}
+
+cudaError_t launch_bwd_fused(const BwdParams& p, int hs, int grid, cudaStream_t stream) {
+  if (hs == 128) return launch_fused_impl<128>(p, grid, stream);
+  if (hs == 64) return launch_fused_impl<64>(p, grid, stream);
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_bwd_delta(const void* o, const void* dout, float* delta, int64_t batch, int64_t q_len,

@@ -400,8 +400,8 @@ class UspAttention:
         return int(lib().usp_engine_a2a_chunks(self._h))
 
     def set_deterministic(self, on: bool = True) -> None:
-        """Backward algorithm: fused one-kernel (default at head size 128; dQ
-        reduced with fp32 atomics, last bits may vary run to run) or the
+        """Backward algorithm: fused one-kernel (default; dQ reduced in fp32
+        in arrival order, last bits may vary run to run) or the
         bitwise-reproducible two-kernel path (``on=True``)."""
         check(lib().usp_engine_set_deterministic(self._h, 1 if on else 0))
 

@@ -37,7 +37,7 @@ def _expected_launches(c: UspCase, det: bool) -> int:
     is counted by the engine too, so only the attention part is asserted:
     delta (1), per ring step one fused kernel (+1 add at t >= 2) or two."""
     R = c.ring
-    fused = c.hs > 64 and not det  # head sizes 65..128 run at the padded size 128
+    fused = not det
     return 1 + (R + max(0, R - 2) if fused else 2 * R)
 
 
