@@ -964,19 +964,23 @@ __global__ void __launch_bounds__(BwdCfg<HS>::kThreads, 1) fa_bwd_dkdv_kernel(co
 // Five GEMMs per (key tile, q tile) instead of the two-kernel path's seven:
 //   S^T  = K Q^T            SS -> TMEM [0,128)
 //   dP^T = V dO^T           SS -> TMEM [128,256)
-//   dV  += P^T dO           TS (P^T bf16 over consumed S^T columns) -> [256,384)
-//   dQ   = dS K             SS, both MN-major -> TMEM [128,256) (dP^T consumed)
-//   dK  += dS^T Q           SS (dS^T K-major from shared memory) -> [384,512)
+//   dV  += P^T dO           TS (P^T bf16 over consumed S^T columns) -> [256,256+HS)
+//   dQ   = dS K             SS, both MN-major -> TMEM [128,128+HS) (dP^T consumed)
+//   dK  += dS^T Q           SS (dS^T K-major from shared memory) -> [256+HS,256+2HS)
 // The compute warps store dS^T (bf16) once, into a 128B-swizzled shared tile
-// — the slot of the tile's dO, dead once the dV MMAs completed — that serves
-// as dK's K-major A and dQ's MN-major A. dQ(i) is a per-tile partial: four
+// — at head size 128 the slot of the tile's dO, dead once the dV MMAs
+// completed; at 64 a buffer of its own — that serves as dK's K-major A and
+// dQ's MN-major A. dQ(i) is a per-tile partial: four
 // drain warps (one per TMEM lane quarter, thread = q row) read all of it into
 // registers and release the dP region for dP^T(i+1), then stage it 32
 // head-dim columns at a time (4 KB per warp, 128B-swizzled, double-buffered)
 // in shared memory, from where TMA reduces it into the fp32 dQ rows
 // (cp.reduce.async.bulk.tensor .add). Per-thread red.global.add from four
 // warps sustains only ~14 B/clk/SM of the ~24 the L2 reduction path takes
-// (tools/microbench/red_rate.cu) and set a 5.6k-clk tile period.
+// (tools/microbench/red_rate.cu) and set a 5.6k-clk tile period. With a
+// key-tile pair per 2-CTA cluster (dQ pre-summed over DSMEM, or Q / dO
+// shared by multicast) and with LSU row reductions it measured slower
+// (DESIGN §4.3).
 // q tiles are walked in descending order with the group's heads innermost, so
 // the resident CTAs (consecutive key tiles of one kv head, longest first)
 // work on the same q tile together (ascending, and heads rotated per key
