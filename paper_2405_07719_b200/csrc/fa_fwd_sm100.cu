@@ -29,6 +29,9 @@
 #include "fa_fwd.hpp"
 #include "ptx_sm100.cuh"
 
+#ifndef USPB_FWD_SPLITLD
+#define USPB_FWD_SPLITLD 1  // S read from TMEM in two halves (A/B: tools/ab_fwd.py)
+#endif
 #ifndef USPB_FWD_STAGES
 #define USPB_FWD_STAGES 4  // K/V pipeline depth: measured best at 4 (2 tiles of K+V) on B200
 #endif
@@ -259,6 +262,61 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS>::kThreads, 1)
         ++s_phase;
         tc_fence_after();
         uint32_t s[KC];
+#if USPB_FWD_SPLITLD
+        // Two halves: the first half's mask and max run under the second
+        // half's TMEM load latency.
+        constexpr int KH = KC / 2;
+#pragma unroll
+        for (int c = 0; c < KH / 32; ++c) tmem_ld32(s_addr + c * 32, s + c * 32);
+#pragma unroll
+        for (int c = 0; c < KH / 32; ++c) tmem_ld_wait(s + c * 32);
+#pragma unroll
+        for (int c = KH / 32; c < KC / 32; ++c) tmem_ld32(s_addr + c * 32, s + c * 32);
+        const int4* kp4 = reinterpret_cast<const int4*>(p.k_pos + (entry & 0x7FFFFFFF) * kTileN);
+        auto mask4 = [&](int c) {  // partial tile: the position mask per element
+          const int4 kp = __ldg(kp4 + c);
+          if (kp.x > qpos) s[4 * c + 0] = __float_as_uint(-INFINITY);
+          if (kp.y > qpos) s[4 * c + 1] = __float_as_uint(-INFINITY);
+          if (kp.z > qpos) s[4 * c + 2] = __float_as_uint(-INFINITY);
+          if (kp.w > qpos) s[4 * c + 3] = __float_as_uint(-INFINITY);
+        };
+        if (entry < 0) {
+#pragma unroll
+          for (int c = 0; c < KH / 4; ++c) mask4(c);
+        }
+        float mx0 = __uint_as_float(s[0]), mx1 = __uint_as_float(s[1]);
+        float mx2 = __uint_as_float(s[2]), mx3 = __uint_as_float(s[3]);
+#pragma unroll
+        for (int i = 4; i < KH; i += 4) {
+          mx0 = fmaxf(mx0, __uint_as_float(s[i + 0]));
+          mx1 = fmaxf(mx1, __uint_as_float(s[i + 1]));
+          mx2 = fmaxf(mx2, __uint_as_float(s[i + 2]));
+          mx3 = fmaxf(mx3, __uint_as_float(s[i + 3]));
+        }
+#pragma unroll
+        for (int c = KH / 32; c < KC / 32; ++c) tmem_ld_wait(s + c * 32);
+        // S is in registers: the shared S buffer may take the next S.
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (k2)
+            mbar_arrive_cluster(mapa_shared(smem_u32(s_free), 0));
+          else
+            mbar_arrive(s_free);
+        }
+        if (tr) trace_ev(p, 1 + 5 * t, s_phase - 1, __uint_as_float(s[KC - 1]));
+        if (entry < 0) {
+#pragma unroll
+          for (int c = KH / 4; c < KC / 4; ++c) mask4(c);
+        }
+#pragma unroll
+        for (int i = KH; i < KC; i += 4) {
+          mx0 = fmaxf(mx0, __uint_as_float(s[i + 0]));
+          mx1 = fmaxf(mx1, __uint_as_float(s[i + 1]));
+          mx2 = fmaxf(mx2, __uint_as_float(s[i + 2]));
+          mx3 = fmaxf(mx3, __uint_as_float(s[i + 3]));
+        }
+#else
 #pragma unroll
         for (int c = 0; c < KC / 32; ++c) tmem_ld32(s_addr + c * 32, s + c * 32);
 #pragma unroll
@@ -294,6 +352,7 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS>::kThreads, 1)
           mx2 = fmaxf(mx2, __uint_as_float(s[i + 2]));
           mx3 = fmaxf(mx3, __uint_as_float(s[i + 3]));
         }
+#endif
         const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
         if (tr) trace_ev(p, 2 + 5 * t, s_phase - 1, mx);
         // SoftmaxState::update (attention.cpp:209-226) with a lazy rescale:
