@@ -362,6 +362,26 @@ class Engine {
 
  private:
   int ring_ctas_ = 1, reserved_sms_ = 0, a2a_ctas_ = 0, a2a_chunks_ = 1;
+  // Direct exchange over a peer-memory transport at bs = 1:
+  // the pack kernels store Q/K/V parts straight into the owning members'
+  // head-sharded buffers (no staging, no copy), and the last attention step
+  // stores O rows straight into the owners' receive buffers.
+  bool direct_a2a() const {
+    static const bool direct_ok = [] {
+      const char* e = dev_env("USP_DIRECT_A2A");
+      return !e || std::atoi(e) != 0;
+    }();
+    return direct_ok && U_ > 1 && B_ == 1 && U_ <= 16 && tr_ && tr_->peer_memory();
+  }
+  // usp_attn_fwd_host with chunked all-to-alls (fwd_host_a2a): the caller's
+  // host buffers, read by fwd()'s chunked branches
+  struct HostIo {
+    const void *q, *k, *v;
+    void* o;
+    float* lse;
+  };
+  const HostIo* hio_ = nullptr;
+  std::vector<cudaEvent_t> ev_hq_, ev_ho_;
   // a2a_steps_[0]: step 0 split in row chunks (a2a in overlap);
   // a2a_steps_[1] (R > 1): step R-1 (a2a out overlap)
   std::vector<std::vector<DevStep>> a2a_steps_;
@@ -386,6 +406,8 @@ class Engine {
     for (auto e : ev_recv_) cudaEventDestroy(e);
     for (auto e : ev_in_) cudaEventDestroy(e);
     for (auto e : ev_attn_) cudaEventDestroy(e);
+    for (auto e : ev_hq_) cudaEventDestroy(e);
+    for (auto e : ev_ho_) cudaEventDestroy(e);
     for (auto e : ev_chunk_misc_)
       if (e) cudaEventDestroy(e);
     for (auto e : ev_acc_) cudaEventDestroy(e);
@@ -429,15 +451,7 @@ class Engine {
     const void* kh = k;
     const void* vh = v;
     uint8_t* kv0 = kv0_.as<uint8_t>();
-    static const bool direct_ok = [] {
-      const char* e = dev_env("USP_DIRECT_A2A");
-      return !e || std::atoi(e) != 0;
-    }();
-    // Direct exchange over a peer-memory transport at bs = 1:
-    // the pack kernels store Q/K/V parts straight into the owning members'
-    // head-sharded buffers (no staging, no copy), and the last attention
-    // step stores O rows straight into the owners' receive buffers.
-    const bool direct = direct_ok && U_ > 1 && B_ == 1 && U_ <= 16 && tr_ && tr_->peer_memory();
+    const bool direct = direct_a2a();
     const bool chunked = !direct && a2a_chunks_ > 1;
     if (direct) {
       // -- 1. Ulysses in, fused with the pack: part m of my Q/K/V rows ->
@@ -474,16 +488,40 @@ class Engine {
       uint8_t* sq = send_.as<uint8_t>();
       uint8_t* sk = sq + U_ * q_part_;
       uint8_t* sv = sk + U_ * kv_part_;
-      batch_begin();
-      pack_heads(q, sq, H_, hl_, st);
-      pack_heads(k, sk, KV_, kvl_, st);
-      pack_heads(v, sv, KV_, kvl_, st);
-      batch_flush(st);
-      stage(st, "pack");
-      USPB_CHECK(cudaEventRecord(ev_chunk_misc_[0], st));
-      USPB_CHECK(cudaStreamWaitEvent(comm_stream_, ev_chunk_misc_[0], 0));
       const size_t qs = q_part_ / a2a_chunks_;
+      const int64_t rc = T_ / a2a_chunks_;
+      if (hio_) {
+        // host buffers (fwd_host_a2a): on h2d_stream_, K and V go up and are
+        // packed, then Q row chunk c goes up and is packed — rows
+        // [c T/C, (c+1) T/C) of the caller's shard are exactly chunk c of
+        // every member's part — so exchange c starts once its rows landed.
+        const size_t qrow = size_t(H_) * hs_ * 2, kvrow = size_t(KV_) * hs_ * 2;
+        USPB_CHECK(cudaMemcpyAsync(const_cast<void*>(k), hio_->k, T_ * kvrow, cudaMemcpyHostToDevice, h2d_stream_));
+        USPB_CHECK(cudaMemcpyAsync(const_cast<void*>(v), hio_->v, T_ * kvrow, cudaMemcpyHostToDevice, h2d_stream_));
+        batch_begin();
+        pack_heads(k, sk, KV_, kvl_, h2d_stream_);
+        pack_heads(v, sv, KV_, kvl_, h2d_stream_);
+        batch_flush(h2d_stream_);
+        for (int c = 0; c < a2a_chunks_; ++c) {
+          const size_t off = size_t(c) * rc * qrow;
+          USPB_CHECK(cudaMemcpyAsync(static_cast<uint8_t*>(const_cast<void*>(q)) + off,
+                                     static_cast<const uint8_t*>(hio_->q) + off, rc * qrow, cudaMemcpyHostToDevice,
+                                     h2d_stream_));
+          pack_heads(q, sq, H_, hl_, h2d_stream_, c * rc, (c + 1) * rc);
+          USPB_CHECK(cudaEventRecord(ev_hq_[c], h2d_stream_));
+        }
+      } else {
+        batch_begin();
+        pack_heads(q, sq, H_, hl_, st);
+        pack_heads(k, sk, KV_, kvl_, st);
+        pack_heads(v, sv, KV_, kvl_, st);
+        batch_flush(st);
+        stage(st, "pack");
+        USPB_CHECK(cudaEventRecord(ev_chunk_misc_[0], st));
+        USPB_CHECK(cudaStreamWaitEvent(comm_stream_, ev_chunk_misc_[0], 0));
+      }
       for (int c = 0; c < a2a_chunks_; ++c) {
+        if (hio_) USPB_CHECK(cudaStreamWaitEvent(comm_stream_, ev_hq_[c], 0));
         std::vector<std::vector<A2APart>> parts(c == 0 ? 3 : 1, std::vector<A2APart>(U_));
         for (int p = 0; p < U_; ++p) {
           parts[0][p] = {sq + p * q_part_ + c * qs, q_h_.as<uint8_t>() + p * q_part_ + c * qs};
@@ -620,6 +658,24 @@ class Engine {
           cudaEvent_t s0 = side_event(comm_stream_);
           tr_->all_to_all(*groups_, parts, {qs}, comm_stream_, /*overlapped=*/c + 1 < a2a_chunks_);
           side_span("a2a_out." + std::to_string(c), s0, side_event(comm_stream_));
+          if (hio_) {
+            // host buffers: chunk c's O rows are unpacked behind their
+            // exchange and go down while chunk c+1 computes; LSE (written by
+            // the attention in place) goes down after the last chunk
+            const int64_t rc = T_ / a2a_chunks_;
+            const size_t qrow = size_t(H_) * hs_ * 2;
+            unpack_heads(o_recv_.p, o, comm_stream_, 0, 0, c * rc, (c + 1) * rc);
+            if (c + 1 == a2a_chunks_) {
+              USPB_CHECK(cudaStreamWaitEvent(d2h_stream_, ev_attn_[c], 0));
+              USPB_CHECK(cudaMemcpyAsync(hio_->lse, lse, size_t(B_) * Tr_ * hl_ * sizeof(float),
+                                         cudaMemcpyDeviceToHost, d2h_stream_));
+            }
+            USPB_CHECK(cudaEventRecord(ev_ho_[c], comm_stream_));
+            USPB_CHECK(cudaStreamWaitEvent(d2h_stream_, ev_ho_[c], 0));
+            USPB_CHECK(cudaMemcpyAsync(static_cast<uint8_t*>(hio_->o) + c * rc * qrow,
+                                       static_cast<uint8_t*>(o) + c * rc * qrow, rc * qrow, cudaMemcpyDeviceToHost,
+                                       d2h_stream_));
+          }
         }
         continue;
       }
@@ -633,8 +689,10 @@ class Engine {
       USPB_CHECK(cudaStreamWaitEvent(st, ev_chunk_misc_[1], 0));
       stage(st, "a2a_out");  // exposed part: the last chunk's exchange
       record_a2a(3, q_part_);
-      unpack_heads(o_recv_.p, o, st);
-      stage(st, "unpack");
+      if (!hio_) {  // (host buffers: unpacked per chunk above)
+        unpack_heads(o_recv_.p, o, st);
+        stage(st, "unpack");
+      }
     } else if (direct_o) {
       tr_->ulysses_done(*groups_, st);  // every member's rows for me have landed
       stage(st, "a2a_out");
@@ -684,7 +742,9 @@ class Engine {
   // U = R = 1 — or all keys otherwise) waits only for them, and its O/LSE
   // rows go down on d2h_stream_. PCIe traffic then overlaps the attention of
   // the neighbouring chunks instead of adding to it (chunk_bounds() sizes the
-  // chunks so it does). Other meshes copy the whole shard around fwd().
+  // chunks so it does). A pure ring pipelines in fwd_host_ring, chunked
+  // Ulysses exchanges in fwd_host_a2a; other meshes copy the whole shard
+  // around fwd().
   void fwd_host(const void* q, const void* k, const void* v, void* o, float* lse, cudaStream_t st) {
     USPB_CHECK(cudaSetDevice(cfg_.device));
     for (const void* ptr : {q, k, v, static_cast<const void*>(o), static_cast<const void*>(lse)})
@@ -706,6 +766,10 @@ class Engine {
     const bool reshape = U_ > 1 || hs_ != hsk_;
     if (U_ == 1 && R_ > 1 && B_ == 1 && !reshape && Tr_ >= 4 * kTileM) {
       fwd_host_ring(q, k, v, o, lse, st);
+      return;
+    }
+    if (U_ > 1 && !direct_a2a() && a2a_chunks_ > 1) {
+      fwd_host_a2a(q, k, v, o, lse, st);
       return;
     }
     const std::vector<int64_t> bounds = chunk_bounds();
@@ -774,6 +838,43 @@ class Engine {
                      at(ev_chunk_out_[c]));
       std::fprintf(stderr, "drained %8.3f ms\n", at(ev_drained_));
     }
+  }
+
+  // usp_attn_fwd_host with chunked Ulysses all-to-alls (U > 1, bs 1, not
+  // the direct peer-memory exchange): fwd() itself, with the host copies
+  // woven into its chunk pipeline (hio_): K/V up and packed, then per row
+  // chunk c Q up -> pack -> exchange c -> step-0 attention of chunk c; at
+  // the last step exchange c -> unpack -> O rows down, so only the first
+  // chunk's upload and the last chunk's download are exposed. Same kernels
+  // and plans as fwd(): bitwise the device-resident results.
+  void fwd_host_a2a(const void* q, const void* k, const void* v, void* o, float* lse, cudaStream_t st) {
+    const int C = a2a_chunks_;
+    if (static_cast<int>(ev_hq_.size()) != C) {
+      for (auto e : ev_hq_) cudaEventDestroy(e);
+      for (auto e : ev_ho_) cudaEventDestroy(e);
+      ev_hq_.assign(C, nullptr);
+      ev_ho_.assign(C, nullptr);
+      for (int c = 0; c < C; ++c) {
+        USPB_CHECK(cudaEventCreateWithFlags(&ev_hq_[c], cudaEventDisableTiming));
+        USPB_CHECK(cudaEventCreateWithFlags(&ev_ho_[c], cudaEventDisableTiming));
+      }
+    }
+    // the previous call's kernels and exchanges may still use the staging
+    // and send buffers (its fwd() ended with st waiting for comm_stream_)
+    USPB_CHECK(cudaEventRecord(ev_entry_, st));
+    USPB_CHECK(cudaStreamWaitEvent(h2d_stream_, ev_entry_, 0));
+    USPB_CHECK(cudaStreamWaitEvent(d2h_stream_, ev_entry_, 0));
+    const HostIo io{q, k, v, o, lse};
+    hio_ = &io;
+    try {
+      fwd(hq_.p, hk_.p, hv_.p, ho_.p, hlse_.as<float>(), st);
+    } catch (...) {
+      hio_ = nullptr;
+      throw;
+    }
+    hio_ = nullptr;
+    USPB_CHECK(cudaEventRecord(ev_drained_, d2h_stream_));
+    USPB_CHECK(cudaStreamWaitEvent(st, ev_drained_, 0));
   }
 
   // usp_attn_fwd_host on a pure ring (U = 1, R > 1, bs 1): K and V go up
@@ -1149,13 +1250,16 @@ class Engine {
   bool batching_ = false;
   std::vector<RowPermute> batch_;
   // (b, T, heads, hs) -> [peer][b][T][heads/U][hsk]
-  void pack_heads(const void* src, void* dst, int heads, int local, cudaStream_t st) {
+  // (bs 1: rows [r0, r1) of every part only, r1 = 0 meaning all T rows)
+  void pack_heads(const void* src, void* dst, int heads, int local, cudaStream_t st, int64_t r0 = 0,
+                  int64_t r1 = 0) {
+    if (r1 == 0) r1 = T_;
     RowPermute rp;
-    rp.src = src;
-    rp.dst = dst;
+    rp.src = static_cast<const uint8_t*>(src) + size_t(r0) * heads * hs_ * 2;
+    rp.dst = static_cast<uint8_t*>(dst) + size_t(r0) * local * hsk_ * 2;
     rp.dims[0] = U_;
     rp.dims[1] = B_;
-    rp.dims[2] = T_;
+    rp.dims[2] = r1 - r0;
     rp.dims[3] = local;
     rp.src_stride[0] = local;
     rp.src_stride[1] = T_ * heads;
@@ -1226,15 +1330,17 @@ class Engine {
     permute(rp, st);
   }
   // [src][b][T][local][hsk] -> (b, T, heads, hs), heads [src*local, (src+1)*local)
-  void unpack_heads(const void* src, void* dst, cudaStream_t st, int heads = 0, int local = 0) {
+  void unpack_heads(const void* src, void* dst, cudaStream_t st, int heads = 0, int local = 0, int64_t r0 = 0,
+                    int64_t r1 = 0) {
     if (!heads) heads = H_;
     if (!local) local = hl_;
+    if (r1 == 0) r1 = T_;
     RowPermute rp;
-    rp.src = src;
-    rp.dst = dst;
+    rp.src = static_cast<const uint8_t*>(src) + size_t(r0) * local * hsk_ * 2;
+    rp.dst = static_cast<uint8_t*>(dst) + size_t(r0) * heads * hs_ * 2;
     rp.dims[0] = U_;
     rp.dims[1] = B_;
-    rp.dims[2] = T_;
+    rp.dims[2] = r1 - r0;
     rp.dims[3] = local;
     rp.src_stride[0] = B_ * T_ * local;
     rp.src_stride[1] = T_ * local;

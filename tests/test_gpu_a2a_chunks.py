@@ -89,3 +89,50 @@ def test_default_chunks_and_ledger(cuda):
         odd.set_a2a_chunks(2)
     ok.close()
     odd.close()
+
+
+@pytest.mark.parametrize("u,r,chunks", [(2, 1, 2), (4, 1, 4), (2, 2, 2), (4, 2, 2), (2, 1, 1)])
+def test_host_buffers_pipelined_bitwise(cuda, u, r, chunks):
+    """usp_attn_fwd_host with chunked exchanges (engine.cu fwd_host_a2a):
+    Q rows go up, are packed and exchanged per chunk, O rows are unpacked and
+    go down per chunk — the same kernels and plans as the device-resident
+    forward, so O and LSE must be bitwise equal to it (chunks = 1: the
+    whole-shard copy path, as a control). Every rank calls from its own
+    Python thread (ctypes releases the GIL), as the in-process world needs."""
+    import threading
+
+    c = UspCase(seq=4096, hc=32, kv_hc=8, hs=128, ulysses=u, ring=r, causal=True, seed=29 + u + r)
+    q, k, v = make_globals(c)
+    tq, tk, tv = (to_bf16(x, cuda) for x in (q, k, v))
+
+    def setup(engines):
+        for e in engines:
+            e.set_a2a_chunks(chunks)
+
+    out, lses, engines, _ = run_usp_gpu(c, tq, tk, tv, cuda, setup=setup)
+    pos = [torch.tensor(e.positions(), dtype=torch.long, device=cuda) for e in engines]
+    pin = lambda t: t.cpu().pin_memory()  # noqa: E731
+    hin = [(pin(tq[:, p]), pin(tk[:, p]), pin(tv[:, p])) for p in pos]
+    hout = [(torch.full(tq[:, p].shape, float("nan"), dtype=torch.bfloat16).pin_memory(),
+             torch.full(lses[i].shape, float("nan"), dtype=torch.float32).pin_memory()) for i, p in enumerate(pos)]
+    errs = []
+
+    def rank(i):
+        try:
+            for _ in range(2):  # the second call reuses staging buffers and events
+                engines[i].forward_host(*hin[i], *hout[i])
+            torch.cuda.synchronize(cuda)
+        except Exception as e:  # noqa: BLE001
+            errs.append(f"rank {i}: {e!r}")
+
+    th = [threading.Thread(target=rank, args=(i,)) for i in range(len(engines))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not errs and not any(t.is_alive() for t in th), errs
+    for i, p in enumerate(pos):
+        oh, lh = hout[i]
+        assert torch.equal(oh.view(torch.int16), out[:, p].cpu().view(torch.int16)), (i, chunks)
+        assert torch.equal(lh.view(torch.int32), lses[i].cpu().view(torch.int32)), (i, chunks)
+        assert engines[i].a2a_chunks == chunks
