@@ -12,7 +12,8 @@
 //   * NQ = 2 query tiles per CTA = two q heads of the same GQA group over the
 //     same rows, so every K/V tile staged in shared memory feeds both, and
 //     the tensor core alternates between the tiles while the other's
-//     softmax runs (S_A/P_A, S_B/P_B, O_A, O_B fill the 512 TMEM columns);
+//     softmax runs (one shared S, P_A, P_B, O_A, O_B fill the 512 TMEM
+//     columns at head size 128);
 //   * S = Q K^T: tcgen05.mma SS (Q, K from 128B-swizzled smem via TMA) into
 //     TMEM; P = exp2(S*scale*log2e - m) is written back over S as bf16 and
 //     O += P V runs as a TS MMA (P from TMEM, V MN-major from smem);

@@ -91,8 +91,10 @@ def test_default_chunks_and_ledger(cuda):
     odd.close()
 
 
-@pytest.mark.parametrize("u,r,chunks", [(2, 1, 2), (4, 1, 4), (2, 2, 2), (4, 2, 2), (2, 1, 1)])
-def test_host_buffers_pipelined_bitwise(cuda, u, r, chunks):
+@pytest.mark.parametrize("u,r,chunks,hs,causal", [(2, 1, 2, 128, True), (4, 1, 4, 128, True), (2, 2, 2, 128, True),
+                                                   (4, 2, 2, 128, True), (2, 1, 1, 128, True), (2, 2, 2, 64, True),
+                                                   (4, 1, 2, 128, False)])
+def test_host_buffers_pipelined_bitwise(cuda, u, r, chunks, hs, causal):
     """usp_attn_fwd_host with chunked exchanges (engine.cu fwd_host_a2a):
     Q rows go up, are packed and exchanged per chunk, O rows are unpacked and
     go down per chunk — the same kernels and plans as the device-resident
@@ -101,7 +103,7 @@ def test_host_buffers_pipelined_bitwise(cuda, u, r, chunks):
     Python thread (ctypes releases the GIL), as the in-process world needs."""
     import threading
 
-    c = UspCase(seq=4096, hc=32, kv_hc=8, hs=128, ulysses=u, ring=r, causal=True, seed=29 + u + r)
+    c = UspCase(seq=4096, hc=32, kv_hc=8, hs=hs, ulysses=u, ring=r, causal=causal, seed=29 + u + r)
     q, k, v = make_globals(c)
     tq, tk, tv = (to_bf16(x, cuda) for x in (q, k, v))
 
