@@ -33,6 +33,9 @@
 #ifndef USPB_FWD_SPLITLD
 #define USPB_FWD_SPLITLD 1  // S read from TMEM in two halves (A/B: tools/ab_fwd.py)
 #endif
+#ifndef USPB_FWD_POLY64
+#define USPB_FWD_POLY64 2  // head size 64: exponential pairs of every 8 computed on the FMA pipe
+#endif
 #ifndef USPB_FWD_STAGES
 #define USPB_FWD_STAGES 4  // K/V pipeline depth: measured best at 4 (2 tiles of K+V) on B200
 #endif
@@ -372,12 +375,25 @@ __global__ void __launch_bounds__(FwdCfg<NQ, HS>::kThreads, 1)
         // of s[] is rewritten only after s[2i], s[2i+1] were consumed.
         const float2 sc2 = make_float2(sl2, sl2), nb2 = make_float2(neg, neg);
         float2 acc2 = make_float2(0.f, 0.f);
+        constexpr int kPolyPairs = HS == 64 ? USPB_FWD_POLY64 : 0;
 #pragma unroll
         for (int i = 0; i < KC / 2; ++i) {
           const float2 x = ffma2(make_float2(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), sc2, nb2);
           float2 e;
-          e.x = ex2(x.x);
-          e.y = ex2(x.y);
+          if constexpr (kPolyPairs > 0) {
+            // head size 64: the MUFU, not the tensor pipe, bounds the step
+            // (2048 clk of exponentials vs 1024 of MMA per key tile), so
+            // kPolyPairs of every 8 pairs go to the FMA pipe instead
+            if (i % 8 < kPolyPairs) {
+              e = exp2_poly2(x);
+            } else {
+              e.x = ex2(x.x);
+              e.y = ex2(x.y);
+            }
+          } else {
+            e.x = ex2(x.x);
+            e.y = ex2(x.y);
+          }
           acc2 = fadd2(acc2, e);
           // one F2FP (cvt.rn.bf16x2.f32) per pair: it does NOT share the
           // MUFU pipe on sm_100 (round 1 assumed so and packed on the integer

@@ -605,21 +605,34 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
       : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
   return d;
 }
-// 2^x on the FMA pipe for a pair (x <= ~126, clamped below at -127):
-// 2^x = 2^round(x) * p(r), r = x - round(x) in [-0.5, 0.5], p a degree-3
-// minimax polynomial (max rel. error 7.7e-5, below bf16's 3.9e-3). Offloads
-// a fraction of the softmax exponentials from the 16/clk/SM MUFU unit.
+__device__ __forceinline__ float2 fadd2_rm(float2 a, float2 b) {  // rounded toward -inf
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\t"
+      "mov.b64 rb, {%4, %5};\n\t"
+      "add.rm.f32x2 rd, ra, rb;\n\t"
+      "mov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+// 2^x for a pair on the FMA pipe (x <= 126): 2^x = 2^floor(x) * p(f),
+// f = x - floor(x) in [0, 1), p a degree-3 polynomial with p(0) = 1 exactly
+// (max rel. error 8.8e-5, below bf16's 3.9e-3). x is clamped at -127, where
+// f = 0 and the exponent arithmetic gives exactly +0 — what ex2.approx.ftz
+// returns for masked (-inf) scores. Offloads a fraction of the softmax
+// exponentials from the 16/clk/SM MUFU unit.
 __device__ __forceinline__ float2 exp2_poly2(float2 x) {
   x.x = fmaxf(x.x, -127.f);
   x.y = fmaxf(x.y, -127.f);
   const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
-  const float2 t = fadd2(x, magic);                           // round(x) in the low bits
-  const float2 f = fadd2(t, make_float2(-12582912.f, -12582912.f));
-  const float2 r = fadd2(x, make_float2(-f.x, -f.y));
-  float2 p = ffma2(make_float2(0.05508876592f, 0.05508876592f), r,
-                   make_float2(0.24260465801f, 0.24260465801f));
-  p = ffma2(p, r, make_float2(0.69327628613f, 0.69327628613f));
-  p = ffma2(p, r, make_float2(0.99992889166f, 0.99992889166f));
+  const float2 t = fadd2_rm(x, magic);                        // floor(x) in the low mantissa bits
+  const float2 j = fadd2(t, make_float2(-12582912.f, -12582912.f));  // floor(x), exact
+  const float2 f = ffma2(j, make_float2(-1.f, -1.f), x);             // x - floor(x), exact
+  float2 p = ffma2(make_float2(0.077119089663028717f, 0.077119089663028717f), f,
+                   make_float2(0.227564394474029541f, 0.227564394474029541f));
+  p = ffma2(p, f, make_float2(0.695146143436431885f, 0.695146143436431885f));
+  p = ffma2(p, f, make_float2(1.f, 1.f));
   const uint32_t bx = __float_as_uint(p.x) + (__float_as_uint(t.x) << 23);
   const uint32_t by = __float_as_uint(p.y) + (__float_as_uint(t.y) << 23);
   return make_float2(__uint_as_float(bx), __uint_as_float(by));

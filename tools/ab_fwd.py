@@ -75,6 +75,8 @@ def main():
         shapes = shapes[:1]
     elif os.environ.get("AB_SHAPES") == "bwd":
         shapes = shapes[:2]
+    elif os.environ.get("AB_SHAPES") == "hs64":
+        shapes = [(32768, 64, 8, 8, 1), (32768, 64, 32, 8, 1), (131072, 64, 32, 8, 1), (32768, 64, 8, 8, 0)]
     for rnd in range(int(os.environ.get("AB_ROUNDS", "2"))):
         for sh in shapes:
             for var in variants:
