@@ -89,10 +89,6 @@ __device__ __forceinline__ void bwd_commit(uint64_t* bar) {
   __syncwarp();
 }
 
-__device__ __forceinline__ void bwd_bar_sync(uint32_t id, uint32_t count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-
 #ifndef USPB_BWD_F2FP
 #define USPB_BWD_F2FP 1  // F2FP packing: +3 % (839 -> 865 TFLOP/s at 128K, A/B)
 #endif
@@ -1212,7 +1208,6 @@ __global__ void __launch_bounds__(FusedCfg<HS>::kThreads, 1) fa_bwd_fused_kernel
         float4 dv1[8];
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
-          const int c = 2 * hf + cc;
           const uint32_t* dp = dp2 + 32 * cc;
           uint32_t* pd = pd2[cc];
 #pragma unroll
