@@ -4,10 +4,11 @@ chunk hand-offs or the ring's double buffers): every unit's arithmetic is
 independent of which CTA claims it. Longer runs: tools/stress.py.
 
 The backward is bitwise repeatable in its deterministic mode
-(UspAttention.set_deterministic). The default fused backward reduces dQ
-partials with fp32 atomics in arrival order: its dK / dV (and the forward)
-are still bit-identical run to run, its dQ agrees to fp32 summation-order
-noise."""
+(UspAttention.set_deterministic: the two-kernel path, every dQ / dK / dV
+tile summed by one CTA in a fixed order), whichever CTA runs which unit and
+however many CTAs there are. The default fused backward reduces dQ
+partials in arrival order: its dK / dV (and the forward) are still
+bit-identical run to run, its dQ agrees to fp32 summation-order noise."""
 import pytest
 import torch
 
@@ -69,3 +70,24 @@ def test_fused_backward_repeatable(cuda, L, hc, kv):
         gr = eng.backward(f, do)
         assert torch.equal(gr.dk, dk0) and torch.equal(gr.dv, dv0)
         assert float((gr.dq.float() - dq0.float()).abs().max()) <= 1e-2 * scale
+
+
+@pytest.mark.parametrize("hs", [128, 64])
+def test_deterministic_dq_independent_of_grid(cuda, hs):
+    """Deterministic mode: dQ / dK / dV bit-identical when the grid shrinks
+    (reserved SMs change which CTA runs which unit and when)."""
+    L, hc, kv = 4096, 8, 2
+    eng = UspAttention(ProcessMesh(1, 1), rank=0, seq_len=L, heads=hc, kv_heads=kv, head_size=hs, causal=True)
+    eng.set_deterministic(True)
+    g = torch.Generator(device=cuda).manual_seed(hs)
+    q = torch.randn(eng.q_shape(), device=cuda, dtype=torch.bfloat16, generator=g)
+    k = torch.randn(eng.kv_shape(), device=cuda, dtype=torch.bfloat16, generator=g)
+    v = torch.randn(eng.kv_shape(), device=cuda, dtype=torch.bfloat16, generator=g)
+    do = torch.randn(eng.q_shape(), device=cuda, dtype=torch.bfloat16, generator=g)
+    f = eng.forward(q, k, v)
+    ref = eng.backward(f, do)
+    ref = [ref.dq.clone(), ref.dk.clone(), ref.dv.clone()]
+    for reserve in (1, 37, 100, 140):
+        eng.set_reserved_sms(reserve)
+        gr = eng.backward(f, do)
+        assert all(torch.equal(a, b) for a, b in zip((gr.dq, gr.dk, gr.dv), ref)), reserve

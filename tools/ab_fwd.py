@@ -35,6 +35,7 @@ def child(L, hs, hc, kv, causal):
     iters = max(5, int(6e11 / (L * L)))
     bwd = os.environ.get("AB_BWD") == "1"
     if bwd:
+        eng.set_deterministic(os.environ.get("AB_DET") == "1")
         fwd = eng.forward(q, k, v, o, lse)
         do = u(eng.q_shape())
         dq, dk, dv = eng.alloc_grads()
