@@ -82,6 +82,8 @@ def parse():
     ap.add_argument("--cpu-sample-len", type=int, default=4096)
     ap.add_argument("--skip-cpu-baseline", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-backward", action="store_true")
+    ap.add_argument("--bwd-steps", type=int, default=3, help="timed steps of the backward report (both modes)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--parity-rows", type=int, default=12, help="sampled query rows checked vs the fp64 oracle")
     ap.add_argument("--parity-ref-rows", type=int, default=4,
@@ -566,6 +568,37 @@ def run_ours(a):
                "path": "paper_2405_07719_b200.UspAttention.forward_host -> usp_attn_fwd_host (C ABI, pinned host "
                        "buffers; H2D/D2H pipelined against the attention in sequence chunks at U=R=1)"}
 
+    # ---- backward of the same workload, reported beside
+    # the forward metric: algorithmic FLOPs = 2.5 x the forward's (five
+    # GEMM-equivalents of the forward's two), device time, max over ranks
+    backward = None
+    if not a.skip_backward:
+        fwd = eng.forward(q, k, v, o, lse, stream)
+        gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+        dout = (torch.rand(q.shape, device=dev, generator=gen) * 2 - 1).to(torch.bfloat16)
+        dq, dk, dv = eng.alloc_grads()
+        backward = {"unit": UNIT, "flop_factor": 2.5, "steps": a.bwd_steps}
+        for mode, det in (("fused", False), ("deterministic", True)):
+            eng.set_deterministic(det)
+            eng.backward(fwd, dout, dq, dk, dv, stream)  # warm-up (plans for this mode)
+            torch.cuda.synchronize(dev)
+            barrier()
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            b0.record(stream)
+            for _ in range(a.bwd_steps):
+                eng.backward(fwd, dout, dq, dk, dv, stream)
+            b1.record(stream)
+            torch.cuda.synchronize(dev)
+            barrier()
+            bms = max_over_ranks(b0.elapsed_time(b1) / a.bwd_steps)
+            backward[mode] = {"value": 2.5 * total_flops / (bms * 1e-3) / 1e12, "ms_per_step": bms,
+                              "launches_per_step": eng.last_launches()}
+        eng.set_deterministic(False)
+        backward["value"] = backward["fused"]["value"]
+        backward["kernel"] = ("fused: fa_bwd_fused_kernel (one launch per ring step, dQ TMA-reduced in fp32); "
+                              "deterministic: fa_bwd_dkdv_kernel + fa_bwd_dq_kernel")
+        del fwd, dout, dq, dk, dv
+
     bw = nccl_bandwidth(dev, world, U, R, rank, same_dev) if distributed else None
     whole = whole_forward_roofline(eng, U, R, ms, peak, bw)
 
@@ -594,7 +627,7 @@ def run_ours(a):
             "pct_of_peak_per_gpu": value / n / peak * 100.0,
             "tokens_per_s": a.seq_len / (ms * 1e-3),
             "roofline": roofline, "whole_forward": whole, "stages_ms_per_step": stages, "parity": parity,
-            "cpu_baseline": cpu, "clocks": clk, "e2e": e2e,
+            "cpu_baseline": cpu, "clocks": clk, "e2e": e2e, "backward": backward,
             "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)

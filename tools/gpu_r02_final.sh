@@ -13,7 +13,7 @@ head -c 300 gpurun_out/${TAG}_bench.json; echo
 timeout 900 python bench.py --impl reference > gpurun_out/${TAG}_bench_reference.json 2> gpurun_out/${TAG}_bench_reference.err
 head -c 300 gpurun_out/${TAG}_bench_reference.json; echo
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-   --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --skip-cpu-baseline --skip-e2e > /dev/null 2>&1
+   --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --skip-cpu-baseline --skip-e2e --skip-backward > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:fa_fwd -s 1 -c 1 \
    -o gpurun_out/${TAG}_fa python tools/profile_target.py 131072 2 > gpurun_out/${TAG}_ncu_fa.log 2>&1
 tail -1 gpurun_out/${TAG}_ncu_fa.log
