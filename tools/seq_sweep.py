@@ -2,7 +2,7 @@
 """Forward and backward throughput across sequence lengths at the Llama-3-8B
 layer shape (hc 32 / kv 8 / hs 128, causal, U = R = 1; development aid).
 Prints one JSON line per length; uniform [-1, 1) inputs as the bench.
-    python tools/seq_sweep.py [L ...]"""
+    python tools/seq_sweep.py [L ...]        (SWEEP_HS=64: head size 64)"""
 import json
 import os
 import sys
@@ -30,7 +30,8 @@ def timed(fn, iters):
 
 def run(L):
     dev = torch.device("cuda", 0)
-    eng = UspAttention(ProcessMesh(1, 1), rank=0, seq_len=L, heads=32, kv_heads=8, head_size=128, causal=True)
+    hs = int(os.environ.get("SWEEP_HS", "128"))
+    eng = UspAttention(ProcessMesh(1, 1), rank=0, seq_len=L, heads=32, kv_heads=8, head_size=hs, causal=True)
     g = torch.Generator(device=dev).manual_seed(L)
     u = lambda s: (torch.rand(s, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)  # noqa: E731
     q, k, v, do = u(eng.q_shape()), u(eng.kv_shape()), u(eng.kv_shape()), u(eng.q_shape())
@@ -45,7 +46,7 @@ def run(L):
     bms = timed(lambda: eng.backward(fwd, do, dq, dk, dv), max(2, iters // 3))
     c = clk.stop()
     F = eng.flops()
-    out = {"L": L, "fwd_ms": round(fms, 3), "fwd_tflops": round(F / fms / 1e9, 1), "bwd_ms": round(bms, 3),
+    out = {"L": L, "hs": hs, "fwd_ms": round(fms, 3), "fwd_tflops": round(F / fms / 1e9, 1), "bwd_ms": round(bms, 3),
            "bwd_tflops_algorithmic": round(2.5 * F / bms / 1e9, 1), "sm_mhz": c["sm_mhz"], "reasons": c["reasons"]}
     eng.close()
     return out
