@@ -83,6 +83,9 @@ def parse():
     ap.add_argument("--skip-cpu-baseline", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-backward", action="store_true")
+    ap.add_argument("--backward-multi", action="store_true",
+                    help="also report the backward when N > 1 (default: N = 1 only; the multi-GPU NCCL backward "
+                         "has no one-GPU test, so the scaling runs do not depend on it)")
     ap.add_argument("--bwd-steps", type=int, default=3, help="timed steps of the backward report (both modes)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--parity-rows", type=int, default=12, help="sampled query rows checked vs the fp64 oracle")
@@ -572,7 +575,7 @@ def run_ours(a):
     # the forward metric: algorithmic FLOPs = 2.5 x the forward's (five
     # GEMM-equivalents of the forward's two), device time, max over ranks
     backward = None
-    if not a.skip_backward:
+    if not a.skip_backward and (not distributed or a.backward_multi):
         fwd = eng.forward(q, k, v, o, lse, stream)
         gen = torch.Generator(device=dev).manual_seed(1234 + rank)
         dout = (torch.rand(q.shape, device=dev, generator=gen) * 2 - 1).to(torch.bfloat16)

@@ -49,7 +49,7 @@ def test_bench_one_gpu(cuda):
 
 
 def test_bench_two_ranks_self_launched(cuda):
-    d = _run(["--gpus", "2"] + SMALL, env={"USP_BENCH_SAME_DEVICE": "1"})
+    d = _run(["--gpus", "2", "--backward-multi"] + SMALL, env={"USP_BENCH_SAME_DEVICE": "1"})
     _check_line(d, 2)
     assert d["config"]["parallelism"] == "u1r2"
 
